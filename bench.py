@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the Kernel K-means hot path (BASELINE.json metric: sec/iteration and total
+clustering time, % of roofline).
+
+  python bench.py --gpus N --steps K --warmup W [--impl ours|reference]
+
+A step is one whole clustering run of the hot path (all SURVEY §8(a) rows): kkm_init
+(X resident on the device -> norms, bf16 split, diag, K = kappa(X X^T) materialised) and
+kkm_fit (max_iter iterations of a2 SpMM, a3 cnorm/J, a4 distances/argmin/sizes, with the
+1D exchange steps when N > 1) -> labels resident on the device. Workload: BASELINE.json
+configs[1] (MNIST-shaped n=60000, d=784, k=10, poly(1,1,2), K materialised, 100 iterations
+per P:639), synthetic and seeded (synth/). N > 1 shards the same n over N GPUs (strong
+scaling). Inputs are far larger than L2 (K = 14.4 GB is streamed every iteration).
+
+--impl reference runs the fp64 CPU oracle (oracle/) as it stands on the host cores on a
+bounded row sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+WORKLOAD = "mnist60k"
+METRIC = "sec/iteration"
+
+
+def workload_desc(cfg, iters):
+    return (f"{WORKLOAD}: MNIST-shaped synthetic n={cfg['n']} d=784 k={cfg['k']} "
+            f"poly(gamma=1,c=1,deg=2), K materialised, {iters} iterations (BASELINE.json configs[1])")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def cores():
+    return len(os.sched_getaffinity(0))
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline)
+def oracle_sample(X, cfg, rows_n=1024, seed=0):
+    """Bounded sample of the same workload on the fp64 oracle: exact K rows for `rows_n`
+    random rows (a1) and one E / c / D / argmin pass over them (a2-a4), extrapolated to n."""
+    import oracle
+    n, k = X.shape[0], cfg["k"]
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    rows = np.sort(np.random.default_rng(seed).choice(n, rows_n, replace=False))
+    labels = oracle.round_robin(n, k)
+    t0 = time.perf_counter()
+    Kr = oracle.kernel_rows(X, rows, *args)
+    t1 = time.perf_counter()
+    E = oracle.E_rows(Kr, labels, k)
+    diag = oracle.kernel_diag(X, *args, rows=rows)
+    cn = np.array([E[labels[rows] == c, c].mean() if (labels[rows] == c).any() else 0.0
+                   for c in range(k)])
+    oracle.assign(E, diag, cn)
+    t2 = time.perf_counter()
+    per_iter = (t2 - t1) * n / rows_n
+    k_build = (t1 - t0) * n / rows_n
+    return dict(sec_per_iter=per_iter, k_build_s=k_build, wall_s=t2 - t0, rows=rows_n)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    X, cfg = synth.make_config(WORKLOAD)
+    iters = args.iters or cfg["iters"]
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores()))
+    for _ in range(args.warmup):
+        oracle_sample(X, cfg, args.ref_rows)
+    samples = [oracle_sample(X, cfg, args.ref_rows, seed=s) for s in range(args.steps)]
+    spi = statistics.mean(s["sec_per_iter"] for s in samples)
+    kb = statistics.mean(s["k_build_s"] for s in samples)
+    total = kb + iters * spi
+    sample = (f"{args.ref_rows} of {cfg['n']} rows per step: exact fp64 K rows + one E/c/D/argmin "
+              f"pass, extrapolated x n/{args.ref_rows} (OMP threads={os.environ['OMP_NUM_THREADS']})")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": spi, "unit": "s/iteration",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(s["wall_s"] for s in samples),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "total_clustering_s": total,
+        "config": {"workload": workload_desc(cfg, iters), "n": cfg["n"], "d": 784, "k": cfg["k"],
+                   "iterations": iters, "parallelism": "cpu-oracle"},
+        "cpu_baseline": {"value": spi, "unit": "s/iteration", "cores": cores(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": spi, "unit": "s/iteration", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({nm for r in self.rows for nm, v in zip(names, r[4:8]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_17136_b200 as kkm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = None
+    if world > 1:
+        uid = [kkm.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = kkm.comm_init(world, rank, uid[0])
+
+    cfg = dict(synth.CONFIGS[WORKLOAD])
+    n, k = cfg["n"], cfg["k"]
+    iters = args.iters or cfg["iters"]
+    r0, r1 = kkm.shard_begin(n, rank, world), kkm.shard_begin(n, rank + 1, world)
+    X_local = synth.mnist_like(n, cfg["seed"], row_begin=r0, row_end=r1)
+    d = X_local.shape[1]
+    precision = {"bf16x3": kkm.PREC_BF16X3, "fp32": kkm.PREC_FP32_SIMT}[args.precision]
+    kw = dict(kind=cfg["kind"], gamma=1.0, coef0=1.0, degree=2, max_iter=iters,
+              precision=precision, rank=rank, nranks=world, comm=comm, timing=True)
+    p = kkm.default_params()
+    p.kind, p.k, p.max_iter, p.precision = cfg["kind"], k, iters, precision
+    ws = torch.empty(kkm.workspace_size(p, n, d, rank, world), dtype=torch.uint8, device=dev)
+    Xd = torch.from_numpy(X_local).to(dev)
+    Xh = torch.from_numpy(X_local).pin_memory()
+    lab_h = torch.empty(n, dtype=torch.int32).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def one_step(X_src, lab_dst=None):
+        h = kkm.KernelKMeans(X_src, n, k, workspace=ws, stream=stream, **kw)
+        it, J, ch = h.fit()
+        if lab_dst is not None:
+            h.assign(lab_dst)
+        ph, nl = h.phase_ms(), h.launch_count()
+        h.destroy()
+        return it, J, ph, nl
+
+    for _ in range(args.warmup):
+        one_step(Xd)
+    barrier()
+
+    # ---- timed region: K steps, X resident in HBM
+    phases, launches, J_last = [], 0, None
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            it, J, ph, nl = one_step(Xd)
+            phases.append(ph)
+            launches += nl
+            J_last = J
+        ev1.record(stream)
+        barrier()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    clocks = clk.summary()
+
+    # ---- e2e: the same through the C-ABI with HOST buffers (H2D of X, D2H of labels inside)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step(Xh, lab_h)
+    e1.record(stream)
+    barrier()
+    e2e_step_ms = e0.elapsed_time(e1) / args.steps
+
+    ph_mean = {key: statistics.mean(p_[key] for p_ in phases) for key in phases[0]}
+    loop_ms = ph_mean["spmm"] + ph_mean["cnorm"] + ph_mean["assign"]
+    vals = torch.tensor([step_ms, e2e_step_ms, loop_ms / iters, ph_mean["spmm"] / iters,
+                         ph_mean["init_gemm"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    step_ms, e2e_step_ms, iter_ms, spmm_ms, gemm_ms = vals.tolist()
+
+    if rank == 0:
+        peaks, peak_kind = measured_peaks()
+        B = -(-n // world)
+        nloc = min(B, n - 0)
+        ldk = -(-n // 32) * 32
+        spmm_bytes = nloc * ldk * 4 + ldk * 4 + nloc * k * 8  # K block + labels + S partials
+        spmm_gbs = spmm_bytes / (spmm_ms * 1e-3) / 1e9
+        gemm_flops = 2.0 * nloc * n * d
+        gemm_tfs = gemm_flops / (gemm_ms * 1e-3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("bytes_per_launch")
+        gemm_peak = peaks["bf16_tflops"] / 3.0 if precision == kkm.PREC_BF16X3 else 148 * 128 * 2 * 1.965e9 / 1e12
+        line = {
+            "metric": METRIC, "value": iter_ms / 1e3, "unit": "s/iteration",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "total_clustering_s": step_ms / 1e3,
+            "config": {"workload": workload_desc(cfg, iters), "n": n, "d": d, "k": k,
+                       "iterations": iters, "precision_a1": args.precision,
+                       "parallelism": f"1D row shards x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (14.4/N GB of K streamed per iteration)"},
+            "roofline": {"kernel": "spmm_onehot (a2)", "bound": "hbm", "achieved": spmm_gbs,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": spmm_gbs / peaks["hbm_gbs"],
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "bytes_per_launch": spmm_bytes, "launch_ms": spmm_ms},
+            "roofline_a1": {"kernel": f"gemm ({args.precision}) + kappa", "bound": "tensor"
+                            if precision == kkm.PREC_BF16X3 else "alu",
+                            "achieved": gemm_tfs, "peak": gemm_peak, "unit": "TFLOP/s",
+                            "frac": gemm_tfs / gemm_peak, "flops_per_launch": gemm_flops,
+                            "launch_ms": gemm_ms},
+            "phases_ms_per_step": ph_mean,
+            "e2e": {"value": e2e_step_ms / 1e3 / iters, "unit": "s/iteration (amortised: H2D X + K build + loop + D2H labels)",
+                    "total_clustering_s": e2e_step_ms / 1e3,
+                    "h2d_bytes_per_step": int(X_local.nbytes), "d2h_bytes_per_step": int(n * 4)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "final_J": float(J_last[-1]),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            X, full_cfg = synth.make_config(WORKLOAD)
+            s = oracle_sample(X, full_cfg, args.ref_rows)
+            line["cpu_baseline"] = {
+                "value": s["sec_per_iter"], "unit": "s/iteration", "cores": cores(), "kind": "oracle",
+                "sample": (f"{args.ref_rows} of {n} rows: exact fp64 K rows + one E/c/D/argmin pass, "
+                           f"extrapolated x n/{args.ref_rows}; K build extrapolated {s['k_build_s']:.1f} s"),
+                "total_clustering_s": s["k_build_s"] + iters * s["sec_per_iter"]}
+        print(json.dumps(line), flush=True)
+
+    if comm:
+        kkm.comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--iters", type=int, default=0, help="override iterations per step")
+    ap.add_argument("--precision", choices=["bf16x3", "fp32"], default="bf16x3")
+    ap.add_argument("--ref-rows", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+    sys.exit(run_reference(args) if args.impl == "reference" else run_ours(args))
+
+
+if __name__ == "__main__":
+    main()

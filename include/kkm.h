@@ -1,0 +1,189 @@
+/*
+ * kkm.h -- C-ABI of the B200-native exact Kernel K-means hot path.
+ *
+ * Method: arXiv 2601.17136 ("PAPER.md"), §2.2. One clustering
+ * iteration computes, for the current assignment cl(.) and its n x k
+ * indicator V (Eq. v, V(c,j) = 1/|L_c| if cl(j) = c):
+ *   (a1) K = kappa(P P^T)               Eqs. (b), (k)
+ *   (a2) E = K V^T                      Eq.  (e)
+ *   (a3) z(i) = E(i, cl(i)); c = V z    Eqs. (z), (c)
+ *   (a4) D = -2E + C~; cl <- argmin_c D(i, c); V <- V(cl)   Eq. (d)
+ * in a loop (Alg. 1). All arithmetic runs in the CUDA kernels of
+ * libkkm.so (sm_100a); this header and the ctypes binding only marshal.
+ *
+ * Conventions
+ *   - Every function returns an int status (KKM_OK = 0); on failure
+ *     kkm_last_error() returns a thread-local message. After KKM_ECUDA or
+ *     KKM_ENCCL a handle is poisoned: destroy it (and abort the communicator).
+ *   - Handles are not thread-safe; use one handle per (rank, stream).
+ *   - "device" pointers are CUDA global memory of the current device;
+ *     pointers documented "host or device" are classified with
+ *     cudaPointerGetAttributes and copied with cudaMemcpyAsync on the handle's
+ *     stream (pinned host memory is the fast path).
+ *   - Matrices are row-major. n = number of points, d = features, k = clusters.
+ *   - Multi-GPU: ranks own contiguous point blocks [kkm_shard_begin(r),
+ *     kkm_shard_begin(r+1)), the paper's 1D column blocks of K (
+ *     K is symmetric so row blocks of K are its column blocks). Collective
+ *     functions must be called by every rank of the communicator.
+ * Readings of the paper that the semantics depend on:
+ *   A1 Gaussian kernel exp(-gamma ||x-y||^2); A3 distances add K(i,i);
+ *   A4 fixed max_iter (+ optional stop when nothing changes); A5 round-robin
+ *   init cl(j) = j mod k on the global index; A6 lowest cluster index wins
+ *   ties; A7 empty clusters get +inf distance and stay empty; A8 objective
+ *   J = tr K - sum_c |L_c| ||mu_c||^2; A14 iteration t uses the labels entering it.
+ */
+#ifndef KKM_H
+#define KKM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define KKM_OK 0
+#define KKM_EINVAL 1  /* bad argument (sizes, params, null pointer, rank range)  */
+#define KKM_ELABEL 2  /* an init / set label is outside [0, k)                  */
+#define KKM_ENOMEM 3  /* workspace too small, or MATERIALIZE does not fit         */
+#define KKM_EUNSUP 4  /* valid but unsupported combination                       */
+#define KKM_ECUDA 5   /* CUDA runtime/driver error (handle poisoned)             */
+#define KKM_ENCCL 6   /* NCCL error (handle poisoned)                           */
+#define KKM_ESTATE 7  /* call out of order (e.g. fit on a poisoned handle)       */
+
+/* ---- kernel function kappa (A1) ------------------------------ */
+#define KKM_KERNEL_LINEAR 0   /* kappa(x,y) = x.y    */
+#define KKM_KERNEL_POLY 1     /* kappa(x,y) = (gamma x.y + coef0)^degree (Eq. k) */
+#define KKM_KERNEL_GAUSSIAN 2 /* kappa(x,y) = exp(-gamma ||x - y||^2)  (A1)     */
+
+/* ---- where K lives ------------------------------------------------------ */
+#define KKM_PATH_AUTO 0        /* materialise if it fits the workspace budget  */
+#define KKM_PATH_MATERIALIZE 1 /* K rows of this rank stored fp32 in HBM once  */
+#define KKM_PATH_STREAM 2      /* K tiles recomputed every iteration (reserved) */
+
+/* ---- precision of the a1 contraction (reading A9) ----------------------- */
+#define KKM_PREC_BF16X3 0   /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi bf16, fp32 TMEM acc */
+#define KKM_PREC_FP32_SIMT 1 /* fp32 CUDA-core FMA (correctness baseline)    */
+
+/* ---- kkm_debug_read selectors --------------------------------------------*/
+#define KKM_DBG_E 0      /* double [n_local x k]: E of the last iteration       */
+#define KKM_DBG_CNORM 1  /* double [k]: c (centroid norms ||mu_c||^2), +inf empty */
+#define KKM_DBG_SIZES 2  /* int32  [k]: |L_c| of the labels entering the last it. */
+#define KKM_DBG_DIAG 3   /* double [n_local]: K(i,i)                              */
+#define KKM_DBG_DFULL 4  /* double [n_local x k]: K_ii - 2E + c of the last iter.  */
+#define KKM_DBG_LABELS_PREV 5 /* int32 [n]: labels entering the last iteration     */
+
+/* ---- phase timers (kkm_phase_ms) ----------------------------------------- */
+#define KKM_PH_INIT_PREP 0  /* X copy/gather, norms, bf16 split, diag           */
+#define KKM_PH_INIT_GEMM 1  /* a1: K = kappa(X X^T) materialisation             */
+#define KKM_PH_SPMM 2       /* a2 per fit (sum over iterations)                 */
+#define KKM_PH_CNORM 3      /* a3 incl. its collective                          */
+#define KKM_PH_ASSIGN 4     /* a4 incl. the labels allgather                    */
+#define KKM_NPHASES 5
+
+typedef struct kkm_params {
+  int32_t kind;            /* KKM_KERNEL_*                                         */
+  double gamma;            /* poly: > 0; Gaussian: >= 0; ignored for linear        */
+  double coef0;            /* poly offset c of Eq. (k)                             */
+  int32_t degree;          /* poly degree >= 1                                    */
+  int32_t k;               /* clusters, 1 <= k <= n                               */
+  int32_t max_iter;        /* iterations per kkm_fit call, >= 0 (100)      */
+  int32_t stop_on_no_change; /* 1: stop early when no label changes (A4)          */
+  int32_t path;            /* KKM_PATH_*                                           */
+  int32_t precision;       /* KKM_PREC_*                                           */
+  int32_t timing;          /* 1: record per-phase CUDA-event times (kkm_phase_ms) */
+  int32_t reserved[6];     /* must be zero                                         */
+} kkm_params;
+
+typedef struct kkm_ctx *kkm_handle;
+
+/* Fills *p with defaults: Gaussian-free polynomial (gamma 1, coef0 1, degree 2,
+ * the paper's benchmark kernel P:640), k = 2, max_iter = 100, AUTO, BF16X3. */
+int kkm_default_params(kkm_params *p);
+
+/* First row owned by `rank` of `nranks` for n points: min(n, rank * ceil(n / nranks)).
+ * Every rank but the last owns exactly ceil(n / nranks) rows (the last may own fewer,
+ * or none), so labels allgather in place without compaction. rank == nranks gives n.
+ * Pure; no CUDA. Returns -1 on bad arguments. */
+int64_t kkm_shard_begin(int64_t n, int32_t rank, int32_t nranks);
+
+/* Bytes of device workspace kkm_init needs for this rank (pure; no CUDA).
+ * Includes the materialised K block (n_local x ceil32(n) fp32) when the
+ * effective path is MATERIALIZE. */
+int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks,
+                       size_t *bytes);
+
+/* Creates a handle and runs the one-time part of the path:
+ *   X_local:  rows [kkm_shard_begin(rank), kkm_shard_begin(rank+1)) of X, fp32,
+ *             row-major with leading dimension ldx >= d; host or device. It is
+ *             read during the call only (copied into the workspace). With
+ *             nranks > 1 the blocks are allgathered over `nccl_comm` (Alg. 1
+ *             line 1).
+ *   init_labels: NULL -> round-robin (A5); else n int32 in [0,k) (host or device,
+ *             identical on every rank).
+ *   workspace: device buffer of >= kkm_workspace_size bytes, 256-B aligned,
+ *             owned by the caller, must outlive the handle.
+ *   cuda_stream: cudaStream_t (NULL = legacy default stream).
+ *   nccl_comm:   ncclComm_t of nranks ranks (NULL iff nranks == 1). Borrowed.
+ * Computes norms, the bf16 hi/lo split, diag K(i,i) and, when materialising,
+ * K[rows, :] with the a1 GEMM + kappa epilogue. Collective. */
+int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t n, int64_t d,
+             int64_t ldx, int32_t rank, int32_t nranks, const int32_t *init_labels,
+             void *workspace, size_t ws_bytes, void *cuda_stream, void *nccl_comm);
+
+/* Runs up to max_iter iterations from the current labels (repeated calls resume).
+ *   iters_run:   host, out (may be NULL).
+ *   J_trace:     host, length >= max_iter + 1, or NULL. J_trace[t] = J of the
+ *                labels entering iteration t; J_trace[iters_run] = J of the final
+ *                labels (A8). fp64.
+ *   changed:     host, length >= max_iter, or NULL: #labels changed by iteration t.
+ * Synchronises the stream once at the end (and once per iteration when
+ * stop_on_no_change is set). Collective. */
+int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed);
+
+/* Copies the current labels of all n points (identical on every rank) into
+ * labels_out (host or device, n int32). Synchronises the stream. */
+int kkm_assign(kkm_handle h, int32_t *labels_out);
+
+/* J of the current labels (one E/c pass; fp64). Collective. */
+int kkm_objective(kkm_handle h, double *J);
+
+/* Replaces the current labels (n int32 in [0,k), host or device, identical on
+ * every rank): used for teacher-forced parity and for resuming. */
+int kkm_set_labels(kkm_handle h, const int32_t *labels);
+
+/* Copies an internal array of the last iteration (selectors KKM_DBG_*) to dst
+ * (host or device). Synchronises. Test hook. */
+int kkm_debug_read(kkm_handle h, int32_t what, void *dst);
+
+/* Evaluates K[i0:i0+m, j0:j0+nc] (global indices, fp32) with the SAME a1
+ * mainloop + kappa epilogue the handle uses, into dst (host or device, m x nc
+ * row-major). Test hook for kernel-value parity. Independent of the stored K. */
+int kkm_kernel_tile(kkm_handle h, int64_t i0, int64_t j0, int32_t m, int32_t nc, float *dst);
+
+/* Per-phase milliseconds (KKM_NPHASES floats, host) accumulated since init
+ * when params.timing = 1; zeros otherwise. */
+int kkm_phase_ms(kkm_handle h, float *ms);
+
+/* Number of CUDA kernels this library launched on the handle's stream since
+ * init (for bench.py's gpu_launches). */
+int kkm_launch_count(kkm_handle h, int64_t *count);
+
+/* Frees the handle (workspace and communicator stay the caller's). */
+int kkm_destroy(kkm_handle h);
+
+/* Thread-local message for the last non-zero status of this thread. */
+const char *kkm_last_error(void);
+
+/* NCCL bootstrap: rank 0 calls kkm_get_unique_id, broadcasts the 128 bytes
+ * (e.g. with torch.distributed), every rank calls kkm_comm_init with the
+ * current device set. kkm_comm_destroy finalises. */
+int kkm_get_unique_id(char id[128]);
+int kkm_comm_init(void **comm, int32_t nranks, int32_t rank, const char id[128]);
+int kkm_comm_destroy(void *comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KKM_H */

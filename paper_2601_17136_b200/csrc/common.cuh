@@ -1,0 +1,102 @@
+// common.cuh -- device helpers shared by the kkm kernels (sm_100a).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kkm {
+
+// Kernel-function parameters as the device sees them (fp32 epilogue math).
+struct KappaParams {
+  int kind;            // KKM_KERNEL_*
+  int degree;          // poly degree
+  float gamma;         // poly gamma
+  float coef0;         // poly offset
+  float neg_gamma_log2e;  // Gaussian: -gamma * log2(e), so K = 2^(neg_gamma_log2e * r2)
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// kappa applied to b = x_i . x_j (Eqs. b, k; Gaussian by reading A1 with
+// r^2 = ||x_i||^2 + ||x_j||^2 - 2 b clamped at 0, reading A23).
+__device__ __forceinline__ float kappa_epilogue(const KappaParams &kp, float b, float ni, float nj) {
+  if (kp.kind == 0) return b;
+  if (kp.kind == 1) {
+    float base = fmaf(kp.gamma, b, kp.coef0);
+    float r = base;
+    for (int e = 1; e < kp.degree; ++e) r *= base;
+    return r;
+  }
+  float r2 = fmaxf(fmaf(-2.0f, b, ni + nj), 0.0f);
+  return ex2_approx(kp.neg_gamma_log2e * r2);
+}
+
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// d += a * b elementwise on float pairs: one FFMA2 (sm_100).
+__device__ __forceinline__ void ffma2(float2 &d, float ax, float ay, float bx, float by) {
+  unsigned long long dd = pack2(d.x, d.y);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(dd) : "l"(pack2(ax, ay)), "l"(pack2(bx, by)));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(dd));
+}
+
+__device__ __forceinline__ float mask_eq(int a, int b) { return a == b ? 1.0f : 0.0f; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- mbarrier / bulk-copy PTX wrappers (Hopper+ async proxy) ----------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D bulk copy global -> shared, completing `bytes` on `bar` (cp.async.bulk, TMA engine).
+__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace kkm

@@ -1,0 +1,661 @@
+// kkm_api.cu -- the C-ABI of include/kkm.h: handle, workspace planner, one-time setup,
+// the clustering loop of Alg. 1 over the kernels in *.cuh, the NCCL
+// exchange steps of the 1D algorithm, and the test hooks.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "kkm.h"
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+#include "prep.cuh"
+#include "spmm.cuh"
+#include "update.cuh"
+
+using namespace kkm;
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+constexpr double kMaterializeBudget = 160e9;  // bytes of K per rank AUTO will store
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Everything the planner derives from (params, n, d, rank, nranks).
+struct Plan {
+  int64_t n, d, B, row0, nloc, npad, ldf, dp, ldk, lablen;
+  int k, nranks, rank, max_iter;
+  bool materialize, bf16x3;
+  int nsplit, chunks_per_split, nfin, nspmm_pass;
+  int64_t rows_per_block;
+  // offsets (bytes) into the workspace
+  size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
+      o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, total;
+};
+
+int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
+  if (!p) return fail(KKM_EINVAL, "params is NULL");
+  if (n < 1 || d < 1) return fail(KKM_EINVAL, "n=%lld d=%lld must be >= 1", (long long)n, (long long)d);
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(KKM_EINVAL, "rank %d / nranks %d out of range", rank, nranks);
+  if (p->k < 1 || p->k > n) return fail(KKM_EINVAL, "k=%d must satisfy 1 <= k <= n=%lld", p->k, (long long)n);
+  if (p->max_iter < 0) return fail(KKM_EINVAL, "max_iter=%d < 0", p->max_iter);
+  if (p->kind < 0 || p->kind > 2) return fail(KKM_EINVAL, "unknown kernel kind %d", p->kind);
+  if (p->kind == KKM_KERNEL_POLY && (p->degree < 1 || !(p->gamma > 0.0)))
+    return fail(KKM_EINVAL, "polynomial kernel needs degree >= 1 and gamma > 0");
+  if (p->kind == KKM_KERNEL_GAUSSIAN && !(p->gamma >= 0.0))
+    return fail(KKM_EINVAL, "Gaussian kernel needs gamma >= 0");
+  if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT)
+    return fail(KKM_EINVAL, "unknown precision %d", p->precision);
+  for (int i = 0; i < 6; ++i)
+    if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
+  Plan &P = *pl;
+  P.n = n;
+  P.d = d;
+  P.k = p->k;
+  P.rank = rank;
+  P.nranks = nranks;
+  P.max_iter = p->max_iter;
+  P.B = ceil_div(n, nranks);
+  P.row0 = std::min<int64_t>(n, (int64_t)rank * P.B);
+  P.nloc = std::max<int64_t>(0, std::min<int64_t>(P.B, n - P.row0));
+  P.npad = P.B * nranks;
+  P.ldf = round_up(d, 4);
+  P.dp = round_up(d, TC_BK);  // bf16 operand rows padded to whole 64-element K blocks
+  P.ldk = round_up(n, 32);
+  P.lablen = round_up(std::max(P.npad, P.ldk), 32);
+  P.bf16x3 = p->precision == KKM_PREC_BF16X3;
+  const double kbytes = (double)P.B * (double)P.ldk * 4.0;
+  if (p->path == KKM_PATH_STREAM) return fail(KKM_EUNSUP, "the streaming path is not built yet");
+  if (p->path == KKM_PATH_MATERIALIZE || p->path == KKM_PATH_AUTO) {
+    if (p->path == KKM_PATH_AUTO && kbytes > kMaterializeBudget)
+      return fail(KKM_EUNSUP, "K block of %.1f GB exceeds the materialisation budget; streaming not built yet",
+                  kbytes / 1e9);
+    P.materialize = true;
+  } else {
+    return fail(KKM_EINVAL, "unknown path %d", p->path);
+  }
+  const int64_t nchunks = ceil_div(P.ldk, SP_CH);
+  P.nsplit = (int)ceil_div(nchunks, SP_MAX_CHUNKS_PER_SPLIT);
+  P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
+  P.nspmm_pass = (int)ceil_div(P.k, SP_KPMAX);
+  P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.nloc, 1), FIN_THREADS));
+  P.rows_per_block = ceil_div(std::max<int64_t>(P.nloc, 1), P.nfin);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  const int64_t k1 = P.k + 1;
+  P.o_Xf = take((size_t)P.npad * P.ldf * 4);
+  P.o_Xhi = P.bf16x3 ? take((size_t)P.npad * P.dp * 2) : 0;
+  P.o_Xlo = P.bf16x3 ? take((size_t)P.npad * P.dp * 2) : 0;
+  P.o_norms = take((size_t)P.npad * 4);
+  P.o_diag = take((size_t)P.B * 8);
+  P.o_K = P.materialize ? take((size_t)P.B * P.ldk * 4) : 0;
+  P.o_lab[0] = take((size_t)P.lablen * 4);
+  P.o_lab[1] = take((size_t)P.lablen * 4);
+  P.o_sizes[0] = take((size_t)P.k * 4);
+  P.o_sizes[1] = take((size_t)P.k * 4);
+  P.o_Spart = take((size_t)P.nsplit * P.B * P.k * 8);
+  P.o_E = take((size_t)P.B * P.k * 8);
+  P.o_blockpart = take((size_t)P.nfin * k1 * 8);
+  P.o_rankpart = take((size_t)nranks * k1 * 8);
+  P.o_cnorm = take((size_t)P.k * 8);
+  P.o_J = take((size_t)(P.max_iter + 2) * 8);
+  P.o_changed = take((size_t)(P.max_iter + 2) * 8);
+  P.o_Dfull = take((size_t)P.B * P.k * 8);
+  P.o_bad = take(16);
+  P.o_E2 = take((size_t)P.B * P.k * 8);
+  P.o_cnorm2 = take((size_t)P.k * 8);
+  P.total = off;
+  return KKM_OK;
+}
+
+}  // namespace
+
+struct kkm_ctx {
+  kkm_params p;
+  Plan P;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  uint8_t *ws = nullptr;
+  float *Xf = nullptr, *norms = nullptr, *K = nullptr;
+  __nv_bfloat16 *Xhi = nullptr, *Xlo = nullptr;
+  double *diag, *Spart, *E, *blockpart, *rankpart, *cnorm, *J, *Dfull;
+  double *E2, *cnorm2;  // E / c of the final-labels pass (kept apart from the last iteration's)
+  int32_t *lab[2], *sizes[2];
+  unsigned long long *changed;
+  int *bad;
+  int cur = 0;  // labels[cur] / sizes[cur] are the labels entering the next iteration
+  bool poisoned = false;
+  bool have_last = false;
+  int64_t launches = 0;
+  float phase_ms[KKM_NPHASES] = {0, 0, 0, 0, 0};
+  KappaParams kp;
+  TcGemm tc;
+};
+
+namespace {
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      h->poisoned = true;                                                                \
+      return fail(KKM_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    }                                                                                    \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    ++h->launches;                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) {                                                             \
+      h->poisoned = true;                                                                \
+      return fail(KKM_ECUDA, "%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+    }                                                                                    \
+  } while (0)
+
+#define CKN(call)                                                                        \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) {                                                             \
+      h->poisoned = true;                                                                \
+      return fail(KKM_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(r_)); \
+    }                                                                                    \
+  } while (0)
+
+#define CKR(expr)        \
+  do {                   \
+    int rc_ = (expr);    \
+    if (rc_) return rc_; \
+  } while (0)
+
+// Host or device pointer copy on the handle's stream.
+int copy_any(kkm_ctx *h, void *dst, const void *src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st));
+  return KKM_OK;
+}
+
+template <int KP>
+int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
+  const Plan &P = h->P;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(spmm_onehot_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)spmm_smem_bytes()));
+    attr_set = true;
+  }
+  const int64_t items = ceil_div(P.nloc, SP_ROWS) * P.nsplit;
+  const int grid = (int)std::min<int64_t>(items, h->num_sms);
+  spmm_onehot_kernel<KP><<<grid, SP_THREADS, spmm_smem_bytes(), h->st>>>(
+      h->K, P.ldk, P.nloc, labels, P.k, c0, P.nsplit, P.chunks_per_split, h->Spart);
+  CKL();
+  return KKM_OK;
+}
+
+// a2: S = unnormalised K V^T for the local rows, with the given full label vector.
+int launch_spmm(kkm_ctx *h, const int32_t *labels) {
+  const Plan &P = h->P;
+  if (P.nloc == 0) return KKM_OK;
+  if (P.k > SP_KPMAX) {
+    for (int c0 = 0; c0 < P.k; c0 += SP_KPMAX) CKR(launch_spmm_kp<SP_KPMAX>(h, labels, c0));
+    return KKM_OK;
+  }
+  const int kp = (P.k + 1) / 2 * 2;
+  switch (kp) {
+    case 2: return launch_spmm_kp<2>(h, labels, 0);
+    case 4: return launch_spmm_kp<4>(h, labels, 0);
+    case 6: return launch_spmm_kp<6>(h, labels, 0);
+    case 8: return launch_spmm_kp<8>(h, labels, 0);
+    case 10: return launch_spmm_kp<10>(h, labels, 0);
+    case 12: return launch_spmm_kp<12>(h, labels, 0);
+    case 14: return launch_spmm_kp<14>(h, labels, 0);
+    default: return launch_spmm_kp<16>(h, labels, 0);
+  }
+}
+
+// a3: E, z, c (cnorm) and J for the labels entering the iteration -> E_out, cnorm_out,
+// J_out. sizes_next / changed_out (may be NULL) are zeroed for the following assign.
+int run_cnorm(kkm_ctx *h, double *E_out, double *cnorm_out, double *J_out, int32_t *sizes_next,
+              unsigned long long *changed_out) {
+  const Plan &P = h->P;
+  const int32_t *labels = h->lab[h->cur];
+  const int32_t *sizes = h->sizes[h->cur];
+  const int k1 = P.k + 1;
+  if (P.nloc > 0) {
+    finalize_kernel<<<P.nfin, FIN_THREADS, (size_t)k1 * FIN_THREADS * 8, h->st>>>(
+        h->Spart, P.nsplit, P.nloc, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block, E_out,
+        h->blockpart);
+    CKL();
+  }
+  cnorm_local_kernel<<<1, 128, 0, h->st>>>(h->blockpart, P.nloc > 0 ? P.nfin : 0, P.k,
+                                           h->rankpart + (int64_t)P.rank * k1);
+  CKL();
+  if (P.nranks > 1)
+    CKN(ncclAllGather(h->rankpart + (int64_t)P.rank * k1, h->rankpart, k1, ncclDouble, h->comm, h->st));
+  cnorm_final_kernel<<<1, 128, 0, h->st>>>(h->rankpart, P.nranks, P.k, sizes, cnorm_out, J_out,
+                                           sizes_next, changed_out);
+  CKL();
+  return KKM_OK;
+}
+
+// a4 + the V update: new labels into lab[cur^1], sizes into sizes[cur^1], allgather.
+int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
+  const Plan &P = h->P;
+  const int nx = h->cur ^ 1;
+  if (P.nloc > 0) {
+    const int th = 256;
+    assign_kernel<<<(unsigned)ceil_div(P.nloc, th), th, (size_t)P.k * 4, h->st>>>(
+        h->E, P.nloc, P.k, h->cnorm, h->diag, h->lab[h->cur] + P.row0, h->lab[nx] + P.row0,
+        h->sizes[nx], changed_out, h->Dfull);
+    CKL();
+  }
+  if (P.nranks > 1) {
+    CKN(ncclGroupStart());
+    CKN(ncclAllGather(h->lab[nx] + P.row0, h->lab[nx], P.B, ncclInt32, h->comm, h->st));
+    CKN(ncclAllReduce(h->sizes[nx], h->sizes[nx], P.k, ncclInt32, ncclSum, h->comm, h->st));
+    CKN(ncclGroupEnd());
+  }
+  return KKM_OK;
+}
+
+int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, float *out, int64_t ldo) {
+  const Plan &P = h->P;
+  if (m <= 0 || ncov <= 0) return KKM_OK;
+  if (P.bf16x3) {
+    int rc = tc_gemm_launch(h->tc, h->Xhi, h->Xlo, P.npad, P.dp, P.n, i0, m, j0, ncov, h->norms,
+                            h->kp, out, ldo, h->st, &h->launches);
+    if (rc) {
+      h->poisoned = true;
+      return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
+    }
+    return KKM_OK;
+  }
+  dim3 grid((unsigned)ceil_div(ncov, SG_BN), (unsigned)ceil_div(m, SG_BM));
+  gemm_simt_kernel<<<grid, 256, 0, h->st>>>(h->Xf, P.ldf, P.n, P.d, i0, m, j0, ncov, h->norms,
+                                             h->kp, out, ldo);
+  CKL();
+  return KKM_OK;
+}
+
+struct EvPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace
+
+extern "C" {
+
+int kkm_default_params(kkm_params *p) {
+  if (!p) return fail(KKM_EINVAL, "params is NULL");
+  std::memset(p, 0, sizeof(*p));
+  p->kind = KKM_KERNEL_POLY;
+  p->gamma = 1.0;
+  p->coef0 = 1.0;
+  p->degree = 2;
+  p->k = 2;
+  p->max_iter = 100;
+  p->path = KKM_PATH_AUTO;
+  p->precision = KKM_PREC_BF16X3;
+  return KKM_OK;
+}
+
+int64_t kkm_shard_begin(int64_t n, int32_t rank, int32_t nranks) {
+  if (nranks < 1 || n < 0 || rank < 0) return -1;
+  const int64_t B = ceil_div(n, nranks);
+  return std::min<int64_t>(n, (int64_t)rank * B);
+}
+
+int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks,
+                       size_t *bytes) {
+  if (!bytes) return fail(KKM_EINVAL, "bytes is NULL");
+  Plan P;
+  CKR(make_plan(p, n, d, rank, nranks, &P));
+  *bytes = P.total;
+  return KKM_OK;
+}
+
+const char *kkm_last_error(void) { return g_err; }
+
+int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t n, int64_t d,
+             int64_t ldx, int32_t rank, int32_t nranks, const int32_t *init_labels, void *workspace,
+             size_t ws_bytes, void *cuda_stream, void *nccl_comm) {
+  if (!out) return fail(KKM_EINVAL, "out is NULL");
+  *out = nullptr;
+  Plan P;
+  CKR(make_plan(p, n, d, rank, nranks, &P));
+  if (ldx < d) return fail(KKM_EINVAL, "ldx=%lld < d=%lld", (long long)ldx, (long long)d);
+  if (!X_local && P.nloc > 0) return fail(KKM_EINVAL, "X_local is NULL");
+  if (!workspace) return fail(KKM_EINVAL, "workspace is NULL");
+  if (((uintptr_t)workspace) & 255) return fail(KKM_EINVAL, "workspace must be 256-byte aligned");
+  if (ws_bytes < P.total)
+    return fail(KKM_ENOMEM, "workspace %zu bytes < required %zu", ws_bytes, P.total);
+  if (nranks > 1 && !nccl_comm) return fail(KKM_EINVAL, "nranks > 1 needs an NCCL communicator");
+
+  kkm_ctx *h = new kkm_ctx();
+  h->p = *p;
+  h->P = P;
+  h->st = (cudaStream_t)cuda_stream;
+  h->comm = (ncclComm_t)nccl_comm;
+  h->ws = (uint8_t *)workspace;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    delete h;
+    return fail(KKM_ECUDA, "no CUDA device");
+  }
+  uint8_t *w = h->ws;
+  h->Xf = (float *)(w + P.o_Xf);
+  h->Xhi = P.bf16x3 ? (__nv_bfloat16 *)(w + P.o_Xhi) : nullptr;
+  h->Xlo = P.bf16x3 ? (__nv_bfloat16 *)(w + P.o_Xlo) : nullptr;
+  h->norms = (float *)(w + P.o_norms);
+  h->diag = (double *)(w + P.o_diag);
+  h->K = P.materialize ? (float *)(w + P.o_K) : nullptr;
+  for (int b = 0; b < 2; ++b) {
+    h->lab[b] = (int32_t *)(w + P.o_lab[b]);
+    h->sizes[b] = (int32_t *)(w + P.o_sizes[b]);
+  }
+  h->Spart = (double *)(w + P.o_Spart);
+  h->E = (double *)(w + P.o_E);
+  h->blockpart = (double *)(w + P.o_blockpart);
+  h->rankpart = (double *)(w + P.o_rankpart);
+  h->cnorm = (double *)(w + P.o_cnorm);
+  h->J = (double *)(w + P.o_J);
+  h->changed = (unsigned long long *)(w + P.o_changed);
+  h->Dfull = (double *)(w + P.o_Dfull);
+  h->bad = (int *)(w + P.o_bad);
+  h->E2 = (double *)(w + P.o_E2);
+  h->cnorm2 = (double *)(w + P.o_cnorm2);
+  h->kp.kind = p->kind;
+  h->kp.degree = p->degree;
+  h->kp.gamma = (float)p->gamma;
+  h->kp.coef0 = (float)p->coef0;
+  h->kp.neg_gamma_log2e = (float)(-p->gamma * 1.4426950408889634);
+
+  int rc = [&]() -> int {
+    cudaEvent_t e0, e1, e2;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    CK(cudaEventRecord(e0, h->st));
+    // ---- X (Alg. 1 line 1: allgather P) into Xf [npad x ldf], zero padded
+    CK(cudaMemsetAsync(h->Xf, 0, (size_t)P.npad * P.ldf * 4, h->st));
+    if (P.nloc > 0)
+      CK(cudaMemcpy2DAsync(h->Xf + P.row0 * P.ldf, P.ldf * 4, X_local, ldx * 4, P.d * 4, P.nloc,
+                           cudaMemcpyDefault, h->st));
+    if (P.nranks > 1)
+      CKN(ncclAllGather(h->Xf + (int64_t)P.rank * P.B * P.ldf, h->Xf, (size_t)P.B * P.ldf, ncclFloat,
+                        h->comm, h->st));
+    // ---- a5: norms, bf16 split, diag
+    {
+      const int wpb = 8;
+      prep_rows_kernel<<<(unsigned)ceil_div(P.npad, wpb), wpb * 32, 0, h->st>>>(
+          h->Xf, P.ldf, P.n, P.npad, P.d, h->norms, h->Xhi, h->Xlo, P.dp);
+      CKL();
+      if (P.nloc > 0) {
+        diag_kernel<<<(unsigned)ceil_div(P.nloc, wpb), wpb * 32, 0, h->st>>>(
+            h->Xf, P.ldf, P.d, P.row0, P.nloc, p->kind, p->gamma, p->coef0, p->degree, h->diag);
+        CKL();
+      }
+    }
+    // ---- labels (A5 round robin, or the caller's) and sizes
+    for (int b = 0; b < 2; ++b) {
+      round_robin_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(h->lab[b], P.n, P.lablen, P.k);
+      CKL();
+    }
+    if (init_labels) {
+      CK(cudaMemsetAsync(h->bad, 0, 4, h->st));
+      int32_t *tmp = h->lab[1];
+      CK(cudaMemcpyAsync(tmp, init_labels, (size_t)P.n * 4, cudaMemcpyDefault, h->st));
+      load_labels_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, h->lab[0], P.n,
+                                                                               P.lablen, P.k, h->bad);
+      CKL();
+      round_robin_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(h->lab[1], P.n, P.lablen, P.k);
+      CKL();
+      int bad = 0;
+      CK(cudaMemcpyAsync(&bad, h->bad, 4, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      if (bad) return fail(KKM_ELABEL, "%d init labels outside [0, %d)", bad, P.k);
+    }
+    CK(cudaMemsetAsync(h->sizes[0], 0, (size_t)P.k * 4, h->st));
+    histogram_kernel<<<std::min<int64_t>(ceil_div(P.n, 256), 1024), 256, (size_t)P.k * 4, h->st>>>(
+        h->lab[0], P.n, P.k, h->sizes[0]);
+    CKL();
+    CK(cudaEventRecord(e1, h->st));
+    // ---- a1: K[rows, :] = kappa(X X^T), materialised once
+    if (P.materialize) CKR(launch_gemm(h, P.row0, P.nloc, 0, P.ldk, h->K, P.ldk));
+    CK(cudaEventRecord(e2, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (h->p.timing) {
+      float a = 0, b = 0;
+      CK(cudaEventElapsedTime(&a, e0, e1));
+      CK(cudaEventElapsedTime(&b, e1, e2));
+      h->phase_ms[KKM_PH_INIT_PREP] += a;
+      h->phase_ms[KKM_PH_INIT_GEMM] += b;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    return KKM_OK;
+  }();
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return KKM_OK;
+}
+
+int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed) {
+  if (!h) return fail(KKM_EINVAL, "handle is NULL");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned by an earlier CUDA/NCCL error");
+  const Plan &P = h->P;
+  const int T = h->p.max_iter;
+  std::vector<cudaEvent_t> ev;
+  const bool timing = h->p.timing != 0;
+  auto rec = [&](std::vector<cudaEvent_t> &v) -> int {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, h->st));
+    v.push_back(e);
+    return KKM_OK;
+  };
+  int t = 0;
+  for (t = 0; t < T; ++t) {
+    if (timing) CKR(rec(ev));
+    CKR(launch_spmm(h, h->lab[h->cur]));                                  // a2
+    if (timing) CKR(rec(ev));
+    CKR(run_cnorm(h, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
+    if (timing) CKR(rec(ev));
+    CKR(run_assign(h, h->changed + t));                                   // a4
+    if (timing) CKR(rec(ev));
+    h->cur ^= 1;
+    h->have_last = true;
+    if (h->p.stop_on_no_change) {
+      unsigned long long c = 0;
+      CK(cudaMemcpyAsync(&c, h->changed + t, 8, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      if (c == 0) {
+        ++t;
+        break;
+      }
+    }
+  }
+  // J of the final labels (one more a2 + a3 pass, as the oracle's J_trace[iters])
+  CKR(launch_spmm(h, h->lab[h->cur]));
+  CKR(run_cnorm(h, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
+  std::vector<double> J((size_t)t + 1);
+  std::vector<unsigned long long> ch((size_t)std::max(t, 1));
+  CK(cudaMemcpyAsync(J.data(), h->J, (size_t)(t + 1) * 8, cudaMemcpyDeviceToHost, h->st));
+  if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (timing) {
+    for (size_t i = 0; i + 3 < ev.size(); i += 4) {
+      float a, b, c;
+      CK(cudaEventElapsedTime(&a, ev[i], ev[i + 1]));
+      CK(cudaEventElapsedTime(&b, ev[i + 1], ev[i + 2]));
+      CK(cudaEventElapsedTime(&c, ev[i + 2], ev[i + 3]));
+      h->phase_ms[KKM_PH_SPMM] += a;
+      h->phase_ms[KKM_PH_CNORM] += b;
+      h->phase_ms[KKM_PH_ASSIGN] += c;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  if (iters_run) *iters_run = t;
+  if (J_trace) std::memcpy(J_trace, J.data(), (size_t)(t + 1) * 8);
+  if (changed)
+    for (int i = 0; i < t; ++i) changed[i] = (int64_t)ch[i];
+  (void)P;
+  return KKM_OK;
+}
+
+int kkm_assign(kkm_handle h, int32_t *labels_out) {
+  if (!h || !labels_out) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  CKR(copy_any(h, labels_out, h->lab[h->cur], (size_t)h->P.n * 4));
+  CK(cudaStreamSynchronize(h->st));
+  return KKM_OK;
+}
+
+int kkm_objective(kkm_handle h, double *J) {
+  if (!h || !J) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  double *slot = h->J + h->P.max_iter + 1;
+  CKR(launch_spmm(h, h->lab[h->cur]));
+  CKR(run_cnorm(h, h->E2, h->cnorm2, slot, nullptr, nullptr));
+  CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return KKM_OK;
+}
+
+int kkm_set_labels(kkm_handle h, const int32_t *labels) {
+  if (!h || !labels) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  const Plan &P = h->P;
+  int32_t *dst = h->lab[h->cur], *tmp = h->lab[h->cur ^ 1];
+  CK(cudaMemsetAsync(h->bad, 0, 4, h->st));
+  CK(cudaMemcpyAsync(tmp, labels, (size_t)P.n * 4, cudaMemcpyDefault, h->st));
+  load_labels_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, dst, P.n, P.lablen, P.k, h->bad);
+  CKL();
+  round_robin_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, P.n, P.lablen, P.k);
+  CKL();
+  CK(cudaMemsetAsync(h->sizes[h->cur], 0, (size_t)P.k * 4, h->st));
+  histogram_kernel<<<std::min<int64_t>(ceil_div(P.n, 256), 1024), 256, (size_t)P.k * 4, h->st>>>(
+      dst, P.n, P.k, h->sizes[h->cur]);
+  CKL();
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, h->bad, 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (bad) return fail(KKM_ELABEL, "%d labels outside [0, %d)", bad, P.k);
+  h->have_last = false;
+  return KKM_OK;
+}
+
+int kkm_debug_read(kkm_handle h, int32_t what, void *dst) {
+  if (!h || !dst) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  const Plan &P = h->P;
+  const int prev = h->cur ^ 1;  // buffers of the labels entering the last iteration
+  switch (what) {
+    case KKM_DBG_E: CKR(copy_any(h, dst, h->E, (size_t)P.nloc * P.k * 8)); break;
+    case KKM_DBG_CNORM: CKR(copy_any(h, dst, h->cnorm, (size_t)P.k * 8)); break;
+    case KKM_DBG_SIZES:
+      CKR(copy_any(h, dst, h->sizes[h->have_last ? prev : h->cur], (size_t)P.k * 4));
+      break;
+    case KKM_DBG_DIAG: CKR(copy_any(h, dst, h->diag, (size_t)P.nloc * 8)); break;
+    case KKM_DBG_DFULL: CKR(copy_any(h, dst, h->Dfull, (size_t)P.nloc * P.k * 8)); break;
+    case KKM_DBG_LABELS_PREV:
+      CKR(copy_any(h, dst, h->lab[h->have_last ? prev : h->cur], (size_t)P.n * 4));
+      break;
+    default: return fail(KKM_EINVAL, "unknown debug selector %d", what);
+  }
+  CK(cudaStreamSynchronize(h->st));
+  return KKM_OK;
+}
+
+int kkm_kernel_tile(kkm_handle h, int64_t i0, int64_t j0, int32_t m, int32_t nc, float *dst) {
+  if (!h || !dst) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  const Plan &P = h->P;
+  if (m < 1 || nc < 1 || i0 < 0 || j0 < 0 || i0 + m > P.n || j0 + nc > P.n)
+    return fail(KKM_EINVAL, "tile out of range");
+  float *tmp = nullptr;
+  CK(cudaMallocAsync((void **)&tmp, (size_t)m * nc * 4, h->st));
+  int rc = launch_gemm(h, i0, m, j0, nc, tmp, nc);
+  if (rc == KKM_OK) rc = copy_any(h, dst, tmp, (size_t)m * nc * 4);
+  cudaFreeAsync(tmp, h->st);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(h->st));
+  return KKM_OK;
+}
+
+int kkm_phase_ms(kkm_handle h, float *ms) {
+  if (!h || !ms) return fail(KKM_EINVAL, "NULL argument");
+  std::memcpy(ms, h->phase_ms, sizeof(h->phase_ms));
+  return KKM_OK;
+}
+
+int kkm_launch_count(kkm_handle h, int64_t *count) {
+  if (!h || !count) return fail(KKM_EINVAL, "NULL argument");
+  *count = h->launches;
+  return KKM_OK;
+}
+
+int kkm_destroy(kkm_handle h) {
+  if (!h) return KKM_OK;
+  cudaStreamSynchronize(h->st);
+  delete h;
+  return KKM_OK;
+}
+
+int kkm_get_unique_id(char id[128]) {
+  if (!id) return fail(KKM_EINVAL, "id is NULL");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(KKM_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return KKM_OK;
+}
+
+int kkm_comm_init(void **comm, int32_t nranks, int32_t rank, const char id[128]) {
+  if (!comm || !id) return fail(KKM_EINVAL, "NULL argument");
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t c;
+  ncclResult_t r = ncclCommInitRank(&c, nranks, u, rank);
+  if (r != ncclSuccess) return fail(KKM_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  *comm = c;
+  return KKM_OK;
+}
+
+int kkm_comm_destroy(void *comm) {
+  if (!comm) return KKM_OK;
+  ncclResult_t r = ncclCommDestroy((ncclComm_t)comm);
+  if (r != ncclSuccess) return fail(KKM_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return KKM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// prep.cuh -- a5: per-run constants.
+//   norms[i] = ||x_i||^2 (fp64 accumulation, stored fp32 for the Gaussian epilogue)
+//   Xhi/Xlo  = bf16 split of X: hi = RN_bf16(x), lo = RN_bf16(x - hi) (reading A9),
+//              rows zero-padded to dp columns for the TMA/UMMA operand tiles
+//   diag[i]  = K(i,i) = kappa(x_i, x_i) in fp64 (reading A3)
+#pragma once
+#include "common.cuh"
+
+namespace kkm {
+
+// One warp per row over all padded rows [0, nrows_pad); rows >= n are zero.
+__global__ void prep_rows_kernel(const float *__restrict__ Xf, int64_t ldf, int64_t n,
+                                 int64_t nrows_pad, int64_t d, float *__restrict__ norms,
+                                 __nv_bfloat16 *__restrict__ Xhi, __nv_bfloat16 *__restrict__ Xlo,
+                                 int64_t dp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= nrows_pad) return;
+  double s = 0.0;
+  const bool valid = row < n;
+  for (int64_t t = lane; t < dp; t += 32) {
+    float x = (valid && t < d) ? Xf[row * ldf + t] : 0.0f;
+    s += (double)x * (double)x;
+    if (Xhi) {
+      __nv_bfloat16 hi = __float2bfloat16_rn(x);
+      __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+      Xhi[row * dp + t] = hi;
+      Xlo[row * dp + t] = lo;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) norms[row] = (float)s;
+}
+
+// diag K(i,i) for the local rows [row0, row0 + nloc), from fp64 squared norms
+// recomputed here (one warp per row) so that diag does not inherit fp32 rounding.
+__global__ void diag_kernel(const float *__restrict__ Xf, int64_t ldf, int64_t d, int64_t row0,
+                            int64_t nloc, int kind, double gamma, double coef0, int degree,
+                            double *__restrict__ diag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= nloc) return;
+  const float *x = Xf + (row0 + r) * ldf;
+  double s = 0.0;
+  for (int64_t t = lane; t < d; t += 32) s += (double)x[t] * (double)x[t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    double v;
+    if (kind == 0) {
+      v = s;
+    } else if (kind == 1) {
+      double base = gamma * s + coef0;
+      v = 1.0;
+      for (int e = 0; e < degree; ++e) v *= base;
+    } else {
+      v = 1.0;  // exp(-gamma * 0)
+    }
+    diag[r] = v;
+  }
+}
+
+// labels[j] = j mod k for j < n (reading A5); -1 on the padding [n, len).
+__global__ void round_robin_kernel(int32_t *__restrict__ labels, int64_t n, int64_t len, int k) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < len) labels[j] = j < n ? (int32_t)(j % k) : -1;
+}
+
+// Copies user labels into the padded label array and validates them; bad[0] counts
+// labels outside [0, k).
+__global__ void load_labels_kernel(const int32_t *__restrict__ src, int32_t *__restrict__ labels,
+                                   int64_t n, int64_t len, int k, int *__restrict__ bad) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= len) return;
+  if (j < n) {
+    int32_t v = src[j];
+    if (v < 0 || v >= k) atomicAdd(bad, 1);
+    labels[j] = v;
+  } else {
+    labels[j] = -1;
+  }
+}
+
+// sizes[c] = |L_c| over labels[0, n) (exact integer histogram).
+__global__ void histogram_kernel(const int32_t *__restrict__ labels, int64_t n, int k,
+                                 int32_t *__restrict__ sizes) {
+  extern __shared__ int32_t hist[];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = labels[j];
+    if (v >= 0 && v < k) atomicAdd(&hist[v], 1);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    if (hist[c]) atomicAdd(&sizes[c], hist[c]);
+}
+
+}  // namespace kkm

@@ -1,0 +1,158 @@
+// spmm.cuh -- a2 on a materialised K: S(i, c) = sum_{j : cl(j) = c} K(i, j), the
+// unnormalised E = K V^T of Eq. (e) (V of Eq. v: one nonzero
+// 1/|L_c| per column, so E(i,c) = S(i,c) / |L_c|, applied in update.cuh).
+//
+// HBM-bound: every iteration streams the rank's K block (n_local x n fp32) once.
+// Design:
+//   * persistent CTAs, one per SM; a work item = 4 consecutive rows x one column
+//     split; warp 8 is a producer that streams 2048-column chunks of those 4 rows
+//     plus the matching labels into a 4-stage shared-memory ring with 1-D bulk
+//     copies (cp.async.bulk, the TMA engine) completing on mbarriers, so the HBM
+//     latency is covered by up to 160 KB in flight per SM without registers;
+//   * 8 consumer warps read the chunk from shared memory (conflict-free LDS.128)
+//     and reduce it into per-lane accumulators acc[row][cluster] with a one-hot
+//     mask: acc += K(i, j) * [cl(j) == c], two columns per FFMA2 (fma.rn.f32x2), so the
+//     cost per element is ~KP/2 FFMA2 + KP/R mask ops and no divergent indexing;
+//   * fp32 within a lane (<= 512 columns per split), fixed-order shuffle tree across
+//     lanes, fp64 across the 8 warps in fixed order -> deterministic.
+#pragma once
+#include "common.cuh"
+
+namespace kkm {
+
+constexpr int SP_ROWS = 4;          // rows per work item
+constexpr int SP_CH = 2048;         // columns per chunk
+constexpr int SP_STAGES = 4;        // smem ring depth
+constexpr int SP_CWARPS = 8;        // consumer warps
+constexpr int SP_THREADS = (SP_CWARPS + 1) * 32;
+constexpr int SP_MAX_CHUNKS_PER_SPLIT = 64;  // bounds fp32 terms per lane
+constexpr int SP_KPMAX = 16;
+
+constexpr size_t spmm_smem_bytes() {
+  return (size_t)SP_STAGES * (SP_ROWS + 1) * SP_CH * 4 + SP_CWARPS * SP_ROWS * SP_KPMAX * 4 +
+         2 * SP_STAGES * 8 + 64;
+}
+
+// Spart[(s * nrows + i) * k + c0 + c] for clusters c0 .. c0 + KP - 1 (c0 + c < k).
+template <int KP>
+__global__ void __launch_bounds__(SP_THREADS, 1)
+    spmm_onehot_kernel(const float *__restrict__ K, int64_t ldk, int64_t nrows,
+                       const int32_t *__restrict__ labels, int k, int c0, int nsplit,
+                       int chunks_per_split, double *__restrict__ Spart) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float *ring = reinterpret_cast<float *>(smem);  // [STAGES][ROWS + 1][CH]
+  float *red = ring + (size_t)SP_STAGES * (SP_ROWS + 1) * SP_CH;  // [CWARPS][ROWS][KPMAX]
+  uint64_t *full = reinterpret_cast<uint64_t *>(red + SP_CWARPS * SP_ROWS * SP_KPMAX);
+  uint64_t *empty = full + SP_STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (ldk + SP_CH - 1) / SP_CH;
+  const int64_t ngroups = (nrows + SP_ROWS - 1) / SP_ROWS;
+  const int64_t nitems = ngroups * nsplit;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SP_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SP_CWARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  if (warp == SP_CWARPS) {
+    // ---------------- producer: one elected lane issues the bulk copies
+    if (lane == 0) {
+      for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int64_t g = item / nsplit;
+        const int s = (int)(item % nsplit);
+        const int64_t q0 = (int64_t)s * chunks_per_split;
+        const int64_t q1 = q0 + chunks_per_split < nchunks ? q0 + chunks_per_split : nchunks;
+        const int64_t r0 = g * SP_ROWS;
+        const int nr = (int)(nrows - r0 < SP_ROWS ? nrows - r0 : SP_ROWS);
+        for (int64_t q = q0; q < q1; ++q) {
+          const int64_t col0 = q * SP_CH;
+          const uint32_t cols = (uint32_t)(ldk - col0 < SP_CH ? ldk - col0 : SP_CH);
+          mbar_wait(&empty[stage], phase ^ 1);
+          float *st = ring + (size_t)stage * (SP_ROWS + 1) * SP_CH;
+          mbar_arrive_expect_tx(&full[stage], (uint32_t)(nr + 1) * cols * 4u);
+          bulk_g2s(st + SP_ROWS * SP_CH, labels + col0, cols * 4u, &full[stage]);
+          for (int r = 0; r < nr; ++r)
+            bulk_g2s(st + r * SP_CH, K + (r0 + r) * ldk + col0, cols * 4u, &full[stage]);
+          if (++stage == SP_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int64_t g = item / nsplit;
+    const int s = (int)(item % nsplit);
+    const int64_t q0 = (int64_t)s * chunks_per_split;
+    const int64_t q1 = q0 + chunks_per_split < nchunks ? q0 + chunks_per_split : nchunks;
+    float2 acc[SP_ROWS][KP];
+#pragma unroll
+    for (int r = 0; r < SP_ROWS; ++r)
+#pragma unroll
+      for (int c = 0; c < KP; ++c) acc[r][c] = make_float2(0.f, 0.f);
+
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t col0 = q * SP_CH;
+      const int cols = (int)(ldk - col0 < SP_CH ? ldk - col0 : SP_CH);
+      mbar_wait(&full[stage], phase);
+      const float *st = ring + (size_t)stage * (SP_ROWS + 1) * SP_CH;
+      const int4 *lab4 = reinterpret_cast<const int4 *>(st + SP_ROWS * SP_CH);
+      const int nquads = cols >> 2;
+      for (int v = warp * 32 + lane; v < nquads; v += SP_CWARPS * 32) {
+        const int4 l = lab4[v];
+        float4 x[SP_ROWS];
+#pragma unroll
+        for (int r = 0; r < SP_ROWS; ++r) x[r] = reinterpret_cast<const float4 *>(st + r * SP_CH)[v];
+#pragma unroll
+        for (int c = 0; c < KP; ++c) {
+          const int cc = c0 + c;
+          const float m0 = mask_eq(l.x, cc), m1 = mask_eq(l.y, cc);
+          const float m2 = mask_eq(l.z, cc), m3 = mask_eq(l.w, cc);
+#pragma unroll
+          for (int r = 0; r < SP_ROWS; ++r) {
+            ffma2(acc[r][c], x[r].x, x[r].y, m0, m1);
+            ffma2(acc[r][c], x[r].z, x[r].w, m2, m3);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == SP_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // ---- fixed-order reduction: lanes (shuffle tree, fp32) then warps (fp64)
+#pragma unroll
+    for (int r = 0; r < SP_ROWS; ++r)
+#pragma unroll
+      for (int c = 0; c < KP; ++c) {
+        float v = warp_sum(acc[r][c].x + acc[r][c].y);
+        if (lane == 0) red[(warp * SP_ROWS + r) * SP_KPMAX + c] = v;
+      }
+    asm volatile("bar.sync 1, %0;" ::"n"(SP_CWARPS * 32));
+    const int64_t r0 = g * SP_ROWS;
+    for (int t = threadIdx.x; t < SP_ROWS * KP; t += SP_CWARPS * 32) {
+      const int r = t / KP, c = t % KP;
+      if (r0 + r < nrows && c0 + c < k) {
+        double sum = 0.0;
+        for (int w = 0; w < SP_CWARPS; ++w) sum += (double)red[(w * SP_ROWS + r) * SP_KPMAX + c];
+        Spart[((int64_t)s * nrows + r0 + r) * k + c0 + c] = sum;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(SP_CWARPS * 32));
+  }
+}
+
+}  // namespace kkm

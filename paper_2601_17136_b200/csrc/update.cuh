@@ -1,0 +1,117 @@
+// update.cuh -- a3 and a4 of the iteration.
+//   finalize:    E(i,c) = S(i,c) / |L_c| (Eq. e with Eq. v), z(i) = E(i, cl(i)) (Eq. z),
+//                per-block fp64 partials of sum_{i in L_c} z(i) and of sum_i (K_ii - z_i)
+//   cnorm_local: fixed-order sum of the block partials -> this rank's (k+1) partials
+//   cnorm_final: fixed-order sum over ranks -> c(c) = ||mu_c||^2 (Eq. c; +inf if empty,
+//                reading A7) and J = tr K - sum_c |L_c| c(c) (reading A8); also zeroes
+//                the next iteration's size histogram and change counter
+//   assign:      D(i,c) = -2E(i,c) + c(c) (Eq. d), lowest-index argmin (A6), new sizes
+//                (exact int histogram) and the number of changed labels
+// All reductions are fixed-order, so results are bitwise reproducible run to run.
+#pragma once
+#include "common.cuh"
+
+namespace kkm {
+
+constexpr int FIN_THREADS = 128;
+
+// grid: nblocks; block b handles rows [b * rows_per_block, ...). Dynamic smem:
+// (k + 1) * FIN_THREADS doubles.
+__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(
+    const double *__restrict__ Spart, int nsplit, int64_t nrows, int k,
+    const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl_local,
+    const double *__restrict__ diag, int64_t rows_per_block, double *__restrict__ E,
+    double *__restrict__ blockpart) {
+  extern __shared__ double sacc[];  // [(k + 1)][FIN_THREADS]
+  const int t = threadIdx.x;
+  for (int c = 0; c <= k; ++c) sacc[c * FIN_THREADS + t] = 0.0;
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t re = rb + rows_per_block < nrows ? rb + rows_per_block : nrows;
+  for (int64_t i = rb + t; i < re; i += FIN_THREADS) {
+    const int li = cl_local[i];
+    double zi = 0.0;
+    for (int c = 0; c < k; ++c) {
+      double s = 0.0;
+      for (int p = 0; p < nsplit; ++p) s += Spart[((int64_t)p * nrows + i) * k + c];
+      const int32_t sz = sizes[c];
+      const double e = sz > 0 ? s / (double)sz : 0.0;
+      E[i * k + c] = e;
+      if (c == li) zi = e;
+    }
+    sacc[li * FIN_THREADS + t] += zi;
+    sacc[k * FIN_THREADS + t] += diag[i] - zi;
+  }
+  __syncthreads();
+  for (int w = FIN_THREADS / 2; w > 0; w >>= 1) {
+    if (t < w)
+      for (int c = 0; c <= k; ++c) sacc[c * FIN_THREADS + t] += sacc[c * FIN_THREADS + t + w];
+    __syncthreads();
+  }
+  for (int c = t; c <= k; c += FIN_THREADS) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sacc[c * FIN_THREADS];
+}
+
+// out[c] = sum_b blockpart[b][c] in ascending b (one thread per c).
+__global__ void cnorm_local_kernel(const double *__restrict__ blockpart, int nblocks, int k,
+                                   double *__restrict__ out) {
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += blockpart[(int64_t)b * (k + 1) + c];
+    out[c] = s;
+  }
+}
+
+// rankpart: [nranks][k + 1]. Writes cnorm[k], J_out[0]; zeroes sizes_next[k], changed_out[0].
+__global__ void cnorm_final_kernel(const double *__restrict__ rankpart, int nranks, int k,
+                                   const int32_t *__restrict__ sizes, double *__restrict__ cnorm,
+                                   double *__restrict__ J_out, int32_t *__restrict__ sizes_next,
+                                   unsigned long long *__restrict__ changed_out) {
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += rankpart[(int64_t)r * (k + 1) + c];
+    if (c < k) {
+      const int32_t sz = sizes[c];
+      cnorm[c] = sz > 0 ? s / (double)sz : __longlong_as_double(0x7ff0000000000000LL);  // +inf
+      if (sizes_next) sizes_next[c] = 0;
+    } else if (J_out) {
+      *J_out = s;  // sum_i (K_ii - z_i) = tr K - sum_c |L_c| c(c)
+    }
+  }
+  if (threadIdx.x == 0 && changed_out) *changed_out = 0ull;
+}
+
+// One thread per local row. new_labels / old labels are the rank's slice.
+__global__ void assign_kernel(const double *__restrict__ E, int64_t nrows, int k,
+                              const double *__restrict__ cnorm, const double *__restrict__ diag,
+                              const int32_t *__restrict__ cl_old, int32_t *__restrict__ cl_new,
+                              int32_t *__restrict__ sizes_next,
+                              unsigned long long *__restrict__ changed_out,
+                              double *__restrict__ Dfull) {
+  extern __shared__ int32_t hist[];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned changed = 0;
+  if (i < nrows) {
+    int best = 0;
+    double bd = __longlong_as_double(0x7ff0000000000000LL);
+    for (int c = 0; c < k; ++c) {
+      const double cn = cnorm[c];
+      const double dsh = isinf(cn) ? cn : fma(-2.0, E[i * k + c], cn);
+      if (Dfull) Dfull[i * k + c] = diag[i] + dsh;
+      if (dsh < bd) {
+        bd = dsh;
+        best = c;
+      }
+    }
+    cl_new[i] = best;
+    changed = (best != cl_old[i]);
+    atomicAdd(&hist[best], 1);
+  }
+  const unsigned wc = __reduce_add_sync(0xffffffffu, changed);
+  if ((threadIdx.x & 31) == 0 && wc) atomicAdd(changed_out, (unsigned long long)wc);
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    if (hist[c]) atomicAdd(&sizes_next[c], hist[c]);
+}
+
+}  // namespace kkm

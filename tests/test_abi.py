@@ -1,0 +1,78 @@
+"""CPU-only checks of the C-ABI boundary: libkkm.so loads, exports every function
+include/kkm.h declares, and the pure (no-CUDA) entry points validate arguments."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2601_17136_b200 as kkm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "kkm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kkm_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    names = header_functions()
+    assert len(names) >= 17, names
+    L = ctypes.CDLL(kkm.lib_path())
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a_and_in_tree():
+    path = kkm.lib_path()
+    assert os.path.dirname(path) == os.path.join(ROOT, "paper_2601_17136_b200")
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out, out
+
+
+def test_default_params_and_shards():
+    p = kkm.default_params()
+    assert (p.kind, p.gamma, p.coef0, p.degree, p.max_iter) == (kkm.KERNEL_POLY, 1.0, 1.0, 2, 100)
+    for n, P in [(10, 3), (60000, 8), (5, 4), (1, 1)]:
+        b = [kkm.shard_begin(n, r, P) for r in range(P + 1)]
+        assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
+        B = -(-n // P)
+        assert all(y - x == B for x, y in zip(b, b[1:]) if y < n)
+    assert kkm.shard_begin(5, -1, 2) == -1
+
+
+def test_workspace_size_and_errors():
+    p = kkm.default_params()
+    p.k = 10
+    nb = kkm.workspace_size(p, 60000, 784)
+    ldk = 60000
+    assert nb >= 60000 * ldk * 4  # K block materialised
+    nb2 = kkm.workspace_size(p, 60000, 784, rank=1, nranks=4)
+    assert nb2 < nb / 3
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(p, 5, 784)  # k > n
+    q = kkm.default_params()
+    q.k, q.kind, q.gamma = 3, kkm.KERNEL_GAUSSIAN, -1.0
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(q, 100, 4)
+    q = kkm.default_params()
+    q.k, q.degree = 3, 0
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(q, 100, 4)
+    q = kkm.default_params()
+    q.k, q.path = 3, kkm.PATH_STREAM
+    with pytest.raises(kkm.KKMError, match="EUNSUP"):
+        kkm.workspace_size(q, 100, 4)
+    q = kkm.default_params()
+    q.k = 3
+    with pytest.raises(kkm.KKMError, match="EUNSUP"):
+        kkm.workspace_size(q, 1_000_000, 784)  # 4 TB of K: too big to materialise
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(p, 60000, 784, rank=4, nranks=4)
+    q = kkm.default_params()
+    q.reserved[2] = 1
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(q, 100, 4)

@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded
+inputs, element by element, under the rules of tests/parity.py."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import TAU, check_iteration, check_kernel_values, check_labels, row_scale
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # the -m gpu suite runs on a B200 box
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2601_17136_b200 as kkm  # noqa: E402
+
+PRECISIONS = [kkm.PREC_FP32_SIMT, kkm.PREC_BF16X3]
+PREC_IDS = ["fp32", "bf16x3"]
+
+
+def _handle(X, k, kind, gamma, coef0, degree, max_iter, precision, **kw):
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    return kkm.KernelKMeans(Xd, X.shape[0], k, kind, gamma, coef0, degree, max_iter=max_iter,
+                            precision=precision, **kw)
+
+
+def teacher_forced(X, k, kind, gamma=1.0, coef0=0.0, degree=1, iters=3, precision=0, init=None):
+    """For each t: inject the oracle's cl_t, run one GPU iteration, compare everything."""
+    ref = oracle.fit(X, k, kind, gamma, coef0, degree, max_iter=iters, init_labels=init,
+                     keep_trace=True)
+    K, diag = ref["K"], ref["diag"]
+    h = _handle(X, k, kind, gamma, coef0, degree, 1, precision)
+    assert np.allclose(h.debug_read(kkm.DBG_DIAG), diag, rtol=1e-12)
+    mism = 0
+    for t in range(ref["iters"]):
+        cl = ref["label_trace"][t]
+        h.set_labels(cl)
+        it = oracle.iteration(K, diag, cl, k)
+        n_it, J, ch = h.fit()
+        assert n_it == 1
+        new = h.assign().cpu().numpy()
+        gpu = dict(E=h.debug_read(kkm.DBG_E), cnorm=h.debug_read(kkm.DBG_CNORM),
+                   Dfull=h.debug_read(kkm.DBG_DFULL), new_labels=new,
+                   sizes=h.debug_read(kkm.DBG_SIZES), J=J[0])
+        assert np.array_equal(h.debug_read(kkm.DBG_LABELS_PREV), cl)
+        mism += check_iteration(gpu, it, diag)
+        assert ch[0] == int((new != cl).sum())
+        if np.array_equal(new, it["new_labels"]):  # final-labels J (J_trace[1])
+            Jn = oracle.objective(diag, new, k, oracle.cnorm(oracle.E_rows(K, new, k), new, k))
+            assert abs(J[1] - Jn) <= 1e-5 * max(abs(Jn), 1e-9 * diag.sum())
+    h.destroy()
+    return mism
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_rings_config1_teacher_forced(precision):
+    """BASELINE.json configs[0]: rings n=1000, d=2, k=2, Gaussian, 30 iterations."""
+    X, cfg = synth.make_config("rings")
+    teacher_forced(X, cfg["k"], cfg["kind"], cfg["gamma"], iters=cfg["iters"], precision=precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_mnist_like_poly_teacher_forced(precision):
+    """configs[1] recipe at n = 3000 (ragged vs 32/128/2048 tiles), poly(1,1,2)."""
+    X, cfg = synth.make_config("mnist60k", n=3000)
+    teacher_forced(X, 10, cfg["kind"], 1.0, 1.0, 2, iters=4, precision=precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_har_like_gaussian_teacher_forced(precision):
+    """configs[2] recipe at n = 2500, d = 561 (not a multiple of 8), Gaussian median gamma."""
+    X, cfg = synth.make_config("har200k", n=2500)
+    teacher_forced(X, 6, cfg["kind"], cfg["gamma"], iters=4, precision=precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_many_clusters_multipass(precision):
+    """k = 21 > 16 exercises the multi-pass one-hot SpMM; linear kernel."""
+    X = synth.blobs(1500, 16, 21, seed=3, sep=4.0)
+    teacher_forced(X, 21, oracle.LINEAR, iters=3, precision=precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_edge_k1_kn_and_tiny(precision):
+    X = synth.blobs(37, 3, 2, seed=5)
+    teacher_forced(X, 1, oracle.POLY, 0.5, 1.0, 3, iters=2, precision=precision)
+    teacher_forced(X, 37, oracle.GAUSSIAN, 0.3, iters=2, precision=precision)
+    teacher_forced(X[:2], 2, oracle.LINEAR, iters=2, precision=precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_empty_cluster(precision):
+    X = synth.blobs(300, 4, 3, seed=8)
+    init = np.zeros(300, dtype=np.int32)
+    init[::3] = 2  # cluster 1 empty
+    teacher_forced(X, 3, oracle.LINEAR, iters=3, precision=precision, init=init)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_free_running_blobs(precision):
+    """Margin-separated blobs: the free-running GPU fit must match the oracle exactly."""
+    X = synth.blobs(4000, 10, 5, seed=12, sep=6.0)
+    ref = oracle.fit(X, 5, oracle.POLY, 0.05, 1.0, 2, max_iter=8)
+    h = _handle(X, 5, oracle.POLY, 0.05, 1.0, 2, 8, precision)
+    it, J, ch = h.fit()
+    lab = h.assign().cpu().numpy()
+    assert it == ref["iters"]
+    assert np.array_equal(lab, ref["labels"])
+    assert np.array_equal(ch, ref["changed"])
+    diag = ref["diag"]
+    tol = 1e-5 * np.maximum(np.abs(ref["J_trace"]), 1e-9 * diag.sum())
+    assert (np.abs(J - ref["J_trace"]) <= tol).all()
+    assert abs(h.objective() - ref["J_trace"][-1]) <= tol[-1]
+    # resume: a second fit continues from the current labels
+    it2, J2, _ = h.fit()
+    assert abs(J2[0] - ref["J_trace"][-1]) <= tol[-1]
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_stop_on_no_change(precision):
+    X = synth.blobs(2000, 6, 4, seed=2, sep=8.0)
+    ref = oracle.fit(X, 4, oracle.LINEAR, max_iter=50, stop_on_no_change=True)
+    h = _handle(X, 4, oracle.LINEAR, 1.0, 0.0, 1, 50, precision, stop_on_no_change=True)
+    it, J, ch = h.fit()
+    assert it == ref["iters"] and ch[-1] == 0
+    assert np.array_equal(h.assign().cpu().numpy(), ref["labels"])
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+@pytest.mark.parametrize("name,n", [("mnist60k", 700), ("har200k", 600), ("rings", 1000)])
+def test_kernel_tiles(precision, name, n):
+    X, cfg = synth.make_config(name, n=n)
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    h = _handle(X, cfg["k"], *args, 1, precision)
+    diag = oracle.kernel_diag(X, *args)
+    for (i0, j0, m, nc) in [(0, 0, n, n), (5, 130, 97, 301), (n - 3, 0, 3, n)]:
+        Kg = h.kernel_tile(i0, j0, m, nc)
+        Kr = oracle.kernel_rows(X, np.arange(i0, i0 + m), *args)[:, j0:j0 + nc]
+        check_kernel_values(Kg, Kr, diag[i0:i0 + m], diag[j0:j0 + nc])
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_host_buffers_e2e(precision):
+    """X and the labels output in host memory (the e2e path of bench.py)."""
+    X = synth.blobs(1000, 8, 4, seed=4, sep=6.0)
+    ref = oracle.fit(X, 4, oracle.GAUSSIAN, 0.01, max_iter=5)
+    Xh = torch.from_numpy(X).pin_memory()
+    h = kkm.KernelKMeans(Xh, 1000, 4, kkm.KERNEL_GAUSSIAN, 0.01, 0.0, 1, max_iter=5,
+                         precision=precision)
+    h.fit()
+    out = torch.empty(1000, dtype=torch.int32).pin_memory()
+    h.assign(out)
+    assert np.array_equal(out.numpy(), ref["labels"])
+
+
+def test_errors_and_poison_free():
+    X = synth.blobs(100, 4, 3, seed=1)
+    with pytest.raises(kkm.KKMError, match="ELABEL"):
+        _handle(X, 3, oracle.LINEAR, 1.0, 0.0, 1, 2, kkm.PREC_FP32_SIMT,
+                init_labels=np.full(100, 3, dtype=np.int32))
+    h = _handle(X, 3, oracle.LINEAR, 1.0, 0.0, 1, 2, kkm.PREC_FP32_SIMT)
+    with pytest.raises(kkm.KKMError, match="ELABEL"):
+        h.set_labels(np.full(100, -1, dtype=np.int32))
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        h.kernel_tile(90, 0, 20, 5)
+    h.fit()  # still usable after argument errors
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_full_size_config2_sampled(precision):
+    """BASELINE.json configs[1] at full size (n = 60000, d = 784, k = 10, poly, K materialised,
+    the bench launch configuration): one iteration checked on 192 sampled rows whose exact
+    fp64 K rows the oracle computes one by one, plus the global identities."""
+    X, cfg = synth.make_config("mnist60k")
+    n, k = X.shape[0], cfg["k"]
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    h = _handle(X, k, *args, 1, precision)
+    it, J, ch = h.fit()
+    E = h.debug_read(kkm.DBG_E)
+    D = h.debug_read(kkm.DBG_DFULL)
+    cn = h.debug_read(kkm.DBG_CNORM)
+    cl = h.debug_read(kkm.DBG_LABELS_PREV)
+    new = h.assign().cpu().numpy()
+    sizes = h.debug_read(kkm.DBG_SIZES)
+    assert np.array_equal(sizes, np.bincount(cl, minlength=k))
+    rows = np.random.default_rng(0).choice(n, 192, replace=False)
+    Kr = oracle.kernel_rows(X, rows, *args)
+    diag = oracle.kernel_diag(X, *args, rows=rows)
+    Er = oracle.E_rows(Kr, cl, k)
+    # cnorm from its definition on the GPU's own E (c_c = mean over L_c of E_ic)
+    cn_def = np.array([E[cl == c, c].mean() for c in range(k)])
+    scale = row_scale(Er, diag, cn_def)
+    assert np.allclose(cn, cn_def, rtol=1e-12, atol=0)
+    assert (np.abs(E[rows] - Er) <= TAU * scale[:, None]).all()
+    nl, Dr = oracle.assign(Er, diag, cn_def)
+    assert (np.abs(D[rows] - Dr) <= TAU * scale[:, None]).all()
+    check_labels(new[rows], nl, Dr, scale)
+    diag_all = h.debug_read(kkm.DBG_DIAG)
+    assert abs(J[0] - (diag_all.sum() - (sizes * cn).sum())) <= 1e-9 * abs(J[0])
+    Kt = h.kernel_tile(int(rows[0]), 0, 1, n)
+    check_kernel_values(Kt, Kr[:1], diag[:1], oracle.kernel_diag(X, *args))
