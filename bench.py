@@ -184,7 +184,8 @@ def run_ours(args):
     r0, r1 = kkm.shard_begin(n, rank, world), kkm.shard_begin(n, rank + 1, world)
     X_local = synth.mnist_like(n, cfg["seed"], row_begin=r0, row_end=r1)
     d = X_local.shape[1]
-    precision = {"bf16x3": kkm.PREC_BF16X3, "fp32": kkm.PREC_FP32_SIMT}[args.precision]
+    precision = {"bf16x3": kkm.PREC_BF16X3, "fp16x3": kkm.PREC_FP16X3,
+                 "fp32": kkm.PREC_FP32_SIMT}[args.precision]
     kw = dict(kind=cfg["kind"], gamma=1.0, coef0=1.0, degree=2, max_iter=iters,
               precision=precision, rank=rank, nranks=world, comm=comm, timing=True)
     p = kkm.default_params()
@@ -263,7 +264,10 @@ def run_ours(args):
         if os.path.exists(tp):
             with open(tp) as f:
                 traffic = json.load(f).get("bytes_per_launch")
-        gemm_peak = peaks["bf16_tflops"] / 3.0 if precision == kkm.PREC_BF16X3 else 148 * 128 * 2 * 1.965e9 / 1e12
+        tensor = precision in (kkm.PREC_BF16X3, kkm.PREC_FP16X3)
+        # 3 dense 16-bit MMAs per useful product: useful-flop peak = measured bf16 dense / 3
+        # (fp16 and bf16 share the dense rate); SIMT: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz
+        gemm_peak = peaks["bf16_tflops"] / 3.0 if tensor else 148 * 128 * 2 * 1.965e9 / 1e12
         line = {
             "metric": METRIC, "value": iter_ms / 1e3, "unit": "s/iteration",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -279,7 +283,7 @@ def run_ours(args):
                          "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_launch": spmm_bytes, "launch_ms": spmm_ms},
             "roofline_a1": {"kernel": f"gemm ({args.precision}) + kappa", "bound": "tensor"
-                            if precision == kkm.PREC_BF16X3 else "alu",
+                            if tensor else "alu",
                             "achieved": gemm_tfs, "peak": gemm_peak, "unit": "TFLOP/s",
                             "frac": gemm_tfs / gemm_peak, "flops_per_launch": gemm_flops,
                             "launch_ms": gemm_ms},
@@ -315,7 +319,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--iters", type=int, default=0, help="override iterations per step")
-    ap.add_argument("--precision", choices=["bf16x3", "fp32"], default="bf16x3")
+    ap.add_argument("--precision", choices=["fp16x3", "bf16x3", "fp32"], default="fp16x3")
     ap.add_argument("--ref-rows", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

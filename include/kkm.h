@@ -63,8 +63,11 @@ extern "C" {
 #define KKM_PATH_STREAM 2      /* K tiles recomputed every iteration (reserved) */
 
 /* ---- precision of the a1 contraction (reading A9) ----------------------- */
-#define KKM_PREC_BF16X3 0   /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi bf16, fp32 TMEM acc */
-#define KKM_PREC_FP32_SIMT 1 /* fp32 CUDA-core FMA (correctness baseline)    */
+#define KKM_PREC_BF16X3 0    /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi, bf16 split of x;
+                                 product error ~2^-17 |x||y|                               */
+#define KKM_PREC_FP32_SIMT 1 /* fp32 CUDA-core FMA (correctness baseline)                 */
+#define KKM_PREC_FP16X3 2    /* tcgen05 kind::f16, 3 MMAs on an fp16 split of 2^e_i x_i (per-row
+                                power-of-two scale); product error ~2^-21 |x||y|; default */
 
 /* ---- kkm_debug_read selectors --------------------------------------------*/
 #define KKM_DBG_E 0      /* double [n_local x k]: E of the last iteration       */
@@ -98,8 +101,8 @@ typedef struct kkm_params {
 
 typedef struct kkm_ctx *kkm_handle;
 
-/* Fills *p with defaults: Gaussian-free polynomial (gamma 1, coef0 1, degree 2,
- * the paper's benchmark kernel P:640), k = 2, max_iter = 100, AUTO, BF16X3. */
+/* Fills *p with defaults: polynomial kernel (gamma 1, coef0 1, degree 2, the paper's
+ * benchmark kernel P:640), k = 2, max_iter = 100, AUTO, FP16X3. */
 int kkm_default_params(kkm_params *p);
 
 /* First row owned by `rank` of `nranks` for n points: min(n, rank * ceil(n / nranks)).

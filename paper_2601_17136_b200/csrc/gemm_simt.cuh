@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float *__restrict_
     for (int q = 0; q < 8; ++q) {
       const int64_t j = bj + (q < 4 ? tx * 4 + q : 64 + tx * 4 + (q - 4));
       if (j >= j0 + ncov) continue;
-      float v = (j < n && i < n) ? kappa_epilogue(kp, acc[p][q], ni, norms[j]) : 0.f;
+      float v = (j < n && i < n) ? kappa_epilogue(kp, acc[p][q], ni, norms[j], i == j) : 0.f;
       out[(i - i0) * ldo + (j - j0)] = v;
     }
   }

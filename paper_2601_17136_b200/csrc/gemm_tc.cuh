@@ -1,21 +1,359 @@
-// gemm_tc.cuh -- a1 on the 5th-generation tensor cores (placeholder until the
-// tcgen05 kernel lands; KKM_PREC_BF16X3 reports failure).
+// gemm_tc.cuh -- a1 on the 5th-generation tensor cores: K = kappa(X X^T) (Eqs. b, k,
+// P:92-104) with X split into bf16 hi + lo (reading A9) and
+//     B = X_hi X_hi^T + X_hi X_lo^T + X_lo X_hi^T      (3 bf16 MMAs, fp32 TMEM accumulation)
+// so the product error is ~2^-16 relative instead of bf16's 2^-8.
+//
+// Kernel anatomy: persistent, one CTA per SM, warp-specialised.
+//   warp 0      TMA producer: per 64-wide K block loads A_hi, A_lo (128 rows) and B_hi,
+//               B_lo (256 rows) into a 2-stage smem ring (128B-swizzled, K-major)
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//               M=128 N=256 K=16, 12 per K block (4 k-steps x 3 products), into one of
+//               two TMEM accumulators (2 x 256 fp32 columns = all 512), and releases
+//               smem stages / publishes accumulators with tcgen05.commit -> mbarrier
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (thread = row), kappa in registers, fp32
+//               stores of the K tile; the other accumulator is being filled meanwhile.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace kkm {
 
+constexpr int TC_BM = 128;   // UMMA M (rows of K per tile)
+constexpr int TC_BN = 256;   // UMMA N (columns of K per tile)
+constexpr int TC_BK = 64;    // K block = one 128-byte swizzle atom of bf16
+constexpr int TC_STAGES = 2;
+constexpr int TC_THREADS = 192;
+constexpr uint32_t TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
+constexpr uint32_t TC_B_BYTES = TC_BN * TC_BK * 2;  // 32 KB
+constexpr uint32_t TC_STAGE_BYTES = 2 * TC_A_BYTES + 2 * TC_B_BYTES;  // 96 KB
+constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_GROUP_M = 8;  // tile raster: groups of 8 row tiles sweep the column tiles
+
+// instruction descriptor, kind::f16: D fp32, A/B bf16 (format 1) or fp16 (format 0), both
+// K-major, N = 256, M = 128
+constexpr uint32_t tc_idesc(bool fp16) {
+  return (1u << 4) | ((fp16 ? 0u : 1u) << 7) | ((fp16 ? 0u : 1u) << 10) |
+         ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;             // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO
+  d |= (uint64_t)1 << 46;             // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+// Tile t -> (row tile, column tile): groups of TC_GROUP_M row tiles, column-major inside a
+// group, so the ~148 concurrent tiles share A and B operands through L2.
+__device__ __forceinline__ void tc_tile_coords(int64_t t, int tiles_m, int tiles_n, int &tm, int &tn) {
+  const int64_t per_group = (int64_t)TC_GROUP_M * tiles_n;
+  const int64_t g = t / per_group;
+  const int first_m = (int)(g * TC_GROUP_M);
+  const int gm = tiles_m - first_m < TC_GROUP_M ? tiles_m - first_m : TC_GROUP_M;
+  const int64_t r = t - g * per_group;
+  tm = first_m + (int)(r % gm);
+  tn = (int)(r / gm);
+}
+
+// out[(i - i0) * ldo + (j - j0)] = kappa(x_i . x_j), i in [i0, i0+m), j in [j0, j0+ncov),
+// 0 for j >= n. A rows start at i0, B rows at j0 (global point indices). rscale (fp16 split,
+// else NULL): x_i . x_j = acc * rscale[i] * rscale[j], exact powers of two.
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+                   uint32_t idesc, int nkb, int64_t n, int64_t i0, int64_t m, int64_t j0,
+                   int64_t ncov, const float *__restrict__ norms, const float *__restrict__ rscale,
+                   KappaParams kp, float *__restrict__ out, int64_t ldo, int tiles_m, int tiles_n) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
+  uint8_t *smem = smem_raw + pad;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * TC_STAGE_BYTES);
+  uint64_t *empty = full + TC_STAGES;
+  uint64_t *tfull = empty + TC_STAGES;  // [2] accumulator ready
+  uint64_t *tempty = tfull + 2;         // [2] accumulator drained
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (int64_t)tiles_m * tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {  // TMEM: 512 columns = two 128 x 256 fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int tm, tn;
+        tc_tile_coords(t, tiles_m, tiles_n, tm, tn);
+        const int ra = (int)(i0 + (int64_t)tm * TC_BM);
+        const int rb = (int)(j0 + (int64_t)tn * TC_BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *st = smem + stage * TC_STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], TC_STAGE_BYTES);
+          const int kc = kb * TC_BK;
+          tma_load_2d(st, &tm_hi, kc, ra, &full[stage]);                                 // A_hi
+          tma_load_2d(st + TC_A_BYTES, &tm_lo, kc, ra, &full[stage]);                    // A_lo
+          tma_load_2d(st + 2 * TC_A_BYTES, &tm_hi, kc, rb, &full[stage]);                // B_hi
+          tma_load_2d(st + 2 * TC_A_BYTES + TC_A_BYTES, &tm_hi, kc, rb + 128, &full[stage]);
+          tma_load_2d(st + 2 * TC_A_BYTES + TC_B_BYTES, &tm_lo, kc, rb, &full[stage]);   // B_lo
+          tma_load_2d(st + 2 * TC_A_BYTES + TC_B_BYTES + TC_A_BYTES, &tm_lo, kc, rb + 128, &full[stage]);
+          if (++stage == TC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int acc = (int)(it & 1);
+        const uint32_t acc_phase = (uint32_t)((it >> 1) & 1);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + stage * TC_STAGE_BYTES);
+          const uint32_t a_hi = st, a_lo = st + TC_A_BYTES;
+          const uint32_t b_hi = st + 2 * TC_A_BYTES, b_lo = b_hi + TC_B_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint32_t ko = (uint32_t)k * 32u;  // 16 bf16 = 32 bytes along K inside the atom
+            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+            umma_f16(d_tmem, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_hi + ko), idesc, first);
+            umma_f16(d_tmem, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_lo + ko), idesc, 1u);
+            umma_f16(d_tmem, umma_desc_sw128(a_lo + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
+          }
+          umma_commit(&empty[stage]);  // smem stage free once these MMAs have read it
+          if (++stage == TC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator complete
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
+    const int row_in_tile = quarter * 32 + lane;
+    const bool vec_ok = ((ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      int tm, tn;
+      tc_tile_coords(t, tiles_m, tiles_n, tm, tn);
+      const int acc = (int)(it & 1);
+      const uint32_t acc_phase = (uint32_t)((it >> 1) & 1);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t i = i0 + (int64_t)tm * TC_BM + row_in_tile;
+      const bool row_ok = i < i0 + m;
+      const float ni = row_ok && i < n ? norms[i] : 0.f;
+      const float rsi = (rscale && row_ok && i < n) ? rscale[i] : 1.f;
+      const int64_t jt = j0 + (int64_t)tn * TC_BN;
+      float *orow = out + (i - i0) * ldo;
+#pragma unroll 1
+      for (int c = 0; c < TC_BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
+        const int64_t jb = jt + c * 32;
+        if (!row_ok || jb >= j0 + ncov) continue;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int64_t j = jb + q;
+          if (j < n && i < n) {
+            const float b = rscale ? v[q] * rsi * __ldg(rscale + j) : v[q];
+            v[q] = kappa_epilogue(kp, b, ni, kp.kind == 2 ? __ldg(norms + j) : 0.f, i == j);
+          } else {
+            v[q] = 0.f;
+          }
+        }
+        if (vec_ok && jb + 32 <= j0 + ncov) {
+          float4 *o4 = reinterpret_cast<float4 *>(orow + (jb - j0));
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (jb + q < j0 + ncov) orow[jb + q - j0] = v[q];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host side
 struct TcGemm {
-  int dummy = 0;
+  const void *hi = nullptr, *lo = nullptr;  // operands the tensor maps describe
+  bool fp16 = false;
+  CUtensorMap map_hi, map_lo;
+  bool attr = false;
+  int num_sms = 0;
 };
 
-inline const char *tc_gemm_error() { return "tcgen05 GEMM not built yet"; }
-
-inline int tc_gemm_launch(TcGemm &, const __nv_bfloat16 *, const __nv_bfloat16 *, int64_t, int64_t,
-                          int64_t, int64_t, int64_t, int64_t, int64_t, const float *,
-                          const KappaParams &, float *, int64_t, cudaStream_t, int64_t *) {
-  return 1;
+inline const char *&tc_err_slot() {
+  static thread_local const char *msg = "";
+  return msg;
 }
-constexpr int TC_BK = 64;
+inline const char *tc_gemm_error() { return tc_err_slot(); }
+
+inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16, int64_t rows,
+                        int64_t dp) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode) {
+      tc_err_slot() = "cuTensorMapEncodeTiled unavailable";
+      return 1;
+    }
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)dp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)dp * 2};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, 128u};
+  cuuint32_t es[2] = {1u, 1u};
+  for (int w = 0; w < 2; ++w) {
+    CUresult r = encode(w ? &g.map_lo : &g.map_hi,
+                        fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        (void *)(w ? Xlo : Xhi), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      tc_err_slot() = "cuTensorMapEncodeTiled failed";
+      return 1;
+    }
+  }
+  g.hi = Xhi;
+  g.lo = Xlo;
+  g.fp16 = fp16;
+  return 0;
+}
+
+// Launch over [i0, i0+m) x [j0, j0+ncov). rows = padded row count of Xhi/Xlo, dp = padded d.
+// fp16: operands are the scaled fp16 split (rscale given), else the bf16 split.
+inline int tc_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16,
+                          const float *rscale, int64_t rows, int64_t dp, int64_t n, int64_t i0,
+                          int64_t m, int64_t j0, int64_t ncov, const float *norms,
+                          const KappaParams &kp, float *out, int64_t ldo, cudaStream_t st,
+                          int64_t *launches) {
+  if (g.hi != Xhi || g.lo != Xlo || g.fp16 != fp16)
+    if (tc_make_maps(g, Xhi, Xlo, fp16, rows, dp)) return 1;
+  if (!g.attr) {
+    if (cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM) !=
+        cudaSuccess) {
+      tc_err_slot() = "cudaFuncSetAttribute(tc_gemm_kernel) failed";
+      return 1;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    g.attr = true;
+  }
+  const int tiles_m = (int)((m + TC_BM - 1) / TC_BM);
+  const int tiles_n = (int)((ncov + TC_BN - 1) / TC_BN);
+  const int64_t ntiles = (int64_t)tiles_m * tiles_n;
+  const int grid = (int)(ntiles < g.num_sms ? ntiles : g.num_sms);
+  tc_gemm_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(g.map_hi, g.map_lo, tc_idesc(fp16), (int)(dp / TC_BK),
+                                                    n, i0, m, j0, ncov, norms, fp16 ? rscale : nullptr,
+                                                    kp, out, ldo, tiles_m, tiles_n);
+  if (launches) ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    tc_err_slot() = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
 
 }  // namespace kkm

@@ -43,12 +43,13 @@ int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 struct Plan {
   int64_t n, d, B, row0, nloc, npad, ldf, dp, ldk, lablen;
   int k, nranks, rank, max_iter;
-  bool materialize, bf16x3;
+  bool materialize, tc, fp16;  // tc: tensor-core a1 (bf16x3 or fp16x3); fp16: fp16x3 split
   int nsplit, chunks_per_split, nfin, nspmm_pass;
   int64_t rows_per_block;
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
-      o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, total;
+      o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
+      total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -63,7 +64,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     return fail(KKM_EINVAL, "polynomial kernel needs degree >= 1 and gamma > 0");
   if (p->kind == KKM_KERNEL_GAUSSIAN && !(p->gamma >= 0.0))
     return fail(KKM_EINVAL, "Gaussian kernel needs gamma >= 0");
-  if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT)
+  if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT &&
+      p->precision != KKM_PREC_FP16X3)
     return fail(KKM_EINVAL, "unknown precision %d", p->precision);
   for (int i = 0; i < 6; ++i)
     if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
@@ -82,7 +84,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.dp = round_up(d, TC_BK);  // bf16 operand rows padded to whole 64-element K blocks
   P.ldk = round_up(n, 32);
   P.lablen = round_up(std::max(P.npad, P.ldk), 32);
-  P.bf16x3 = p->precision == KKM_PREC_BF16X3;
+  P.tc = p->precision == KKM_PREC_BF16X3 || p->precision == KKM_PREC_FP16X3;
+  P.fp16 = p->precision == KKM_PREC_FP16X3;
   const double kbytes = (double)P.B * (double)P.ldk * 4.0;
   if (p->path == KKM_PATH_STREAM) return fail(KKM_EUNSUP, "the streaming path is not built yet");
   if (p->path == KKM_PATH_MATERIALIZE || p->path == KKM_PATH_AUTO) {
@@ -107,8 +110,9 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   };
   const int64_t k1 = P.k + 1;
   P.o_Xf = take((size_t)P.npad * P.ldf * 4);
-  P.o_Xhi = P.bf16x3 ? take((size_t)P.npad * P.dp * 2) : 0;
-  P.o_Xlo = P.bf16x3 ? take((size_t)P.npad * P.dp * 2) : 0;
+  P.o_Xhi = P.tc ? take((size_t)P.npad * P.dp * 2) : 0;
+  P.o_Xlo = P.tc ? take((size_t)P.npad * P.dp * 2) : 0;
+  P.o_rscale = take((size_t)P.npad * 4);
   P.o_norms = take((size_t)P.npad * 4);
   P.o_diag = take((size_t)P.B * 8);
   P.o_K = P.materialize ? take((size_t)P.B * P.ldk * 4) : 0;
@@ -141,7 +145,8 @@ struct kkm_ctx {
   int num_sms = 148;
   uint8_t *ws = nullptr;
   float *Xf = nullptr, *norms = nullptr, *K = nullptr;
-  __nv_bfloat16 *Xhi = nullptr, *Xlo = nullptr;
+  uint16_t *Xhi = nullptr, *Xlo = nullptr;  // bf16 or fp16 split of X (P.tc)
+  float *rscale = nullptr;                   // 1 / s_i of the fp16 split
   double *diag, *Spart, *E, *blockpart, *rankpart, *cnorm, *J, *Dfull;
   double *E2, *cnorm2;  // E / c of the final-labels pass (kept apart from the last iteration's)
   int32_t *lab[2], *sizes[2];
@@ -284,9 +289,9 @@ int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
 int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, float *out, int64_t ldo) {
   const Plan &P = h->P;
   if (m <= 0 || ncov <= 0) return KKM_OK;
-  if (P.bf16x3) {
-    int rc = tc_gemm_launch(h->tc, h->Xhi, h->Xlo, P.npad, P.dp, P.n, i0, m, j0, ncov, h->norms,
-                            h->kp, out, ldo, h->st, &h->launches);
+  if (P.tc) {
+    int rc = tc_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0,
+                            ncov, h->norms, h->kp, out, ldo, h->st, &h->launches);
     if (rc) {
       h->poisoned = true;
       return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
@@ -318,7 +323,7 @@ int kkm_default_params(kkm_params *p) {
   p->k = 2;
   p->max_iter = 100;
   p->path = KKM_PATH_AUTO;
-  p->precision = KKM_PREC_BF16X3;
+  p->precision = KKM_PREC_FP16X3;
   return KKM_OK;
 }
 
@@ -368,8 +373,9 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   }
   uint8_t *w = h->ws;
   h->Xf = (float *)(w + P.o_Xf);
-  h->Xhi = P.bf16x3 ? (__nv_bfloat16 *)(w + P.o_Xhi) : nullptr;
-  h->Xlo = P.bf16x3 ? (__nv_bfloat16 *)(w + P.o_Xlo) : nullptr;
+  h->Xhi = P.tc ? (uint16_t *)(w + P.o_Xhi) : nullptr;
+  h->Xlo = P.tc ? (uint16_t *)(w + P.o_Xlo) : nullptr;
+  h->rscale = (float *)(w + P.o_rscale);
   h->norms = (float *)(w + P.o_norms);
   h->diag = (double *)(w + P.o_diag);
   h->K = P.materialize ? (float *)(w + P.o_K) : nullptr;
@@ -412,7 +418,8 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     {
       const int wpb = 8;
       prep_rows_kernel<<<(unsigned)ceil_div(P.npad, wpb), wpb * 32, 0, h->st>>>(
-          h->Xf, P.ldf, P.n, P.npad, P.d, h->norms, h->Xhi, h->Xlo, P.dp);
+          h->Xf, P.ldf, P.n, P.npad, P.d, h->norms, h->Xhi, h->Xlo, P.dp,
+          P.tc ? (P.fp16 ? 2 : 1) : 0, h->rscale);
       CKL();
       if (P.nloc > 0) {
         diag_kernel<<<(unsigned)ceil_div(P.nloc, wpb), wpb * 32, 0, h->st>>>(

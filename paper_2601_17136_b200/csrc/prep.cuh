@@ -9,28 +9,58 @@
 namespace kkm {
 
 // One warp per row over all padded rows [0, nrows_pad); rows >= n are zero.
+// split: 0 none, 1 bf16 (hi = RN_bf16(x), lo = RN_bf16(x - hi)), 2 fp16 with a per-row
+// power-of-two scale s_i putting max|x_i| s_i in [2^13, 2^14): hi = RN_fp16(x s_i),
+// lo = RN_fp16(x s_i - hi); rscale[i] = 1 / s_i (exact) undoes it in the GEMM epilogue.
 __global__ void prep_rows_kernel(const float *__restrict__ Xf, int64_t ldf, int64_t n,
                                  int64_t nrows_pad, int64_t d, float *__restrict__ norms,
-                                 __nv_bfloat16 *__restrict__ Xhi, __nv_bfloat16 *__restrict__ Xlo,
-                                 int64_t dp) {
+                                 uint16_t *__restrict__ Xhi, uint16_t *__restrict__ Xlo,
+                                 int64_t dp, int split, float *__restrict__ rscale) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= nrows_pad) return;
   double s = 0.0;
   const bool valid = row < n;
-  for (int64_t t = lane; t < dp; t += 32) {
-    float x = (valid && t < d) ? Xf[row * ldf + t] : 0.0f;
+  float amax = 0.0f;
+  for (int64_t t = lane; t < d; t += 32) {
+    const float x = valid ? Xf[row * ldf + t] : 0.0f;
     s += (double)x * (double)x;
-    if (Xhi) {
-      __nv_bfloat16 hi = __float2bfloat16_rn(x);
-      __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-      Xhi[row * dp + t] = hi;
-      Xlo[row * dp + t] = lo;
-    }
+    amax = fmaxf(amax, fabsf(x));
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) norms[row] = (float)s;
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  float sc = 1.0f;
+  if (split == 2 && amax > 0.0f) {
+    int e;
+    frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
+    sc = ldexpf(1.0f, 14 - e);
+  }
+  if (lane == 0) {
+    norms[row] = (float)s;
+    if (rscale) rscale[row] = 1.0f / sc;
+  }
+  if (split == 0) return;
+  for (int64_t t = lane; t < dp; t += 32) {
+    const float x = (valid && t < d) ? Xf[row * ldf + t] : 0.0f;
+    uint16_t hi, lo;
+    if (split == 1) {
+      const __nv_bfloat16 h = __float2bfloat16_rn(x);
+      const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+      hi = __bfloat16_as_ushort(h);
+      lo = __bfloat16_as_ushort(l);
+    } else {
+      const float xs = x * sc;
+      const __half h = __float2half_rn(xs);
+      const __half l = __float2half_rn(xs - __half2float(h));
+      hi = __half_as_ushort(h);
+      lo = __half_as_ushort(l);
+    }
+    Xhi[row * dp + t] = hi;
+    Xlo[row * dp + t] = lo;
+  }
 }
 
 // diag K(i,i) for the local rows [row0, row0 + nloc), from fp64 squared norms

@@ -16,7 +16,7 @@ _NAMES = {1: "KKM_EINVAL", 2: "KKM_ELABEL", 3: "KKM_ENOMEM", 4: "KKM_EUNSUP", 5:
           6: "KKM_ENCCL", 7: "KKM_ESTATE"}
 KERNEL_LINEAR, KERNEL_POLY, KERNEL_GAUSSIAN = 0, 1, 2
 PATH_AUTO, PATH_MATERIALIZE, PATH_STREAM = 0, 1, 2
-PREC_BF16X3, PREC_FP32_SIMT = 0, 1
+PREC_BF16X3, PREC_FP32_SIMT, PREC_FP16X3 = 0, 1, 2
 DBG_E, DBG_CNORM, DBG_SIZES, DBG_DIAG, DBG_DFULL, DBG_LABELS_PREV = range(6)
 PHASES = ("init_prep", "init_gemm", "spmm", "cnorm", "assign")
 
@@ -135,7 +135,7 @@ class KernelKMeans:
     def __init__(self, X_local, n: int, k: int, kind: int = KERNEL_POLY, gamma: float = 1.0,
                  coef0: float = 1.0, degree: int = 2, max_iter: int = 100,
                  stop_on_no_change: bool = False, path: int = PATH_AUTO,
-                 precision: int = PREC_BF16X3, timing: bool = False, init_labels=None,
+                 precision: int = PREC_FP16X3, timing: bool = False, init_labels=None,
                  rank: int = 0, nranks: int = 1, comm=None, stream=None, device=None,
                  workspace=None):
         import torch

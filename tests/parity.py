@@ -9,12 +9,19 @@ relative in the stated GPU precision"), with "relative" made well defined near z
           minimum (a near tie: "identical except for points whose best/second-best gap is
           below that tolerance")
   sizes:  bit-exact when the labels are identical
-  J:      |dJ| <= 1e-5 * max(|J|, 1e-9 tr K)   ("final objective within 1e-5 relative")
+  J:      |dJ| <= max(1e-5 |J|, 1e-7 tr K)   ("final objective within 1e-5 relative"; the
+          floor is the fp32 storage error of K (the paper's precision), ~2^-24 per
+          entry: J = sum_i (K_ii - z_i) carries ~6e-8 tr K of rounding, so relative error is
+          meaningless as J -> 0, e.g. k = n singletons where J = 0 exactly)
 """
 import numpy as np
 
 TAU = 1e-4
 TAU_J = 1e-5
+
+
+def j_tol(J, diag):
+    return max(TAU_J * abs(J), 1e-7 * float(np.sum(np.abs(diag))))
 
 
 def check_kernel_values(Kg, Kr, diag_rows, diag_cols, tau=TAU):
@@ -65,8 +72,6 @@ def check_iteration(gpu, ref, diag, tau=TAU, rows=None):
     nmis = check_labels(gpu["new_labels"], ref["new_labels"], ref["Dfull"], scale, tau)
     if "sizes" in gpu and "sizes" in ref:
         assert np.array_equal(np.asarray(gpu["sizes"]), np.asarray(ref["sizes"]))
-    if "J" in gpu and "J" in ref:
-        trK = float(np.sum(diag)) if rows is None else None
-        tol = TAU_J * max(abs(ref["J"]), 1e-9 * (trK or abs(ref["J"])))
-        assert abs(gpu["J"] - ref["J"]) <= tol, (gpu["J"], ref["J"])
+    if "J" in gpu and "J" in ref and rows is None:
+        assert abs(gpu["J"] - ref["J"]) <= j_tol(ref["J"], diag), (gpu["J"], ref["J"])
     return nmis

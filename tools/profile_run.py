@@ -1,0 +1,25 @@
+"""One clustering run of a BASELINE config for profiling (ncu) and error studies."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2601_17136_b200 as kkm  # noqa: E402
+import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="mnist60k")
+ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--precision", default="fp16x3")
+a = ap.parse_args()
+X, cfg = synth.make_config(a.config, n=a.n or None)
+prec = {"fp16x3": kkm.PREC_FP16X3, "bf16x3": kkm.PREC_BF16X3, "fp32": kkm.PREC_FP32_SIMT}[a.precision]
+h = kkm.KernelKMeans(torch.from_numpy(X).cuda(), X.shape[0], cfg["k"], cfg["kind"], cfg["gamma"],
+                     cfg["coef0"], cfg["degree"], max_iter=a.iters, precision=prec, timing=True)
+it, J, ch = h.fit()
+torch.cuda.synchronize()
+print("iters", it, "J", J[-1], "phases", h.phase_ms())
