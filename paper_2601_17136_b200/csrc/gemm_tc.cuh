@@ -5,13 +5,15 @@
 //
 // Kernel anatomy: persistent, one CTA per SM, warp-specialised.
 //   warp 0      TMA producer: per 64-wide K block loads A_hi, A_lo (128 rows) and B_hi,
-//               B_lo (256 rows) into a 2-stage smem ring (128B-swizzled, K-major)
+//               B_lo (256 rows) into a 2-stage smem ring (128B-swizzled, K-major), L2
+//               evict-last so the operands stay resident while K streams out
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
-//               M=128 N=256 K=16, 12 per K block (4 k-steps x 3 products), into one of
-//               two TMEM accumulators (2 x 256 fp32 columns = all 512), and releases
-//               smem stages / publishes accumulators with tcgen05.commit -> mbarrier
-//   warps 2..5  epilogue: tcgen05.ld 32x32b (thread = row), kappa in registers, fp32
-//               stores of the K tile; the other accumulator is being filled meanwhile.
+//               M=128 N=256 K=16, 12 per K block (4 k-steps x 3 products), hi*hi into the
+//               main TMEM accumulator and hi*lo + lo*hi into a correction accumulator;
+//               tcgen05.commit -> mbarrier releases smem stages / publishes the tile
+//   warps 2..9  epilogue: tcgen05.ld 32x32b (thread = row, 8 warps = 4 lane quarters x 2
+//               column halves), main + correction, kappa, 128B-swizzled smem staging and
+//               TMA bulk-tensor stores (L2 evict-first) of 32x32 fp32 boxes of K.
 #pragma once
 #include <cuda.h>
 
@@ -23,11 +25,9 @@ constexpr int TC_BM = 128;   // UMMA M (rows of K per tile)
 constexpr int TC_BN = 256;   // UMMA N (columns of K per tile)
 constexpr int TC_BK = 64;    // K block = one 128-byte swizzle atom of bf16
 constexpr int TC_STAGES = 2;
-constexpr int TC_THREADS = 192;
 constexpr uint32_t TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
 constexpr uint32_t TC_B_BYTES = TC_BN * TC_BK * 2;  // 32 KB
 constexpr uint32_t TC_STAGE_BYTES = 2 * TC_A_BYTES + 2 * TC_B_BYTES;  // 96 KB
-constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TC_GROUP_M = 8;  // tile raster: groups of 8 row tiles sweep the column tiles
 
 // instruction descriptor, kind::f16: D fp32, A/B bf16 (format 1) or fp16 (format 0), both
@@ -109,23 +109,64 @@ __device__ __forceinline__ void tc_tile_coords(int64_t t, int tiles_m, int tiles
   tn = (int)(r / gm);
 }
 
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void tma_load_2d_hint(void *smem_dst, const CUtensorMap *map, int c0, int c1,
+                                                 uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int c1, const void *smem_src,
+                                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(smem_src)), "l"(pol)
+      : "memory");
+}
+
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_THREADS_V2 = (2 + TC_EPI_WARPS) * 32;
+constexpr uint32_t TC_STAGING_BYTES = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
+constexpr size_t TC_SMEM_V2 = (size_t)TC_STAGES * TC_STAGE_BYTES + TC_EPI_WARPS * TC_STAGING_BYTES +
+                              1024 /*align*/ + 128 /*barriers*/;
+
 // out[(i - i0) * ldo + (j - j0)] = kappa(x_i . x_j), i in [i0, i0+m), j in [j0, j0+ncov),
-// 0 for j >= n. A rows start at i0, B rows at j0 (global point indices). rscale (fp16 split,
-// else NULL): x_i . x_j = acc * rscale[i] * rscale[j], exact powers of two.
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// 0 for j >= n, written by TMA stores through `tm_out` (an fp32 [m x ncov] view of out).
+// A rows start at i0, B rows at j0 (global point indices). rscale (fp16 split, else NULL):
+// x_i . x_j = acc * rscale[i] * rscale[j], exact powers of two.
+// TMEM: the hi*hi products accumulate in columns [0, 256), the small hi*lo + lo*hi
+// corrections in [256, 512): the tensor core's fp32 accumulation truncates once per MMA
+// relative to the running sum, so keeping the corrections out of the main sum cuts the
+// one-signed error of b by ~3x; the two are added in fp32 (RN).
+__global__ void __launch_bounds__(TC_THREADS_V2, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
-                   uint32_t idesc, int nkb, int64_t n, int64_t i0, int64_t m, int64_t j0,
-                   int64_t ncov, const float *__restrict__ norms, const float *__restrict__ rscale,
-                   KappaParams kp, float *__restrict__ out, int64_t ldo, int tiles_m, int tiles_n) {
+                   const __grid_constant__ CUtensorMap tm_out, uint32_t idesc, int nkb, int64_t n,
+                   int64_t i0, int64_t m, int64_t j0, int64_t ncov, const float *__restrict__ norms,
+                   const float *__restrict__ rscale, KappaParams kp, int tiles_m, int tiles_n) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   uint8_t *smem = smem_raw + pad;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * TC_STAGE_BYTES);
+  uint8_t *staging = smem + TC_STAGES * TC_STAGE_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(staging + TC_EPI_WARPS * TC_STAGING_BYTES);
   uint64_t *empty = full + TC_STAGES;
-  uint64_t *tfull = empty + TC_STAGES;  // [2] accumulator ready
-  uint64_t *tempty = tfull + 2;         // [2] accumulator drained
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *tfull = empty + TC_STAGES;  // accumulators ready
+  uint64_t *tempty = tfull + 1;         // accumulators drained
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (int64_t)tiles_m * tiles_n;
@@ -135,13 +176,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
-    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, TC_EPI_WARPS);
     fence_barrier_init();
   }
-  if (warp == 1) {  // TMEM: 512 columns = two 128 x 256 fp32 accumulators
+  if (warp == 1) {  // TMEM: 512 columns = main (hi*hi) + correction 128 x 256 fp32 accumulators
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
@@ -155,6 +194,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      const uint64_t keep = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -167,12 +207,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t *st = smem + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], TC_STAGE_BYTES);
           const int kc = kb * TC_BK;
-          tma_load_2d(st, &tm_hi, kc, ra, &full[stage]);                                 // A_hi
-          tma_load_2d(st + TC_A_BYTES, &tm_lo, kc, ra, &full[stage]);                    // A_lo
-          tma_load_2d(st + 2 * TC_A_BYTES, &tm_hi, kc, rb, &full[stage]);                // B_hi
-          tma_load_2d(st + 2 * TC_A_BYTES + TC_A_BYTES, &tm_hi, kc, rb + 128, &full[stage]);
-          tma_load_2d(st + 2 * TC_A_BYTES + TC_B_BYTES, &tm_lo, kc, rb, &full[stage]);   // B_lo
-          tma_load_2d(st + 2 * TC_A_BYTES + TC_B_BYTES + TC_A_BYTES, &tm_lo, kc, rb + 128, &full[stage]);
+          tma_load_2d_hint(st, &tm_hi, kc, ra, &full[stage], keep);                          // A_hi
+          tma_load_2d_hint(st + TC_A_BYTES, &tm_lo, kc, ra, &full[stage], keep);             // A_lo
+          tma_load_2d_hint(st + 2 * TC_A_BYTES, &tm_hi, kc, rb, &full[stage], keep);         // B_hi
+          tma_load_2d_hint(st + 3 * TC_A_BYTES, &tm_hi, kc, rb + 128, &full[stage], keep);
+          tma_load_2d_hint(st + 2 * TC_A_BYTES + TC_B_BYTES, &tm_lo, kc, rb, &full[stage], keep);  // B_lo
+          tma_load_2d_hint(st + 3 * TC_A_BYTES + TC_B_BYTES, &tm_lo, kc, rb + 128, &full[stage], keep);
           if (++stage == TC_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -186,12 +226,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int64_t it = 0;
+      const uint32_t d_main = tmem_base, d_corr = tmem_base + (uint32_t)TC_BN;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int acc = (int)(it & 1);
-        const uint32_t acc_phase = (uint32_t)((it >> 1) & 1);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait(tempty, (uint32_t)(it & 1) ^ 1u);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -200,11 +238,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint32_t b_hi = st + 2 * TC_A_BYTES, b_lo = b_hi + TC_B_BYTES;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
-            const uint32_t ko = (uint32_t)k * 32u;  // 16 bf16 = 32 bytes along K inside the atom
-            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
-            umma_f16(d_tmem, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_hi + ko), idesc, first);
-            umma_f16(d_tmem, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_lo + ko), idesc, 1u);
-            umma_f16(d_tmem, umma_desc_sw128(a_lo + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
+            const uint32_t ko = (uint32_t)k * 32u;  // 16 elements = 32 bytes along K in the atom
+            const uint32_t acc = (kb == 0 && k == 0) ? 0u : 1u;
+            umma_f16(d_corr, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_lo + ko), idesc, acc);
+            umma_f16(d_corr, umma_desc_sw128(a_lo + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
+            umma_f16(d_main, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_hi + ko), idesc, acc);
           }
           umma_commit(&empty[stage]);  // smem stage free once these MMAs have read it
           if (++stage == TC_STAGES) {
@@ -212,58 +250,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator complete
+        umma_commit(tfull);  // accumulators complete
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------------------ epilogue (warps 2..9)
+    const int e = warp - 2;
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
-    const int row_in_tile = quarter * 32 + lane;
-    const bool vec_ok = ((ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    const int half = e >> 2;       // tile columns [128*half, 128*half + 128)
+    uint8_t *stg = staging + e * TC_STAGING_BYTES;
+    const uint64_t evict = l2_policy_evict_first();
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       int tm, tn;
       tc_tile_coords(t, tiles_m, tiles_n, tm, tn);
-      const int acc = (int)(it & 1);
-      const uint32_t acc_phase = (uint32_t)((it >> 1) & 1);
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait(tfull, (uint32_t)(it & 1));
       tc_fence_after();
-      const int64_t i = i0 + (int64_t)tm * TC_BM + row_in_tile;
-      const bool row_ok = i < i0 + m;
-      const float ni = row_ok && i < n ? norms[i] : 0.f;
-      const float rsi = (rscale && row_ok && i < n) ? rscale[i] : 1.f;
-      const int64_t jt = j0 + (int64_t)tn * TC_BN;
-      float *orow = out + (i - i0) * ldo;
+      const int64_t ibase = i0 + (int64_t)tm * TC_BM + quarter * 32;  // first row of this warp
+      const int64_t i = ibase + lane;
+      const bool row_ok = i < i0 + m && i < n;
+      const float ni = row_ok ? norms[i] : 0.f;
+      const float rsi = (rscale && row_ok) ? rscale[i] : 1.f;
 #pragma unroll 1
-      for (int c = 0; c < TC_BN / 32; ++c) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
-        const int64_t jb = jt + c * 32;
-        if (!row_ok || jb >= j0 + ncov) continue;
+      for (int c = 0; c < 4; ++c) {
+        const int col = half * 128 + c * 32;  // column offset inside the tile
+        const int64_t jb = j0 + (int64_t)tn * TC_BN + col;
+        float v[32], u[32];
+        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16);
+        tmem_ld32(tq + (uint32_t)col, v);
+        tmem_ld32(tq + (uint32_t)(TC_BN + col), u);
+        if (jb >= j0 + ncov) continue;  // whole chunk outside the requested columns
+        const bool full_cols = jb + 32 <= n;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
           const int64_t j = jb + q;
-          if (j < n && i < n) {
-            const float b = rscale ? v[q] * rsi * __ldg(rscale + j) : v[q];
-            v[q] = kappa_epilogue(kp, b, ni, kp.kind == 2 ? __ldg(norms + j) : 0.f, i == j);
-          } else {
-            v[q] = 0.f;
-          }
+          float b = v[q] + u[q];
+          if (rscale) b *= rsi * __ldg(rscale + (full_cols || j < n ? j : 0));
+          const float nj = kp.kind == 2 ? __ldg(norms + (full_cols || j < n ? j : 0)) : 0.f;
+          const float kv = kappa_epilogue(kp, b, ni, nj, i == j);
+          v[q] = (row_ok && (full_cols || j < n)) ? kv : 0.f;
         }
-        if (vec_ok && jb + 32 <= j0 + ncov) {
-          float4 *o4 = reinterpret_cast<float4 *>(orow + (jb - j0));
+        // previous TMA store from this staging buffer must have finished reading it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
 #pragma unroll
-          for (int q = 0; q < 8; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (jb + q < j0 + ncov) orow[jb + q - j0] = v[q];
+        for (int u4 = 0; u4 < 8; ++u4) {  // 128B-swizzled row: 16B chunk u4 at (u4 ^ (row & 7))
+          float4 *dst = reinterpret_cast<float4 *>(stg + lane * 128 + ((u4 ^ (lane & 7)) << 4));
+          *dst = make_float4(v[4 * u4], v[4 * u4 + 1], v[4 * u4 + 2], v[4 * u4 + 3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tm_out, (int)(jb - j0), (int)(ibase - i0), stg, evict);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) mbar_arrive(tempty);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (warp == 1) {
@@ -277,6 +323,7 @@ struct TcGemm {
   const void *hi = nullptr, *lo = nullptr;  // operands the tensor maps describe
   bool fp16 = false;
   CUtensorMap map_hi, map_lo;
+  CUtensorMap map_out;                        // re-encoded per launch (cheap, host only)
   bool attr = false;
   int num_sms = 0;
 };
@@ -287,9 +334,14 @@ inline const char *&tc_err_slot() {
 }
 inline const char *tc_gemm_error() { return tc_err_slot(); }
 
+inline PFN_cuTensorMapEncodeTiled_v12000 &tc_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+  return f;
+}
+
 inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16, int64_t rows,
                         int64_t dp) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  PFN_cuTensorMapEncodeTiled_v12000 &encode = tc_encode_fn();
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) !=
@@ -320,8 +372,25 @@ inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, boo
   return 0;
 }
 
+// fp32 [m x ncov] view of out (row pitch ldo floats, a multiple of 4) for the TMA stores.
+inline int tc_make_out_map(TcGemm &g, float *out, int64_t m, int64_t ncov, int64_t ldo) {
+  cuuint64_t dims[2] = {(cuuint64_t)ncov, (cuuint64_t)m};
+  cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
+  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = tc_encode_fn()(&g.map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)out, dims, strides,
+                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    tc_err_slot() = "cuTensorMapEncodeTiled (output) failed";
+    return 1;
+  }
+  return 0;
+}
+
 // Launch over [i0, i0+m) x [j0, j0+ncov). rows = padded row count of Xhi/Xlo, dp = padded d.
-// fp16: operands are the scaled fp16 split (rscale given), else the bf16 split.
+// fp16: operands are the scaled fp16 split (rscale given), else the bf16 split. out must be
+// 16-byte aligned with ldo % 4 == 0 (TMA store).
 inline int tc_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16,
                           const float *rscale, int64_t rows, int64_t dp, int64_t n, int64_t i0,
                           int64_t m, int64_t j0, int64_t ncov, const float *norms,
@@ -329,8 +398,13 @@ inline int tc_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, b
                           int64_t *launches) {
   if (g.hi != Xhi || g.lo != Xlo || g.fp16 != fp16)
     if (tc_make_maps(g, Xhi, Xlo, fp16, rows, dp)) return 1;
+  if ((ldo & 3) || (reinterpret_cast<uintptr_t>(out) & 15)) {
+    tc_err_slot() = "tcgen05 GEMM output needs 16-byte alignment and ldo % 4 == 0";
+    return 1;
+  }
+  if (tc_make_out_map(g, out, m, ncov, ldo)) return 1;
   if (!g.attr) {
-    if (cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM) !=
+    if (cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM_V2) !=
         cudaSuccess) {
       tc_err_slot() = "cudaFuncSetAttribute(tc_gemm_kernel) failed";
       return 1;
@@ -344,9 +418,9 @@ inline int tc_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, b
   const int tiles_n = (int)((ncov + TC_BN - 1) / TC_BN);
   const int64_t ntiles = (int64_t)tiles_m * tiles_n;
   const int grid = (int)(ntiles < g.num_sms ? ntiles : g.num_sms);
-  tc_gemm_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(g.map_hi, g.map_lo, tc_idesc(fp16), (int)(dp / TC_BK),
-                                                    n, i0, m, j0, ncov, norms, fp16 ? rscale : nullptr,
-                                                    kp, out, ldo, tiles_m, tiles_n);
+  tc_gemm_kernel<<<grid, TC_THREADS_V2, TC_SMEM_V2, st>>>(g.map_hi, g.map_lo, g.map_out, tc_idesc(fp16),
+                                                          (int)(dp / TC_BK), n, i0, m, j0, ncov, norms,
+                                                          fp16 ? rscale : nullptr, kp, tiles_m, tiles_n);
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -609,9 +609,14 @@ int kkm_kernel_tile(kkm_handle h, int64_t i0, int64_t j0, int32_t m, int32_t nc,
   if (m < 1 || nc < 1 || i0 < 0 || j0 < 0 || i0 + m > P.n || j0 + nc > P.n)
     return fail(KKM_EINVAL, "tile out of range");
   float *tmp = nullptr;
-  CK(cudaMallocAsync((void **)&tmp, (size_t)m * nc * 4, h->st));
-  int rc = launch_gemm(h, i0, m, j0, nc, tmp, nc);
-  if (rc == KKM_OK) rc = copy_any(h, dst, tmp, (size_t)m * nc * 4);
+  const int64_t ldt = round_up(nc, 4);  // TMA-store pitch
+  CK(cudaMallocAsync((void **)&tmp, (size_t)m * ldt * 4, h->st));
+  int rc = launch_gemm(h, i0, m, j0, nc, tmp, ldt);
+  if (rc == KKM_OK) {
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)nc * 4, tmp, (size_t)ldt * 4, (size_t)nc * 4, m,
+                                      cudaMemcpyDefault, h->st);
+    if (e != cudaSuccess) rc = fail(KKM_ECUDA, "kernel_tile copy: %s", cudaGetErrorString(e));
+  }
   cudaFreeAsync(tmp, h->st);
   if (rc) return rc;
   CK(cudaStreamSynchronize(h->st));

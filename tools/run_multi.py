@@ -1,0 +1,51 @@
+"""Multi-GPU (NCCL, 1D) parity check, launched with torchrun on N GPUs: every rank runs the
+C-ABI with its row shard; rank 0 compares against the single-GPU run and the oracle."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import paper_2601_17136_b200 as kkm  # noqa: E402
+import synth  # noqa: E402
+
+world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+uid = [kkm.get_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(uid, src=0)
+comm = kkm.comm_init(world, rank, uid[0])
+ok = True
+for name, n, iters in [("har200k", 3001, 6), ("mnist60k", 2500, 5), ("rings", 1000, 10)]:
+    X, cfg = synth.make_config(name, n=n)
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    r0, r1 = kkm.shard_begin(n, rank, world), kkm.shard_begin(n, rank + 1, world)
+    h = kkm.KernelKMeans(torch.from_numpy(X[r0:r1]).cuda(), n, cfg["k"], *args, max_iter=iters,
+                         rank=rank, nranks=world, comm=comm)
+    it, J, ch = h.fit()
+    lab = h.assign().cpu().numpy()
+    cn = h.debug_read(kkm.DBG_CNORM)
+    gl = [None] * world
+    dist.all_gather_object(gl, (lab, cn, J))
+    if rank == 0:
+        same = all(np.array_equal(g[0], lab) and np.array_equal(g[1], cn) and np.array_equal(g[2], J)
+                   for g in gl)
+        one = kkm.KernelKMeans(torch.from_numpy(X).cuda(), n, cfg["k"], *args, max_iter=iters)
+        it1, J1, _ = one.fit()
+        lab1 = one.assign().cpu().numpy()
+        ref = oracle.fit(X, cfg["k"], *args, max_iter=iters)
+        msg = (f"{name} n={n} P={world}: ranks identical={same} labels==1gpu {np.array_equal(lab, lab1)} "
+               f"labels==oracle {np.array_equal(lab, ref['labels'])} "
+               f"maxrel J vs 1gpu {np.max(np.abs(J - J1) / np.abs(J1)):.2e} "
+               f"vs oracle {np.max(np.abs(J - ref['J_trace']) / np.abs(ref['J_trace'])):.2e}")
+        print(msg, flush=True)
+        ok &= same and np.array_equal(lab, lab1)
+    h.destroy()
+    dist.barrier()
+kkm.comm_destroy(comm)
+dist.destroy_process_group()
+if rank == 0:
+    print("MULTI OK" if ok else "MULTI FAIL")
