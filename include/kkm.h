@@ -58,9 +58,11 @@ extern "C" {
 #define KKM_KERNEL_GAUSSIAN 2 /* kappa(x,y) = exp(-gamma ||x - y||^2)  (A1)     */
 
 /* ---- where K lives ------------------------------------------------------ */
-#define KKM_PATH_AUTO 0        /* materialise if it fits the workspace budget  */
-#define KKM_PATH_MATERIALIZE 1 /* K rows of this rank stored fp32 in HBM once  */
-#define KKM_PATH_STREAM 2      /* K tiles recomputed every iteration (reserved) */
+#define KKM_PATH_AUTO 0        /* materialise if the K block fits 160 GB, else stream         */
+#define KKM_PATH_MATERIALIZE 1 /* K rows of this rank stored fp32 in HBM once               */
+#define KKM_PATH_STREAM 2      /* K tiles recomputed every iteration by the fused tensor-core
+                                  kernel and reduced in TMEM/registers; K never stored.
+                                  Needs FP16X3/BF16X3 and k <= 16 (else KKM_EUNSUP)        */
 
 /* ---- precision of the a1 contraction (reading A9) ----------------------- */
 #define KKM_PREC_BF16X3 0    /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi, bf16 split of x;

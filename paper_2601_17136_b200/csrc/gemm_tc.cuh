@@ -12,8 +12,9 @@
 //               main TMEM accumulator and hi*lo + lo*hi into a correction accumulator;
 //               tcgen05.commit -> mbarrier releases smem stages / publishes the tile
 //   warps 2..9  epilogue: tcgen05.ld 32x32b (thread = row, 8 warps = 4 lane quarters x 2
-//               column halves), main + correction, kappa, 128B-swizzled smem staging and
-//               TMA bulk-tensor stores (L2 evict-first) of 32x32 fp32 boxes of K.
+//               column halves), main + correction, per-column factors from smem (LDS.128
+//               broadcast), kappa, 64B-swizzled smem staging and TMA bulk-tensor stores
+//               (L2 evict-first) of 32x16 fp32 boxes of K.
 #pragma once
 #include <cuda.h>
 
@@ -28,7 +29,7 @@ constexpr int TC_STAGES = 2;
 constexpr uint32_t TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
 constexpr uint32_t TC_B_BYTES = TC_BN * TC_BK * 2;  // 32 KB
 constexpr uint32_t TC_STAGE_BYTES = 2 * TC_A_BYTES + 2 * TC_B_BYTES;  // 96 KB
-constexpr int TC_GROUP_M = 8;  // tile raster: groups of 8 row tiles sweep the column tiles
+constexpr int TC_GROUP_M = 32;  // tile raster: groups of 32 row tiles sweep the column tiles
 
 // instruction descriptor, kind::f16: D fp32, A/B bf16 (format 1) or fp16 (format 0), both
 // K-major, N = 256, M = 128
@@ -79,22 +80,50 @@ __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
-// 32 consecutive fp32 columns of this thread's TMEM lane.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+// 32 consecutive fp32 columns of this thread's TMEM lane (no wait: call tmem_wait_ld()
+// before reading v).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
       "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
       "%30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
-        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
-        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
+        "=f"(v[14]), "=f"(v[15]), "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]),
+        "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]), "=f"(v[25]), "=f"(v[26]), "=f"(v[27]),
+        "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// main + correction accumulators of 32 columns, summed (fp32 RN).
+__device__ __forceinline__ void tmem_ld_sum32(uint32_t t_main, uint32_t t_corr, float (&v)[32]) {
+  float w[32];
+  tmem_ld32_nowait(t_main, v);
+  tmem_ld32_nowait(t_corr, w);
+  tmem_wait_ld();
 #pragma unroll
-  for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
+  for (int q = 0; q < 32; ++q) v[q] += w[q];
+}
+
+// Lane-parallel load of 128 per-column constants (norm_j, rscale_j) of columns [j, j+128) into
+// smem cn[0..128) / cn[128..256); missing columns get (0, 1). Ends with __syncwarp.
+__device__ __forceinline__ void stage_column_constants(float *cn, const float *__restrict__ norms,
+                                                       const float *__restrict__ rscale, int64_t j,
+                                                       int64_t nvalid, bool need_norm, int lane) {
+  const int64_t p = j + lane * 4;
+  float4 nv = make_float4(0.f, 0.f, 0.f, 0.f), rv = make_float4(1.f, 1.f, 1.f, 1.f);
+  float *pn = &nv.x, *pr = &rv.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (p + q < nvalid) {
+      if (need_norm) pn[q] = __ldg(norms + p + q);
+      if (rscale) pr[q] = __ldg(rscale + p + q);
+    }
+  __syncwarp();
+  reinterpret_cast<float4 *>(cn)[lane] = nv;
+  reinterpret_cast<float4 *>(cn + 128)[lane] = rv;
+  __syncwarp();
 }
 
 // Tile t -> (row tile, column tile): groups of TC_GROUP_M row tiles, column-major inside a
@@ -140,9 +169,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int
 
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS_V2 = (2 + TC_EPI_WARPS) * 32;
-constexpr uint32_t TC_STAGING_BYTES = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
-constexpr size_t TC_SMEM_V2 = (size_t)TC_STAGES * TC_STAGE_BYTES + TC_EPI_WARPS * TC_STAGING_BYTES +
-                              1024 /*align*/ + 128 /*barriers*/;
+constexpr uint32_t TC_STAGING_BYTES = 32 * 16 * 4;  // per epilogue warp: 32 rows x 16 fp32 (SW64 box)
+constexpr uint32_t TC_COLC_BYTES = 256 * 4;          // per epilogue warp: 128 x (norm_j, rscale_j)
+constexpr size_t TC_SMEM_V2 = (size_t)TC_STAGES * TC_STAGE_BYTES +
+                              TC_EPI_WARPS * (TC_STAGING_BYTES + TC_COLC_BYTES) + 1024 /*align*/ +
+                              128 /*barriers*/;
 
 // out[(i - i0) * ldo + (j - j0)] = kappa(x_i . x_j), i in [i0, i0+m), j in [j0, j0+ncov),
 // 0 for j >= n, written by TMA stores through `tm_out` (an fp32 [m x ncov] view of out).
@@ -162,7 +193,8 @@ __global__ void __launch_bounds__(TC_THREADS_V2, 1)
   const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
   uint8_t *smem = smem_raw + pad;
   uint8_t *staging = smem + TC_STAGES * TC_STAGE_BYTES;
-  uint64_t *full = reinterpret_cast<uint64_t *>(staging + TC_EPI_WARPS * TC_STAGING_BYTES);
+  float *colc = reinterpret_cast<float *>(staging + TC_EPI_WARPS * TC_STAGING_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(staging + TC_EPI_WARPS * (TC_STAGING_BYTES + TC_COLC_BYTES));
   uint64_t *empty = full + TC_STAGES;
   uint64_t *tfull = empty + TC_STAGES;  // accumulators ready
   uint64_t *tempty = tfull + 1;         // accumulators drained
@@ -259,50 +291,60 @@ __global__ void __launch_bounds__(TC_THREADS_V2, 1)
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
     const int half = e >> 2;       // tile columns [128*half, 128*half + 128)
     uint8_t *stg = staging + e * TC_STAGING_BYTES;
+    float *cn = colc + e * 256;
     const uint64_t evict = l2_policy_evict_first();
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       int tm, tn;
       tc_tile_coords(t, tiles_m, tiles_n, tm, tn);
-      mbar_wait(tfull, (uint32_t)(it & 1));
-      tc_fence_after();
       const int64_t ibase = i0 + (int64_t)tm * TC_BM + quarter * 32;  // first row of this warp
       const int64_t i = ibase + lane;
       const bool row_ok = i < i0 + m && i < n;
       const float ni = row_ok ? norms[i] : 0.f;
       const float rsi = (rscale && row_ok) ? rscale[i] : 1.f;
+      const int64_t jw = j0 + (int64_t)tn * TC_BN + half * 128;  // first column of this warp
+      stage_column_constants(cn, norms, rscale, jw, n, kp.kind == 2, lane);
+      mbar_wait(tfull, (uint32_t)(it & 1));
+      tc_fence_after();
+      const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         const int col = half * 128 + c * 32;  // column offset inside the tile
-        const int64_t jb = j0 + (int64_t)tn * TC_BN + col;
-        float v[32], u[32];
-        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16);
-        tmem_ld32(tq + (uint32_t)col, v);
-        tmem_ld32(tq + (uint32_t)(TC_BN + col), u);
+        const int64_t jb = jw + c * 32;
+        float v[32];
+        tmem_ld_sum32(tq + (uint32_t)col, tq + (uint32_t)(TC_BN + col), v);
         if (jb >= j0 + ncov) continue;  // whole chunk outside the requested columns
-        const bool full_cols = jb + 32 <= n;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int64_t j = jb + q;
-          float b = v[q] + u[q];
-          if (rscale) b *= rsi * __ldg(rscale + (full_cols || j < n ? j : 0));
-          const float nj = kp.kind == 2 ? __ldg(norms + (full_cols || j < n ? j : 0)) : 0.f;
-          const float kv = kappa_epilogue(kp, b, ni, nj, i == j);
-          v[q] = (row_ok && (full_cols || j < n)) ? kv : 0.f;
-        }
-        // previous TMA store from this staging buffer must have finished reading it
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 nj = reinterpret_cast<const float4 *>(cn + c * 32)[q4];
+          const float4 rj = reinterpret_cast<const float4 *>(cn + 128 + c * 32)[q4];
+          const float njs[4] = {nj.x, nj.y, nj.z, nj.w}, rjs[4] = {rj.x, rj.y, rj.z, rj.w};
 #pragma unroll
-        for (int u4 = 0; u4 < 8; ++u4) {  // 128B-swizzled row: 16B chunk u4 at (u4 ^ (row & 7))
-          float4 *dst = reinterpret_cast<float4 *>(stg + lane * 128 + ((u4 ^ (lane & 7)) << 4));
-          *dst = make_float4(v[4 * u4], v[4 * u4 + 1], v[4 * u4 + 2], v[4 * u4 + 3]);
+          for (int u = 0; u < 4; ++u) {
+            const int q = 4 * q4 + u;
+            const int64_t j = jb + q;
+            const float b = rscale ? v[q] * (rsi * rjs[u]) : v[q];
+            const float kv = kappa_epilogue(kp, b, ni, njs[u], i == j);
+            v[q] = (row_ok && j < n) ? kv : 0.f;
+          }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tm_out, (int)(jb - j0), (int)(ibase - i0), stg, evict);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // two 16-column boxes per 32-column chunk
+          // the previous TMA store from this staging buffer must have finished reading it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {  // 64B-swizzled row: 16B chunk u4 at u4 ^ ((row >> 1) & 3)
+            float4 *dst = reinterpret_cast<float4 *>(stg + lane * 64 + ((u4 ^ ((lane >> 1) & 3)) << 4));
+            const int q = hh * 16 + 4 * u4;
+            *dst = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && jb + hh * 16 < j0 + ncov) {
+            tma_store_2d(&tm_out, (int)(jb + hh * 16 - j0), (int)(ibase - i0), stg, evict);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
         }
       }
       tc_fence_before();
@@ -376,10 +418,10 @@ inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, boo
 inline int tc_make_out_map(TcGemm &g, float *out, int64_t m, int64_t ncov, int64_t ldo) {
   cuuint64_t dims[2] = {(cuuint64_t)ncov, (cuuint64_t)m};
   cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
-  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t box[2] = {16u, 32u};
   cuuint32_t es[2] = {1u, 1u};
   CUresult r = tc_encode_fn()(&g.map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)out, dims, strides,
-                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     tc_err_slot() = "cuTensorMapEncodeTiled (output) failed";

@@ -17,7 +17,9 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "prep.cuh"
+#include "sort.cuh"
 #include "spmm.cuh"
+#include "stream.cuh"
 #include "update.cuh"
 
 using namespace kkm;
@@ -44,12 +46,13 @@ struct Plan {
   int64_t n, d, B, row0, nloc, npad, ldf, dp, ldk, lablen;
   int k, nranks, rank, max_iter;
   bool materialize, tc, fp16;  // tc: tensor-core a1 (bf16x3 or fp16x3); fp16: fp16x3 split
+  int sort_blocks;              // streaming: blocks of the counting sort
   int nsplit, chunks_per_split, nfin, nspmm_pass;
   int64_t rows_per_block;
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
-      total;
+      o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -87,18 +90,31 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.tc = p->precision == KKM_PREC_BF16X3 || p->precision == KKM_PREC_FP16X3;
   P.fp16 = p->precision == KKM_PREC_FP16X3;
   const double kbytes = (double)P.B * (double)P.ldk * 4.0;
-  if (p->path == KKM_PATH_STREAM) return fail(KKM_EUNSUP, "the streaming path is not built yet");
-  if (p->path == KKM_PATH_MATERIALIZE || p->path == KKM_PATH_AUTO) {
-    if (p->path == KKM_PATH_AUTO && kbytes > kMaterializeBudget)
-      return fail(KKM_EUNSUP, "K block of %.1f GB exceeds the materialisation budget; streaming not built yet",
-                  kbytes / 1e9);
+  if (p->path == KKM_PATH_MATERIALIZE) {
     P.materialize = true;
+  } else if (p->path == KKM_PATH_STREAM) {
+    P.materialize = false;
+  } else if (p->path == KKM_PATH_AUTO) {
+    P.materialize = kbytes <= kMaterializeBudget;
   } else {
     return fail(KKM_EINVAL, "unknown path %d", p->path);
   }
-  const int64_t nchunks = ceil_div(P.ldk, SP_CH);
-  P.nsplit = (int)ceil_div(nchunks, SP_MAX_CHUNKS_PER_SPLIT);
-  P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
+  if (!P.materialize) {
+    if (!P.tc)
+      return fail(KKM_EUNSUP, "the streaming path needs a tensor-core precision (FP16X3 or BF16X3)");
+    if (P.k > 16) return fail(KKM_EUNSUP, "the streaming path supports k <= 16 (k=%d)", P.k);
+  }
+  if (P.materialize) {
+    const int64_t nchunks = ceil_div(P.ldk, SP_CH);
+    P.nsplit = (int)ceil_div(nchunks, SP_MAX_CHUNKS_PER_SPLIT);
+    P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
+  } else {
+    // work units of the fused kernel = 128-row tiles x column splits; 148 SMs assumed for the
+    // load-balance choice (B200); each split writes one partial per column half
+    P.nsplit = 2 * ts_choose_splits(P.B, P.n, 148);
+    P.chunks_per_split = 0;
+  }
+  P.sort_blocks = (int)ceil_div(P.n, SORT_BLOCK);
   P.nspmm_pass = (int)ceil_div(P.k, SP_KPMAX);
   P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.nloc, 1), FIN_THREADS));
   P.rows_per_block = ceil_div(std::max<int64_t>(P.nloc, 1), P.nfin);
@@ -131,6 +147,17 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.o_bad = take(16);
   P.o_E2 = take((size_t)P.B * P.k * 8);
   P.o_cnorm2 = take((size_t)P.k * 8);
+  if (!P.materialize) {
+    P.o_Shi = take((size_t)P.npad * P.dp * 2);
+    P.o_Slo = take((size_t)P.npad * P.dp * 2);
+    P.o_snorms = take((size_t)P.npad * 4);
+    P.o_srscale = take((size_t)P.npad * 4);
+    P.o_perm = take((size_t)P.lablen * 4);
+    P.o_pos = take((size_t)P.lablen * 4);
+    P.o_seg = take((size_t)(P.k + 1) * 4);
+    P.o_bcount = take((size_t)P.sort_blocks * P.k * 4);
+    P.o_boff = take((size_t)P.sort_blocks * P.k * 4);
+  }
   P.total = off;
   return KKM_OK;
 }
@@ -149,6 +176,11 @@ struct kkm_ctx {
   float *rscale = nullptr;                   // 1 / s_i of the fp16 split
   double *diag, *Spart, *E, *blockpart, *rankpart, *cnorm, *J, *Dfull;
   double *E2, *cnorm2;  // E / c of the final-labels pass (kept apart from the last iteration's)
+  // streaming path: cluster-sorted operands and the sort
+  uint16_t *Shi = nullptr, *Slo = nullptr;
+  float *snorms = nullptr, *srscale = nullptr;
+  int32_t *perm = nullptr, *pos = nullptr, *seg = nullptr, *bcount = nullptr, *boff = nullptr;
+  TcStream ts;
   int32_t *lab[2], *sizes[2];
   unsigned long long *changed;
   int *bad;
@@ -220,9 +252,38 @@ int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
   return KKM_OK;
 }
 
-// a2: S = unnormalised K V^T for the local rows, with the given full label vector.
-int launch_spmm(kkm_ctx *h, const int32_t *labels) {
+// Streaming a1+a2: sort the points by label, gather the split operands in that order, then
+// the fused tensor-core kernel writes S partials (Spart) for the local rows.
+int launch_stream(kkm_ctx *h, const int32_t *labels, const int32_t *sizes) {
   const Plan &P = h->P;
+  const int k = P.k;
+  sort_count_kernel<<<P.sort_blocks, 256, (size_t)k * 4, h->st>>>(labels, P.n, k, h->bcount);
+  CKL();
+  sort_scan_kernel<<<k + 1, 1024, 1024 * 4, h->st>>>(h->bcount, P.sort_blocks, k, sizes, h->boff, h->seg);
+  CKL();
+  sort_scatter_kernel<<<P.sort_blocks, 256, (size_t)9 * k * 4, h->st>>>(labels, P.n, k, h->boff, h->perm,
+                                                                        h->pos);
+  CKL();
+  gather_rows_kernel<<<(unsigned)ceil_div(P.npad, 8), 256, 0, h->st>>>(
+      h->Xhi, h->Xlo, h->norms, h->rscale, h->perm, P.n, P.npad, P.dp, h->Shi, h->Slo, h->snorms,
+      h->srscale);
+  CKL();
+  if (P.nloc == 0) return KKM_OK;
+  int rc = tc_stream_launch(h->ts, h->Xhi, h->Xlo, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, P.row0, P.nloc,
+                            h->norms, h->rscale, h->snorms, h->srscale, h->pos, h->seg, k, h->kp,
+                            P.nsplit / 2, h->Spart, h->st, &h->launches);
+  if (rc) {
+    h->poisoned = true;
+    return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
+  }
+  return KKM_OK;
+}
+
+// a2: S = unnormalised K V^T for the local rows, with the given full label vector (and the
+// sizes of those labels, used by the streaming path's sort).
+int launch_spmm(kkm_ctx *h, const int32_t *labels, const int32_t *sizes) {
+  const Plan &P = h->P;
+  if (!P.materialize) return launch_stream(h, labels, sizes);
   if (P.nloc == 0) return KKM_OK;
   if (P.k > SP_KPMAX) {
     for (int c0 = 0; c0 < P.k; c0 += SP_KPMAX) CKR(launch_spmm_kp<SP_KPMAX>(h, labels, c0));
@@ -394,6 +455,17 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   h->bad = (int *)(w + P.o_bad);
   h->E2 = (double *)(w + P.o_E2);
   h->cnorm2 = (double *)(w + P.o_cnorm2);
+  if (!P.materialize) {
+    h->Shi = (uint16_t *)(w + P.o_Shi);
+    h->Slo = (uint16_t *)(w + P.o_Slo);
+    h->snorms = (float *)(w + P.o_snorms);
+    h->srscale = (float *)(w + P.o_srscale);
+    h->perm = (int32_t *)(w + P.o_perm);
+    h->pos = (int32_t *)(w + P.o_pos);
+    h->seg = (int32_t *)(w + P.o_seg);
+    h->bcount = (int32_t *)(w + P.o_bcount);
+    h->boff = (int32_t *)(w + P.o_boff);
+  }
   h->kp.kind = p->kind;
   h->kp.degree = p->degree;
   h->kp.gamma = (float)p->gamma;
@@ -492,7 +564,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   int t = 0;
   for (t = 0; t < T; ++t) {
     if (timing) CKR(rec(ev));
-    CKR(launch_spmm(h, h->lab[h->cur]));                                  // a2
+    CKR(launch_spmm(h, h->lab[h->cur], h->sizes[h->cur]));              // a2
     if (timing) CKR(rec(ev));
     CKR(run_cnorm(h, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
     if (timing) CKR(rec(ev));
@@ -511,7 +583,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
     }
   }
   // J of the final labels (one more a2 + a3 pass, as the oracle's J_trace[iters])
-  CKR(launch_spmm(h, h->lab[h->cur]));
+  CKR(launch_spmm(h, h->lab[h->cur], h->sizes[h->cur]));
   CKR(run_cnorm(h, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
   std::vector<double> J((size_t)t + 1);
   std::vector<unsigned long long> ch((size_t)std::max(t, 1));
@@ -550,7 +622,7 @@ int kkm_objective(kkm_handle h, double *J) {
   if (!h || !J) return fail(KKM_EINVAL, "NULL argument");
   if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
   double *slot = h->J + h->P.max_iter + 1;
-  CKR(launch_spmm(h, h->lab[h->cur]));
+  CKR(launch_spmm(h, h->lab[h->cur], h->sizes[h->cur]));
   CKR(run_cnorm(h, h->E2, h->cnorm2, slot, nullptr, nullptr));
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));

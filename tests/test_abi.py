@@ -63,13 +63,19 @@ def test_workspace_size_and_errors():
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(q, 100, 4)
     q = kkm.default_params()
-    q.k, q.path = 3, kkm.PATH_STREAM
+    q.k, q.path, q.precision = 3, kkm.PATH_STREAM, kkm.PREC_FP32_SIMT
     with pytest.raises(kkm.KKMError, match="EUNSUP"):
-        kkm.workspace_size(q, 100, 4)
+        kkm.workspace_size(q, 100, 4)  # streaming needs a tensor-core precision
     q = kkm.default_params()
-    q.k = 3
+    q.k, q.path = 17, kkm.PATH_STREAM
     with pytest.raises(kkm.KKMError, match="EUNSUP"):
-        kkm.workspace_size(q, 1_000_000, 784)  # 4 TB of K: too big to materialise
+        kkm.workspace_size(q, 100, 4)  # streaming supports k <= 16
+    q = kkm.default_params()
+    q.k = 10
+    nb_stream = kkm.workspace_size(q, 1_000_000, 784)  # 4 TB of K: AUTO streams
+    assert nb_stream < 20e9
+    q.path = kkm.PATH_STREAM
+    assert kkm.workspace_size(q, 1_000_000, 784) == nb_stream
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(p, 60000, 784, rank=4, nranks=4)
     q = kkm.default_params()
