@@ -98,7 +98,10 @@ typedef struct kkm_params {
   int32_t path;            /* KKM_PATH_*                                           */
   int32_t precision;       /* KKM_PREC_*                                           */
   int32_t timing;          /* 1: record per-phase CUDA-event times (kkm_phase_ms) */
-  int32_t reserved[6];     /* must be zero                                         */
+  int32_t grid_rows;       /* 1.5D process grid pr x (nranks/pr), column-major ranks
+                              (P:604); 0 or 1 = the 1D algorithm (Alg. 1). Must divide
+                              nranks. See kkm_init.                                   */
+  int32_t reserved[5];     /* must be zero                                         */
 } kkm_params;
 
 typedef struct kkm_ctx *kkm_handle;
@@ -119,7 +122,14 @@ int64_t kkm_shard_begin(int64_t n, int32_t rank, int32_t nranks);
 int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks,
                        size_t *bytes);
 
-/* Creates a handle and runs the one-time part of the path:
+/* Creates a handle and runs the one-time part of the path.
+ * Sharding (P = nranks, B = ceil(n / P), pr = grid_rows, pc = P / pr, rank = i + j * pr):
+ *   - rank r owns the 1D block [r B, (r+1) B) of points (its labels, E rows, distances);
+ *   - it computes E partials for the points of column block j = 1D blocks [j pr, (j+1) pr)
+ *     against the points of row block i = 1D blocks [i pc, (i+1) pc) (K_ij of the 2D grid,
+ *     P:440-487), then a ReduceScatter over the pr ranks of process column j leaves each rank
+ *     the full E of its own 1D block (the paper's column-split Reduce-Scatter).
+ *   pr = 1 is the 1D algorithm (column block = own block, row block = all points).
  *   X_local:  rows [kkm_shard_begin(rank), kkm_shard_begin(rank+1)) of X, fp32,
  *             row-major with leading dimension ldx >= d; host or device. It is
  *             read during the call only (copied into the workspace). With

@@ -44,6 +44,10 @@ int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 // Everything the planner derives from (params, n, d, rank, nranks).
 struct Plan {
   int64_t n, d, B, row0, nloc, npad, ldf, dp, ldk, lablen;
+  // 1.5D grid: pr x pc, rank = gi + gj * pr. A set = column block gj (output rows
+  // of the a2 partials), B set = row block gi (reduction columns). pr = 1: A = own rows, B = all.
+  int pr, pc, gi, gj;
+  int64_t a0, nA, nApad, b0, nB;
   int k, nranks, rank, max_iter;
   bool materialize, tc, fp16;  // tc: tensor-core a1 (bf16x3 or fp16x3); fp16: fp16x3 split
   int sort_blocks;              // streaming: blocks of the counting sort
@@ -52,7 +56,8 @@ struct Plan {
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
-      o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, total;
+      o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
+      total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -70,8 +75,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT &&
       p->precision != KKM_PREC_FP16X3)
     return fail(KKM_EINVAL, "unknown precision %d", p->precision);
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 5; ++i)
     if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
+  const int pr = p->grid_rows <= 1 ? 1 : p->grid_rows;
+  if (nranks % pr) return fail(KKM_EUNSUP, "grid_rows=%d does not divide nranks=%d", pr, nranks);
   Plan &P = *pl;
   P.n = n;
   P.d = d;
@@ -83,13 +90,22 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.row0 = std::min<int64_t>(n, (int64_t)rank * P.B);
   P.nloc = std::max<int64_t>(0, std::min<int64_t>(P.B, n - P.row0));
   P.npad = P.B * nranks;
+  P.pr = pr;
+  P.pc = nranks / pr;
+  P.gi = rank % pr;
+  P.gj = rank / pr;
+  P.a0 = std::min<int64_t>(n, (int64_t)P.gj * pr * P.B);
+  P.nA = std::max<int64_t>(0, std::min<int64_t>((int64_t)pr * P.B, n - P.a0));
+  P.nApad = (int64_t)pr * P.B;
+  P.b0 = std::min<int64_t>(n, (int64_t)P.gi * P.pc * P.B);
+  P.nB = std::max<int64_t>(0, std::min<int64_t>((int64_t)P.pc * P.B, n - P.b0));
   P.ldf = round_up(d, 4);
   P.dp = round_up(d, TC_BK);  // bf16 operand rows padded to whole 64-element K blocks
-  P.ldk = round_up(n, 32);
-  P.lablen = round_up(std::max(P.npad, P.ldk), 32);
+  P.ldk = round_up(std::max<int64_t>(P.nB, 1), 32);  // K tile row pitch (columns = B set)
+  P.lablen = round_up(std::max(P.npad, round_up(n, 32)), 32);
   P.tc = p->precision == KKM_PREC_BF16X3 || p->precision == KKM_PREC_FP16X3;
   P.fp16 = p->precision == KKM_PREC_FP16X3;
-  const double kbytes = (double)P.B * (double)P.ldk * 4.0;
+  const double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
   if (p->path == KKM_PATH_MATERIALIZE) {
     P.materialize = true;
   } else if (p->path == KKM_PATH_STREAM) {
@@ -111,10 +127,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   } else {
     // work units of the fused kernel = 128-row tiles x column splits; 148 SMs assumed for the
     // load-balance choice (B200); each split writes one partial per column half
-    P.nsplit = 2 * ts_choose_splits(P.B, P.n, 148);
+    P.nsplit = 2 * ts_choose_splits(P.nA, P.nB, 148);
     P.chunks_per_split = 0;
   }
-  P.sort_blocks = (int)ceil_div(P.n, SORT_BLOCK);
+  P.sort_blocks = (int)ceil_div(std::max<int64_t>(P.nB, 1), SORT_BLOCK);
   P.nspmm_pass = (int)ceil_div(P.k, SP_KPMAX);
   P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.nloc, 1), FIN_THREADS));
   P.rows_per_block = ceil_div(std::max<int64_t>(P.nloc, 1), P.nfin);
@@ -131,12 +147,12 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.o_rscale = take((size_t)P.npad * 4);
   P.o_norms = take((size_t)P.npad * 4);
   P.o_diag = take((size_t)P.B * 8);
-  P.o_K = P.materialize ? take((size_t)P.B * P.ldk * 4) : 0;
+  P.o_K = P.materialize ? take((size_t)P.nApad * P.ldk * 4) : 0;
   P.o_lab[0] = take((size_t)P.lablen * 4);
   P.o_lab[1] = take((size_t)P.lablen * 4);
   P.o_sizes[0] = take((size_t)P.k * 4);
   P.o_sizes[1] = take((size_t)P.k * 4);
-  P.o_Spart = take((size_t)P.nsplit * P.B * P.k * 8);
+  P.o_Spart = take((size_t)P.nsplit * P.nApad * P.k * 8);
   P.o_E = take((size_t)P.B * P.k * 8);
   P.o_blockpart = take((size_t)P.nfin * k1 * 8);
   P.o_rankpart = take((size_t)nranks * k1 * 8);
@@ -157,6 +173,11 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_seg = take((size_t)(P.k + 1) * 4);
     P.o_bcount = take((size_t)P.sort_blocks * P.k * 4);
     P.o_boff = take((size_t)P.sort_blocks * P.k * 4);
+  }
+  if (P.pr > 1) {
+    P.o_labB = take((size_t)P.ldk * 4);
+    P.o_Scol = take((size_t)P.nApad * P.k * 8);
+    P.o_Smine = take((size_t)P.B * P.k * 8);
   }
   P.total = off;
   return KKM_OK;
@@ -181,6 +202,10 @@ struct kkm_ctx {
   float *snorms = nullptr, *srscale = nullptr;
   int32_t *perm = nullptr, *pos = nullptr, *seg = nullptr, *bcount = nullptr, *boff = nullptr;
   TcStream ts;
+  // 1.5D: padded labels of the B set, column-block partials, own-block sums; column comm
+  int32_t *labB = nullptr;
+  double *Scol = nullptr, *Smine = nullptr;
+  ncclComm_t colcomm = nullptr;
   int32_t *lab[2], *sizes[2];
   unsigned long long *changed;
   int *bad;
@@ -244,34 +269,35 @@ int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
                             (int)spmm_smem_bytes()));
     attr_set = true;
   }
-  const int64_t items = ceil_div(P.nloc, SP_ROWS) * P.nsplit;
+  const int64_t items = ceil_div(P.nA, SP_ROWS) * P.nsplit;
   const int grid = (int)std::min<int64_t>(items, h->num_sms);
   spmm_onehot_kernel<KP><<<grid, SP_THREADS, spmm_smem_bytes(), h->st>>>(
-      h->K, P.ldk, P.nloc, labels, P.k, c0, P.nsplit, P.chunks_per_split, h->Spart);
+      h->K, P.ldk, P.nA, labels, P.k, c0, P.nsplit, P.chunks_per_split, P.nApad, h->Spart);
   CKL();
   return KKM_OK;
 }
 
-// Streaming a1+a2: sort the points by label, gather the split operands in that order, then
-// the fused tensor-core kernel writes S partials (Spart) for the local rows.
-int launch_stream(kkm_ctx *h, const int32_t *labels, const int32_t *sizes) {
+// Streaming a1+a2: sort the B set's points by label, gather the split operands in that order,
+// then the fused tensor-core kernel writes S partials (Spart) for the A set's rows.
+int launch_stream(kkm_ctx *h, const int32_t *labels) {
   const Plan &P = h->P;
   const int k = P.k;
-  sort_count_kernel<<<P.sort_blocks, 256, (size_t)k * 4, h->st>>>(labels, P.n, k, h->bcount);
+  const int32_t *labB = labels + P.b0;
+  sort_count_kernel<<<P.sort_blocks, 256, (size_t)k * 4, h->st>>>(labB, P.nB, k, h->bcount);
   CKL();
-  sort_scan_kernel<<<k + 1, 1024, 1024 * 4, h->st>>>(h->bcount, P.sort_blocks, k, sizes, h->boff, h->seg);
+  sort_scan_kernel<<<k + 1, 1024, 1024 * 4, h->st>>>(h->bcount, P.sort_blocks, k, h->boff, h->seg);
   CKL();
-  sort_scatter_kernel<<<P.sort_blocks, 256, (size_t)9 * k * 4, h->st>>>(labels, P.n, k, h->boff, h->perm,
+  sort_scatter_kernel<<<P.sort_blocks, 256, (size_t)9 * k * 4, h->st>>>(labB, P.nB, k, h->boff, h->perm,
                                                                         h->pos);
   CKL();
   gather_rows_kernel<<<(unsigned)ceil_div(P.npad, 8), 256, 0, h->st>>>(
-      h->Xhi, h->Xlo, h->norms, h->rscale, h->perm, P.n, P.npad, P.dp, h->Shi, h->Slo, h->snorms,
+      h->Xhi, h->Xlo, h->norms, h->rscale, h->perm, P.b0, P.nB, P.npad, P.dp, h->Shi, h->Slo, h->snorms,
       h->srscale);
   CKL();
-  if (P.nloc == 0) return KKM_OK;
-  int rc = tc_stream_launch(h->ts, h->Xhi, h->Xlo, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, P.row0, P.nloc,
-                            h->norms, h->rscale, h->snorms, h->srscale, h->pos, h->seg, k, h->kp,
-                            P.nsplit / 2, h->Spart, h->st, &h->launches);
+  if (P.nA == 0) return KKM_OK;
+  int rc = tc_stream_launch(h->ts, h->Xhi, h->Xlo, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.nB, P.b0, P.a0,
+                            P.nA, P.nApad, h->norms, h->rscale, h->snorms, h->srscale, h->pos, h->seg, k,
+                            h->kp, P.nsplit / 2, h->Spart, h->st, &h->launches);
   if (rc) {
     h->poisoned = true;
     return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
@@ -279,12 +305,15 @@ int launch_stream(kkm_ctx *h, const int32_t *labels, const int32_t *sizes) {
   return KKM_OK;
 }
 
-// a2: S = unnormalised K V^T for the local rows, with the given full label vector (and the
-// sizes of those labels, used by the streaming path's sort).
-int launch_spmm(kkm_ctx *h, const int32_t *labels, const int32_t *sizes) {
+// a2 on the materialised K tile (A set rows x B set columns).
+int launch_spmm_mat(kkm_ctx *h, const int32_t *labels) {
   const Plan &P = h->P;
-  if (!P.materialize) return launch_stream(h, labels, sizes);
-  if (P.nloc == 0) return KKM_OK;
+  if (P.nA == 0) return KKM_OK;
+  if (P.pr > 1) {  // the B set's labels, -1 padded to the tile pitch
+    copy_labels_kernel<<<(unsigned)ceil_div(P.ldk, 256), 256, 0, h->st>>>(labels + P.b0, P.nB, P.ldk, h->labB);
+    CKL();
+    labels = h->labB;
+  }
   if (P.k > SP_KPMAX) {
     for (int c0 = 0; c0 < P.k; c0 += SP_KPMAX) CKR(launch_spmm_kp<SP_KPMAX>(h, labels, c0));
     return KKM_OK;
@@ -302,18 +331,38 @@ int launch_spmm(kkm_ctx *h, const int32_t *labels, const int32_t *sizes) {
   }
 }
 
+// a2 + the 1.5D column-split reduce-scatter: afterwards the S partials of this rank's own 1D
+// block are in s_out[nsplit_out][B][k] (the 1D case reduces nothing: s_out = Spart).
+int launch_spmm(kkm_ctx *h, const int32_t *labels, const double **s_out, int *nsplit_out) {
+  const Plan &P = h->P;
+  CKR(P.materialize ? launch_spmm_mat(h, labels) : launch_stream(h, labels));
+  if (P.pr == 1) {
+    *s_out = h->Spart;
+    *nsplit_out = P.nsplit;
+    return KKM_OK;
+  }
+  split_sum_kernel<<<(unsigned)ceil_div(P.nApad * P.k, 256), 256, 0, h->st>>>(h->Spart, P.nsplit, P.nA,
+                                                                              P.nApad, P.k, h->Scol);
+  CKL();
+  // P(i, j) keeps piece i of column block j = its own 1D block (column-major ranks)
+  CKN(ncclReduceScatter(h->Scol, h->Smine, (size_t)P.B * P.k, ncclDouble, ncclSum, h->colcomm, h->st));
+  *s_out = h->Smine;
+  *nsplit_out = 1;
+  return KKM_OK;
+}
+
 // a3: E, z, c (cnorm) and J for the labels entering the iteration -> E_out, cnorm_out,
 // J_out. sizes_next / changed_out (may be NULL) are zeroed for the following assign.
-int run_cnorm(kkm_ctx *h, double *E_out, double *cnorm_out, double *J_out, int32_t *sizes_next,
-              unsigned long long *changed_out) {
+int run_cnorm(kkm_ctx *h, const double *S, int nsplit, double *E_out, double *cnorm_out, double *J_out,
+              int32_t *sizes_next, unsigned long long *changed_out) {
   const Plan &P = h->P;
   const int32_t *labels = h->lab[h->cur];
   const int32_t *sizes = h->sizes[h->cur];
   const int k1 = P.k + 1;
   if (P.nloc > 0) {
     finalize_kernel<<<P.nfin, FIN_THREADS, (size_t)k1 * FIN_THREADS * 8, h->st>>>(
-        h->Spart, P.nsplit, P.nloc, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block, E_out,
-        h->blockpart);
+        S, nsplit, P.nloc, P.pr > 1 ? P.B : P.nApad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
+        E_out, h->blockpart);
     CKL();
   }
   cnorm_local_kernel<<<1, 128, 0, h->st>>>(h->blockpart, P.nloc > 0 ? P.nfin : 0, P.k,
@@ -466,6 +515,11 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->bcount = (int32_t *)(w + P.o_bcount);
     h->boff = (int32_t *)(w + P.o_boff);
   }
+  if (P.pr > 1) {
+    h->labB = (int32_t *)(w + P.o_labB);
+    h->Scol = (double *)(w + P.o_Scol);
+    h->Smine = (double *)(w + P.o_Smine);
+  }
   h->kp.kind = p->kind;
   h->kp.degree = p->degree;
   h->kp.gamma = (float)p->gamma;
@@ -523,8 +577,8 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         h->lab[0], P.n, P.k, h->sizes[0]);
     CKL();
     CK(cudaEventRecord(e1, h->st));
-    // ---- a1: K[rows, :] = kappa(X X^T), materialised once
-    if (P.materialize) CKR(launch_gemm(h, P.row0, P.nloc, 0, P.ldk, h->K, P.ldk));
+    // ---- a1: K tile [A set, B set] = kappa(X X^T), materialised once
+    if (P.materialize) CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));
     CK(cudaEventRecord(e2, h->st));
     CK(cudaStreamSynchronize(h->st));
     if (h->p.timing) {
@@ -539,6 +593,10 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     cudaEventDestroy(e2);
     return KKM_OK;
   }();
+  if (rc == KKM_OK && P.pr > 1) {  // process-column communicator: ranks gi + gj * pr, key gi
+    ncclResult_t r = ncclCommSplit(h->comm, P.gj, P.gi, &h->colcomm, nullptr);
+    if (r != ncclSuccess) rc = fail(KKM_ENCCL, "ncclCommSplit: %s", ncclGetErrorString(r));
+  }
   if (rc) {
     delete h;
     return rc;
@@ -564,9 +622,11 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   int t = 0;
   for (t = 0; t < T; ++t) {
     if (timing) CKR(rec(ev));
-    CKR(launch_spmm(h, h->lab[h->cur], h->sizes[h->cur]));              // a2
+    const double *S = nullptr;
+    int ns = 0;
+    CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));                         // a2 (+ 1.5D reduce-scatter)
     if (timing) CKR(rec(ev));
-    CKR(run_cnorm(h, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
+    CKR(run_cnorm(h, S, ns, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
     if (timing) CKR(rec(ev));
     CKR(run_assign(h, h->changed + t));                                   // a4
     if (timing) CKR(rec(ev));
@@ -583,8 +643,12 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
     }
   }
   // J of the final labels (one more a2 + a3 pass, as the oracle's J_trace[iters])
-  CKR(launch_spmm(h, h->lab[h->cur], h->sizes[h->cur]));
-  CKR(run_cnorm(h, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
+  {
+    const double *S = nullptr;
+    int ns = 0;
+    CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
+    CKR(run_cnorm(h, S, ns, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
+  }
   std::vector<double> J((size_t)t + 1);
   std::vector<unsigned long long> ch((size_t)std::max(t, 1));
   CK(cudaMemcpyAsync(J.data(), h->J, (size_t)(t + 1) * 8, cudaMemcpyDeviceToHost, h->st));
@@ -622,8 +686,10 @@ int kkm_objective(kkm_handle h, double *J) {
   if (!h || !J) return fail(KKM_EINVAL, "NULL argument");
   if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
   double *slot = h->J + h->P.max_iter + 1;
-  CKR(launch_spmm(h, h->lab[h->cur], h->sizes[h->cur]));
-  CKR(run_cnorm(h, h->E2, h->cnorm2, slot, nullptr, nullptr));
+  const double *S = nullptr;
+  int ns = 0;
+  CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
+  CKR(run_cnorm(h, S, ns, h->E2, h->cnorm2, slot, nullptr, nullptr));
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return KKM_OK;
@@ -710,6 +776,7 @@ int kkm_launch_count(kkm_handle h, int64_t *count) {
 int kkm_destroy(kkm_handle h) {
   if (!h) return KKM_OK;
   cudaStreamSynchronize(h->st);
+  if (h->colcomm) ncclCommDestroy(h->colcomm);
   delete h;
   return KKM_OK;
 }

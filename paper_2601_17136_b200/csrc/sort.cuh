@@ -24,37 +24,46 @@ __global__ void sort_count_kernel(const int32_t *__restrict__ labels, int64_t n,
   for (int c = threadIdx.x; c < k; c += blockDim.x) blockcount[(int64_t)blockIdx.x * k + c] = h[c];
 }
 
-// One block per cluster c (+ block k computes seg): blockoff[b][c] = seg[c] + sum_{b' < b}
-// blockcount[b'][c]; seg[c] = sum_{c' < c} |L_c'|, seg[k] = n.
+// Per-cluster totals over the sorted set: tot[c] = sum_b blockcount[b][c] (block-wide sum).
+__device__ int32_t cluster_total(const int32_t *__restrict__ blockcount, int nb, int k, int c, int32_t *buf) {
+  int32_t s = 0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s += blockcount[(int64_t)b * k + c];
+  buf[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < (unsigned)w) buf[threadIdx.x] += buf[threadIdx.x + w];
+    __syncthreads();
+  }
+  const int32_t t = buf[0];
+  __syncthreads();
+  return t;
+}
+
+// One block per cluster c (+ block k writes seg): blockoff[b][c] = seg[c] + sum_{b' < b}
+// blockcount[b'][c]; seg[c] = sum_{c' < c} (points of cluster c' in the set), seg[k] = set size.
+// blockDim.x must be a power of two.
 __global__ void sort_scan_kernel(const int32_t *__restrict__ blockcount, int nb, int k,
-                                 const int32_t *__restrict__ sizes, int32_t *__restrict__ blockoff,
-                                 int32_t *__restrict__ seg) {
+                                 int32_t *__restrict__ blockoff, int32_t *__restrict__ seg) {
   const int c = blockIdx.x;
+  extern __shared__ int32_t buf[];
   __shared__ int32_t base;
   __shared__ int32_t carry;
-  if (threadIdx.x == 0) {
-    int32_t s = 0;
-    for (int cc = 0; cc < c && cc < k; ++cc) s += sizes[cc];
-    base = s;
-    carry = 0;
-    if (c == k) {
-      for (int cc = 0; cc < k; ++cc) seg[cc] = 0;
-    }
+  int32_t s = 0;
+  for (int cc = 0; cc < (c < k ? c : k); ++cc) {
+    const int32_t t = cluster_total(blockcount, nb, k, cc, buf);
+    if (c == k && threadIdx.x == 0) seg[cc] = s;
+    s += t;
   }
-  __syncthreads();
-  if (c == k) {  // segment starts
-    if (threadIdx.x == 0) {
-      int32_t s = 0;
-      for (int cc = 0; cc < k; ++cc) {
-        seg[cc] = s;
-        s += sizes[cc];
-      }
-      seg[k] = s;
-    }
+  if (c == k) {
+    if (threadIdx.x == 0) seg[k] = s;
     return;
   }
+  if (threadIdx.x == 0) {
+    base = s;
+    carry = 0;
+  }
+  __syncthreads();
   // block-wide exclusive scan over b in tiles of blockDim.x
-  extern __shared__ int32_t buf[];
   for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
     const int b = b0 + threadIdx.x;
     const int32_t v = b < nb ? blockcount[(int64_t)b * k + c] : 0;
@@ -113,11 +122,12 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(const int32_t *__rest
   }
 }
 
-// Sorted copies: Xs[p] = X[perm[p]] for the hi and lo operands (dp 16-bit values per row,
-// uint4 vectors), vs[p] = v[perm[p]] for norms and rscale. Rows p in [n, npad) are zeroed.
+// Sorted copies of the set [b0, b0 + n): Xs[p] = X[b0 + perm[p]] for the hi and lo operands
+// (dp 16-bit values per row, uint4 vectors), vs[p] = v[b0 + perm[p]] for norms and rscale.
+// Rows p in [n, npad) are zeroed.
 __global__ void gather_rows_kernel(const uint16_t *__restrict__ Xhi, const uint16_t *__restrict__ Xlo,
                                    const float *__restrict__ norms, const float *__restrict__ rscale,
-                                   const int32_t *__restrict__ perm, int64_t n, int64_t npad,
+                                   const int32_t *__restrict__ perm, int64_t b0, int64_t n, int64_t npad,
                                    int64_t dp, uint16_t *__restrict__ Shi, uint16_t *__restrict__ Slo,
                                    float *__restrict__ snorms, float *__restrict__ srscale) {
   const int lane = threadIdx.x & 31;
@@ -127,7 +137,7 @@ __global__ void gather_rows_kernel(const uint16_t *__restrict__ Xhi, const uint1
   uint4 *dh = reinterpret_cast<uint4 *>(Shi + p * dp);
   uint4 *dl = reinterpret_cast<uint4 *>(Slo + p * dp);
   if (p < n) {
-    const int64_t j = perm[p];
+    const int64_t j = b0 + perm[p];
     const uint4 *sh = reinterpret_cast<const uint4 *>(Xhi + j * dp);
     const uint4 *sl = reinterpret_cast<const uint4 *>(Xlo + j * dp);
     for (int64_t v = lane; v < nv; v += 32) {

@@ -33,12 +33,12 @@ constexpr size_t spmm_smem_bytes() {
          2 * SP_STAGES * 8 + 64;
 }
 
-// Spart[(s * nrows + i) * k + c0 + c] for clusters c0 .. c0 + KP - 1 (c0 + c < k).
+// Spart[(s * rows_pad + i) * k + c0 + c] for clusters c0 .. c0 + KP - 1 (c0 + c < k).
 template <int KP>
 __global__ void __launch_bounds__(SP_THREADS, 1)
     spmm_onehot_kernel(const float *__restrict__ K, int64_t ldk, int64_t nrows,
                        const int32_t *__restrict__ labels, int k, int c0, int nsplit,
-                       int chunks_per_split, double *__restrict__ Spart) {
+                       int chunks_per_split, int64_t rows_pad, double *__restrict__ Spart) {
   extern __shared__ __align__(128) uint8_t smem[];
   float *ring = reinterpret_cast<float *>(smem);  // [STAGES][ROWS + 1][CH]
   float *red = ring + (size_t)SP_STAGES * (SP_ROWS + 1) * SP_CH;  // [CWARPS][ROWS][KPMAX]
@@ -148,11 +148,34 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
       if (r0 + r < nrows && c0 + c < k) {
         double sum = 0.0;
         for (int w = 0; w < SP_CWARPS; ++w) sum += (double)red[(w * SP_ROWS + r) * SP_KPMAX + c];
-        Spart[((int64_t)s * nrows + r0 + r) * k + c0 + c] = sum;
+        Spart[((int64_t)s * rows_pad + r0 + r) * k + c0 + c] = sum;
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(SP_CWARPS * 32));
   }
+}
+
+}  // namespace kkm
+
+namespace kkm {
+
+// labB[t] = labels[t] for t < nB, -1 on [nB, len): the B set's labels at the K-tile pitch.
+__global__ void copy_labels_kernel(const int32_t *__restrict__ labels, int64_t nB, int64_t len,
+                                   int32_t *__restrict__ labB) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < len) labB[t] = t < nB ? labels[t] : -1;
+}
+
+// Scol[r][c] = sum_s Spart[s][r][c] (fixed order) for r < nA, 0 on [nA, rows_pad).
+__global__ void split_sum_kernel(const double *__restrict__ Spart, int nsplit, int64_t nA, int64_t rows_pad,
+                                 int k, double *__restrict__ Scol) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows_pad * k) return;
+  const int64_t r = t / k;
+  double s = 0.0;
+  if (r < nA)
+    for (int p = 0; p < nsplit; ++p) s += Spart[(int64_t)p * rows_pad * k + t];
+  Scol[t] = s;
 }
 
 }  // namespace kkm

@@ -31,7 +31,8 @@ template <int KMAX>
 __global__ void __launch_bounds__(TC_THREADS_V2, 1)
     tc_stream_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                      const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                     uint32_t idesc, int nkb, int64_t n, int64_t row0, int64_t nloc,
+                     uint32_t idesc, int nkb, int64_t n, int64_t b0, int64_t row0, int64_t nloc,
+                     int64_t rows_pad,
                      const float *__restrict__ norms, const float *__restrict__ rscale,
                      const float *__restrict__ snorms, const float *__restrict__ srscale,
                      const int32_t *__restrict__ pos, const int32_t *__restrict__ seg_g, int k,
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(TC_THREADS_V2, 1)
       const int64_t i = row0 + r;
       const float ni = row_ok ? norms[i] : 0.f;
       const float rsi = (fp16 && row_ok) ? rscale[i] : 1.f;
-      const int64_t mypos = (row_ok && kp.kind == 2) ? pos[i] : -1;
+      const int64_t mypos = (row_ok && kp.kind == 2 && i >= b0 && i < b0 + n) ? pos[i - b0] : -1;
       double acc[KMAX];
 #pragma unroll
       for (int c = 0; c < KMAX; ++c) acc[c] = 0.0;
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(TC_THREADS_V2, 1)
         if (lane == 0) mbar_arrive(tempty);
       }
       if (row_ok) {
-        double *dst = Spart + ((int64_t)(2 * sp + half) * nloc + r) * k;
+        double *dst = Spart + ((int64_t)(2 * sp + half) * rows_pad + r) * k;
 #pragma unroll
         for (int c = 0; c < KMAX; ++c)
           if (c < k) dst[c] = acc[c];
@@ -275,7 +276,8 @@ inline int ts_encode(CUtensorMap *m, const void *ptr, bool fp16, int64_t rows, i
 
 template <int KMAX>
 inline int ts_launch_k(TcStream &g, bool &attr, int grid, cudaStream_t st, uint32_t idesc, int nkb, int64_t n,
-                       int64_t row0, int64_t nloc, const float *norms, const float *rscale,
+                       int64_t b0, int64_t row0, int64_t nloc, int64_t rows_pad, const float *norms,
+                       const float *rscale,
                        const float *snorms, const float *srscale, const int32_t *pos, const int32_t *seg,
                        int k, const KappaParams &kp, int tiles_m, int tiles_n, int nsplit, int tps,
                        double *Spart) {
@@ -288,15 +290,17 @@ inline int ts_launch_k(TcStream &g, bool &attr, int grid, cudaStream_t st, uint3
     attr = true;
   }
   tc_stream_kernel<KMAX><<<grid, TC_THREADS_V2, TS_SMEM, st>>>(
-      g.a_hi, g.a_lo, g.b_hi, g.b_lo, idesc, nkb, n, row0, nloc, norms, rscale, snorms, srscale, pos, seg,
-      k, kp, tiles_m, tiles_n, nsplit, tps, Spart);
+      g.a_hi, g.a_lo, g.b_hi, g.b_lo, idesc, nkb, n, b0, row0, nloc, rows_pad, norms, rscale, snorms, srscale,
+      pos, seg, k, kp, tiles_m, tiles_n, nsplit, tps, Spart);
   return 0;
 }
 
-// Spart[2*split + half][r][c] for local rows r in [0, nloc) (global row0 + r), all n columns.
+// Spart[2*split + half][r][c] (row pitch rows_pad) for rows r in [0, nloc) (global row0 + r)
+// against the n sorted columns of the set starting at global point b0.
 inline int tc_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *Xlo, const uint16_t *Shi,
                             const uint16_t *Slo, bool fp16, int64_t rows, int64_t dp, int64_t n,
-                            int64_t row0, int64_t nloc, const float *norms, const float *rscale,
+                            int64_t b0, int64_t row0, int64_t nloc, int64_t rows_pad,
+                            const float *norms, const float *rscale,
                             const float *snorms, const float *srscale, const int32_t *pos,
                             const int32_t *seg, int k, const KappaParams &kp, int nsplit, double *Spart,
                             cudaStream_t st, int64_t *launches) {
@@ -329,13 +333,16 @@ inline int tc_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *Xl
   const int nkb = (int)(dp / TC_BK);
   int rc;
   if (k <= 4)
-    rc = ts_launch_k<4>(g, g.attr4, grid, st, idesc, nkb, n, row0, nloc, norms, fp16 ? rscale : nullptr,
+    rc = ts_launch_k<4>(g, g.attr4, grid, st, idesc, nkb, n, b0, row0, nloc, rows_pad, norms,
+                         fp16 ? rscale : nullptr,
                         snorms, srscale, pos, seg, k, kp, tiles_m, tiles_n, nsplit, tps, Spart);
   else if (k <= 8)
-    rc = ts_launch_k<8>(g, g.attr8, grid, st, idesc, nkb, n, row0, nloc, norms, fp16 ? rscale : nullptr,
+    rc = ts_launch_k<8>(g, g.attr8, grid, st, idesc, nkb, n, b0, row0, nloc, rows_pad, norms,
+                         fp16 ? rscale : nullptr,
                         snorms, srscale, pos, seg, k, kp, tiles_m, tiles_n, nsplit, tps, Spart);
   else
-    rc = ts_launch_k<16>(g, g.attr16, grid, st, idesc, nkb, n, row0, nloc, norms, fp16 ? rscale : nullptr,
+    rc = ts_launch_k<16>(g, g.attr16, grid, st, idesc, nkb, n, b0, row0, nloc, rows_pad, norms,
+                         fp16 ? rscale : nullptr,
                          snorms, srscale, pos, seg, k, kp, tiles_m, tiles_n, nsplit, tps, Spart);
   if (rc) return rc;
   if (launches) ++*launches;

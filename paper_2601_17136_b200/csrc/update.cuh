@@ -18,7 +18,7 @@ constexpr int FIN_THREADS = 128;
 // grid: nblocks; block b handles rows [b * rows_per_block, ...). Dynamic smem:
 // (k + 1) * FIN_THREADS doubles.
 __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(
-    const double *__restrict__ Spart, int nsplit, int64_t nrows, int k,
+    const double *__restrict__ Spart, int nsplit, int64_t nrows, int64_t rows_pad, int k,
     const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl_local,
     const double *__restrict__ diag, int64_t rows_per_block, double *__restrict__ E,
     double *__restrict__ blockpart) {
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(
     double zi = 0.0;
     for (int c = 0; c < k; ++c) {
       double s = 0.0;
-      for (int p = 0; p < nsplit; ++p) s += Spart[((int64_t)p * nrows + i) * k + c];
+      for (int p = 0; p < nsplit; ++p) s += Spart[((int64_t)p * rows_pad + i) * k + c];
       const int32_t sz = sizes[c];
       const double e = sz > 0 ? s / (double)sz : 0.0;
       E[i * k + c] = e;

@@ -32,7 +32,7 @@ class KKMParams(ctypes.Structure):
                 ("degree", ctypes.c_int32), ("k", ctypes.c_int32), ("max_iter", ctypes.c_int32),
                 ("stop_on_no_change", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("timing", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("grid_rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 _lib = None
@@ -137,7 +137,7 @@ class KernelKMeans:
                  stop_on_no_change: bool = False, path: int = PATH_AUTO,
                  precision: int = PREC_FP16X3, timing: bool = False, init_labels=None,
                  rank: int = 0, nranks: int = 1, comm=None, stream=None, device=None,
-                 workspace=None):
+                 workspace=None, grid_rows: int = 1):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
@@ -149,6 +149,7 @@ class KernelKMeans:
         p.kind, p.gamma, p.coef0, p.degree = kind, gamma, coef0, degree
         p.k, p.max_iter, p.stop_on_no_change = k, max_iter, int(stop_on_no_change)
         p.path, p.precision, p.timing = path, precision, int(timing)
+        p.grid_rows = grid_rows
         self.params = p
         self.max_iter = max_iter
         nb = workspace_size(p, self.n, self.d, rank, nranks)

@@ -79,6 +79,15 @@ def test_workspace_size_and_errors():
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(p, 60000, 784, rank=4, nranks=4)
     q = kkm.default_params()
+    q.k, q.grid_rows = 3, 3
+    with pytest.raises(kkm.KKMError, match="EUNSUP"):
+        kkm.workspace_size(q, 100, 4, rank=0, nranks=4)  # 3 does not divide 4
+    q.grid_rows = 2  # 2 x 2 grid: K tile = column block (2 of 4 blocks) x row block (2 of 4)
+    nb_15 = kkm.workspace_size(q, 60000, 784, rank=1, nranks=4)
+    q.grid_rows = 1
+    nb_1d = kkm.workspace_size(q, 60000, 784, rank=1, nranks=4)
+    assert abs(nb_15 - nb_1d) < 0.05 * nb_1d  # same K-tile size, n^2 / P
+    q = kkm.default_params()
     q.reserved[2] = 1
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(q, 100, 4)

@@ -157,3 +157,87 @@ def test_shard_layout_in_process(n, P):
         assert abs(J - ref["J"]) <= 1e-12 * max(1.0, abs(ref["J"]))
     b = [shard_begin(n, r, P) for r in range(P + 1)]
     assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
+
+
+def one_iteration_15d(X, labels, k, args, pr, pc, rank, coll):
+    """One iteration of the 1.5D schedule (Alg. 2) as rank = gi + gj * pr of a pr x pc
+    grid executes it: partial E for the points of column block gj against row block gi, a
+    column-split reduce-scatter over process column gj, then the 1D tail."""
+    n = X.shape[0]
+    P = pr * pc
+    B = -(-n // P)
+    gi, gj = rank % pr, rank // pr
+    a0, a1 = min(n, gj * pr * B), min(n, (gj + 1) * pr * B)   # column block gj (A set)
+    b0, b1 = min(n, gi * pc * B), min(n, (gi + 1) * pc * B)   # row block gi (B set)
+    sizes = np.bincount(labels, minlength=k)
+    Ka = oracle.kernel_rows(X, np.arange(a0, a1), *args)[:, b0:b1] if a1 > a0 else np.zeros((0, b1 - b0))
+    lb = labels[b0:b1]
+    Spart = np.zeros((pr * B, k))
+    for c in range(k):
+        Spart[:a1 - a0, c] = Ka[:, lb == c].sum(axis=1)         # sum over the B set only
+    # reduce-scatter along process column gj: rank (l, gj) keeps rows [l B, (l+1) B)
+    allS = coll("col", gj, gi, Spart)                          # pr x (pr B) x k from column peers
+    mine = sum(allS[l] for l in range(pr))[gi * B:(gi + 1) * B]
+    r0, r1 = min(n, rank * B), min(n, (rank + 1) * B)
+    assert r0 == a0 + gi * B or r0 == n
+    E = mine[:r1 - r0] / np.maximum(sizes, 1)
+    diag = oracle.kernel_diag(X, *args, rows=np.arange(r0, r1)) if r1 > r0 else np.zeros(0)
+    part = np.zeros(k + 1)
+    for ii, i in enumerate(range(r0, r1)):
+        z = E[ii, labels[i]]
+        part[labels[i]] += z
+        part[k] += diag[ii] - z
+    allp = coll("world", 0, rank, part)
+    tot = np.zeros(k + 1)
+    for r in range(P):
+        tot += allp[r]
+    cn = np.where(sizes > 0, tot[:k] / np.maximum(sizes, 1), np.inf)
+    new_local, _ = oracle.assign(E, diag, cn) if r1 > r0 else (np.zeros(0, np.int32), None)
+    send = np.full(B, -1, dtype=np.int32)
+    send[:new_local.size] = new_local
+    return coll("world", 1, rank, send).reshape(-1)[:n], cn, tot[k]
+
+
+class _GroupRendezvous:
+    """In-process collectives over named groups: ("col", j) has the pr ranks of process column j
+    ordered by process row; ("world", tag) all ranks."""
+
+    def __init__(self, pr, pc):
+        self.pr, self.pc, self.slots = pr, pc, {}
+
+    def view(self, rank):
+        counter = {}
+
+        def coll(group, tag, member, buf):
+            key = (group, tag, counter.get((group, tag), 0))
+            counter[(group, tag)] = key[2] + 1
+            size = self.pr if group == "col" else self.pr * self.pc
+            self.slots.setdefault(key, {})[member] = np.array(buf)
+            if len(self.slots[key]) < size:
+                raise _Pending(key)
+            return np.stack([self.slots[key][m] for m in range(size)])
+        return coll
+
+
+@pytest.mark.parametrize("n,pr,pc", [(64, 2, 2), (101, 2, 4), (37, 3, 2), (50, 4, 1), (9, 2, 2)])
+def test_15d_schedule_matches_oracle(n, pr, pc):
+    X = synth.blobs(n, 3, 3, seed=n + pr)
+    k = 3
+    args = (oracle.POLY, 0.5, 1.0, 2)
+    labels = oracle.round_robin(n, k)
+    rv = _GroupRendezvous(pr, pc)
+    results = {}
+    for _ in range(4):
+        for r in range(pr * pc):
+            if r in results:
+                continue
+            try:
+                results[r] = one_iteration_15d(X, labels, k, args, pr, pc, r, rv.view(r))
+            except _Pending:
+                pass
+    assert len(results) == pr * pc
+    ref = oracle.iteration(oracle.kernel_matrix(X, *args), oracle.kernel_diag(X, *args), labels, k)
+    for lab, cn, J in results.values():
+        assert np.array_equal(lab, ref["new_labels"])
+        assert np.allclose(cn, ref["cnorm"], rtol=1e-12)
+        assert abs(J - ref["J"]) <= 1e-10 * max(1.0, abs(ref["J"]))

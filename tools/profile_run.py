@@ -16,10 +16,13 @@ ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--precision", default="fp16x3")
 ap.add_argument("--path", default="auto", choices=["auto", "mat", "stream"])
+ap.add_argument("--k", type=int, default=0, help="override the cluster count")
 a = ap.parse_args()
 X, cfg = synth.make_config(a.config, n=a.n or None)
 prec = {"fp16x3": kkm.PREC_FP16X3, "bf16x3": kkm.PREC_BF16X3, "fp32": kkm.PREC_FP32_SIMT}[a.precision]
 path = {"auto": kkm.PATH_AUTO, "mat": kkm.PATH_MATERIALIZE, "stream": kkm.PATH_STREAM}[a.path]
+if a.k:
+    cfg["k"] = a.k
 h = kkm.KernelKMeans(torch.from_numpy(X).cuda(), X.shape[0], cfg["k"], cfg["kind"], cfg["gamma"],
                      cfg["coef0"], cfg["degree"], max_iter=a.iters, precision=prec, timing=True, path=path)
 it, J, ch = h.fit()
@@ -33,3 +36,6 @@ if a.path == "stream":
     print(f"stream a1+a2 per iteration {per:.2f} ms -> useful {flops / (per * 1e-3) / 1e12:.1f} TFLOP/s")
 else:
     print(f"a1 GEMM {ph['init_gemm']:.2f} ms -> useful {flops / (ph['init_gemm'] * 1e-3) / 1e12:.1f} TFLOP/s")
+    ldk = -(-n // 32) * 32
+    per = ph["spmm"] / it
+    print(f"a2 SpMM k={cfg['k']} {per:.3f} ms/iter -> {n * ldk * 4 / (per * 1e-3) / 1e9:.0f} GB/s")
