@@ -15,6 +15,9 @@ Recipes follow SURVEY.md §8(d) "Synthetic inputs"; DESIGN.md restates them.
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 __all__ = [
@@ -129,8 +132,21 @@ def mnist_prototypes(seed: int, nclass: int = 10) -> np.ndarray:
     return protos
 
 
+def _parallel_chunks(nrows: int, chunk: int, fn):
+    """Runs fn(c0, c1) over [0, nrows) in chunks on host threads (numpy releases the GIL);
+    every row is a pure function of (seed, index), so the result does not depend on the split."""
+    starts = list(range(0, nrows, chunk))
+    workers = max(1, min(len(starts), len(os.sched_getaffinity(0))))
+    if workers == 1:
+        for c0 in starts:
+            fn(c0, min(nrows, c0 + chunk))
+        return
+    with ThreadPoolExecutor(workers) as ex:
+        list(ex.map(lambda c0: fn(c0, min(nrows, c0 + chunk)), starts))
+
+
 def mnist_like(n: int = 60000, seed: int = 2, row_begin: int = 0, row_end: int | None = None,
-               return_truth: bool = False, chunk: int = 65536, rows=None):
+               return_truth: bool = False, chunk: int = 8192, rows=None):
     """MNIST-shaped rows (d = 784) per SURVEY §8(d) cfg2: class = keyed hash mod 10,
     prototype shifted by +-2 px, contrast U[0.7, 1], N(0, 0.1^2) noise only on the
     prototype's support (> 0.05), clipped to [0, 1], quantised to multiples of 1/255."""
@@ -139,8 +155,9 @@ def mnist_like(n: int = 60000, seed: int = 2, row_begin: int = 0, row_end: int |
     rows_all = _rows(n, row_begin, row_end, rows)
     X = np.empty((rows_all.size, S * S), dtype=np.float32)
     truth = np.empty(rows_all.size, dtype=np.int32)
-    for c0 in range(0, rows_all.size, chunk):
-        rows = rows_all[c0:c0 + chunk]
+
+    def work(c0, c1):
+        rows = rows_all[c0:c1]
         bits = counter_bits(seed, 200, rows, 3)
         cls = (bits[:, 0] % np.uint64(10)).astype(np.int64)
         dy = (bits[:, 1] % np.uint64(5)).astype(np.int64) - 2
@@ -156,15 +173,17 @@ def mnist_like(n: int = 60000, seed: int = 2, row_begin: int = 0, row_end: int |
         support = img > 0.05
         img = img + support * (0.1 * counter_normal(seed, 202, rows, S * S))
         img = np.clip(img, 0.0, 1.0)
-        X[c0:c0 + rows.size] = (np.rint(img * 255.0) / 255.0).astype(np.float32)
-        truth[c0:c0 + rows.size] = cls
+        X[c0:c1] = (np.rint(img * 255.0) / 255.0).astype(np.float32)
+        truth[c0:c1] = cls
+
+    _parallel_chunks(rows_all.size, chunk, work)
     return (X, truth) if return_truth else X
 
 
 # ---------------------------------------------------------------- config 3
 def har_like(n: int = 200000, seed: int = 3, d: int = 561, latent: int = 20, nclass: int = 6,
              row_begin: int = 0, row_end: int | None = None, return_truth: bool = False,
-             chunk: int = 65536, rows=None):
+             chunk: int = 8192, rows=None):
     """HAR-shaped rows per SURVEY §8(d) cfg3: mu_c ~ N(0, 9 I_20), A in R^{d x 20} with
     N(0, 1/20) entries, x = tanh(0.5 A (mu_c + eps) + 0.05 xi); x in (-1, 1)."""
     mu = 3.0 * counter_normal(seed, 300, np.arange(nclass), latent)
@@ -172,12 +191,15 @@ def har_like(n: int = 200000, seed: int = 3, d: int = 561, latent: int = 20, ncl
     rows_all = _rows(n, row_begin, row_end, rows)
     X = np.empty((rows_all.size, d), dtype=np.float32)
     truth = np.empty(rows_all.size, dtype=np.int32)
-    for c0 in range(0, rows_all.size, chunk):
-        rows = rows_all[c0:c0 + chunk]
+
+    def work(c0, c1):
+        rows = rows_all[c0:c1]
         cls = (counter_bits(seed, 302, rows, 1)[:, 0] % np.uint64(nclass)).astype(np.int64)
         z = mu[cls] + counter_normal(seed, 303, rows, latent)
-        X[c0:c0 + rows.size] = np.tanh(0.5 * z @ A.T + 0.05 * counter_normal(seed, 304, rows, d))
-        truth[c0:c0 + rows.size] = cls
+        X[c0:c1] = np.tanh(0.5 * z @ A.T + 0.05 * counter_normal(seed, 304, rows, d))
+        truth[c0:c1] = cls
+
+    _parallel_chunks(rows_all.size, chunk, work)
     return (X, truth) if return_truth else X
 
 
