@@ -16,6 +16,12 @@ struct KappaParams {
   float neg_gamma_log2e;  // Gaussian: -gamma * log2(e), so K = 2^(neg_gamma_log2e * r2)
 };
 
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -38,11 +44,6 @@ __device__ __forceinline__ float kappa_epilogue(const KappaParams &kp, float b, 
   return ex2_approx(kp.neg_gamma_log2e * r2);
 }
 
-__device__ __forceinline__ unsigned long long pack2(float a, float b) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
 
 // d += a * b elementwise on float pairs: one FFMA2 (sm_100).
 __device__ __forceinline__ void ffma2(float2 &d, float ax, float ay, float bx, float by) {
@@ -52,6 +53,31 @@ __device__ __forceinline__ void ffma2(float2 &d, float ax, float ay, float bx, f
 }
 
 __device__ __forceinline__ float mask_eq(int a, int b) { return a == b ? 1.0f : 0.0f; }
+
+// Packed fp32 pair arithmetic (sm_100 add/mul/fma.rn.f32x2): one instruction for two lanes
+// of work; operands are register pairs (x, y).
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pack2(a.x, a.y)), "l"(pack2(b.x, b.y)));
+  float2 o;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pack2(a.x, a.y)), "l"(pack2(b.x, b.y)));
+  float2 o;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pack2(a.x, a.y)), "l"(pack2(b.x, b.y)),
+      "l"(pack2(c.x, c.y)));
+  float2 o;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

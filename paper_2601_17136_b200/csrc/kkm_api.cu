@@ -20,6 +20,7 @@
 #include "sort.cuh"
 #include "spmm.cuh"
 #include "stream.cuh"
+#include "tc2.cuh"
 #include "update.cuh"
 
 using namespace kkm;
@@ -51,13 +52,14 @@ struct Plan {
   int k, nranks, rank, max_iter;
   bool materialize, tc, fp16;  // tc: tensor-core a1 (bf16x3 or fp16x3); fp16: fp16x3 split
   int sort_blocks;              // streaming: blocks of the counting sort
+  bool spmm_v2;                 // materialised a2 with label-sorted 32-column groups (k <= 64)
   int nsplit, chunks_per_split, nfin, nspmm_pass;
   int64_t rows_per_block;
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      total;
+      o_codes, total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -120,14 +122,25 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       return fail(KKM_EUNSUP, "the streaming path needs a tensor-core precision (FP16X3 or BF16X3)");
     if (P.k > 16) return fail(KKM_EUNSUP, "the streaming path supports k <= 16 (k=%d)", P.k);
   }
-  if (P.materialize) {
+  // v1 (one-hot FFMA2) is faster for k <= 16 (5.4 TB/s at k = 10); v2 (sorted groups, shuffle
+  // bound at ~3.9 TB/s for any k) replaces v1's ceil(k/16) passes over K for 16 < k <= 64.
+  P.spmm_v2 = P.k > SP_KPMAX && P.k <= SG_MAX_K;
+  if (P.materialize && P.spmm_v2) {
+    const int64_t nchunks = ceil_div(P.ldk, SG_CH);
+    const int64_t groups = ceil_div(std::max<int64_t>(P.nA, 1), SG_ROWS);
+    // splits: bound the chunks per item, and give >= ~4 items per SM for load balance
+    int64_t ns = std::max<int64_t>(ceil_div(nchunks, SG_MAX_CHUNKS_PER_SPLIT), ceil_div(4 * 148, groups));
+    ns = std::min<int64_t>(std::max<int64_t>(ns, 1), nchunks);
+    P.nsplit = (int)ns;
+    P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
+  } else if (P.materialize) {
     const int64_t nchunks = ceil_div(P.ldk, SP_CH);
     P.nsplit = (int)ceil_div(nchunks, SP_MAX_CHUNKS_PER_SPLIT);
     P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
   } else {
     // work units of the fused kernel = 128-row tiles x column splits; 148 SMs assumed for the
     // load-balance choice (B200); each split writes one partial per column half
-    P.nsplit = 2 * ts_choose_splits(P.nA, P.nB, 148);
+    P.nsplit = 2 * ts_choose_splits((P.nA + 1) / 2, P.nB, 74);  // 74 CTA pairs, 256-row pair tiles
     P.chunks_per_split = 0;
   }
   P.sort_blocks = (int)ceil_div(std::max<int64_t>(P.nB, 1), SORT_BLOCK);
@@ -174,6 +187,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_bcount = take((size_t)P.sort_blocks * P.k * 4);
     P.o_boff = take((size_t)P.sort_blocks * P.k * 4);
   }
+  if (P.materialize && P.spmm_v2) P.o_codes = take((size_t)P.ldk * 4);
   if (P.pr > 1) {
     P.o_labB = take((size_t)P.ldk * 4);
     P.o_Scol = take((size_t)P.nApad * P.k * 8);
@@ -205,6 +219,7 @@ struct kkm_ctx {
   // 1.5D: padded labels of the B set, column-block partials, own-block sums; column comm
   int32_t *labB = nullptr;
   double *Scol = nullptr, *Smine = nullptr;
+  uint32_t *codes = nullptr;  // SpMM v2 per-iteration group codes
   ncclComm_t colcomm = nullptr;
   int32_t *lab[2], *sizes[2];
   unsigned long long *changed;
@@ -295,9 +310,9 @@ int launch_stream(kkm_ctx *h, const int32_t *labels) {
       h->srscale);
   CKL();
   if (P.nA == 0) return KKM_OK;
-  int rc = tc_stream_launch(h->ts, h->Xhi, h->Xlo, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.nB, P.b0, P.a0,
-                            P.nA, P.nApad, h->norms, h->rscale, h->snorms, h->srscale, h->pos, h->seg, k,
-                            h->kp, P.nsplit / 2, h->Spart, h->st, &h->launches);
+  int rc = tc2_stream_launch(h->ts, h->Xhi, h->Xlo, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.nB, P.b0, P.a0,
+                             P.nA, P.nApad, h->norms, h->rscale, h->snorms, h->srscale, h->pos, h->seg, k,
+                             h->kp, P.nsplit / 2, h->Spart, h->st, &h->launches);
   if (rc) {
     h->poisoned = true;
     return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
@@ -309,6 +324,23 @@ int launch_stream(kkm_ctx *h, const int32_t *labels) {
 int launch_spmm_mat(kkm_ctx *h, const int32_t *labels) {
   const Plan &P = h->P;
   if (P.nA == 0) return KKM_OK;
+  if (P.spmm_v2) {
+    const int64_t ngroups = P.ldk / 32;
+    group_code_kernel<<<(unsigned)ceil_div(ngroups, 8), 256, 0, h->st>>>(labels + P.b0, P.nB, P.ldk, h->codes);
+    CKL();
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(spmm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sg_smem_bytes(SG_MAX_K)));
+      attr = true;
+    }
+    const int64_t items = ceil_div(P.nA, SG_ROWS) * P.nsplit;
+    const int grid = (int)std::min<int64_t>(items, h->num_sms);
+    spmm_group_kernel<<<grid, SG_THREADS, sg_smem_bytes(P.k), h->st>>>(h->K, P.ldk, P.nA, h->codes, P.k, P.nsplit,
+                                                                     P.chunks_per_split, P.nApad, h->Spart);
+    CKL();
+    return KKM_OK;
+  }
   if (P.pr > 1) {  // the B set's labels, -1 padded to the tile pitch
     copy_labels_kernel<<<(unsigned)ceil_div(P.ldk, 256), 256, 0, h->st>>>(labels + P.b0, P.nB, P.ldk, h->labB);
     CKL();
@@ -400,8 +432,8 @@ int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, flo
   const Plan &P = h->P;
   if (m <= 0 || ncov <= 0) return KKM_OK;
   if (P.tc) {
-    int rc = tc_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0,
-                            ncov, h->norms, h->kp, out, ldo, h->st, &h->launches);
+    int rc = tc2_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0,
+                             ncov, h->norms, h->kp, out, ldo, h->st, &h->launches);
     if (rc) {
       h->poisoned = true;
       return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
@@ -515,6 +547,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->bcount = (int32_t *)(w + P.o_bcount);
     h->boff = (int32_t *)(w + P.o_boff);
   }
+  if (P.materialize && P.spmm_v2) h->codes = (uint32_t *)(w + P.o_codes);
   if (P.pr > 1) {
     h->labB = (int32_t *)(w + P.o_labB);
     h->Scol = (double *)(w + P.o_Scol);

@@ -179,3 +179,172 @@ __global__ void split_sum_kernel(const double *__restrict__ Spart, int nsplit, i
 }
 
 }  // namespace kkm
+
+// =====================================================================================
+// SpMM v2: label-sorted 32-column groups (k-independent, ~0.5 instructions per element).
+//
+// Once per iteration `group_code_kernel` stably sorts every aligned group of 32 columns by
+// label (one warp per group) and packs, for each sorted position p of group g,
+//   code[32 g + p] = src | lab << 8 | rem << 16 | head << 24
+// src = the group lane holding that column, lab = its label (255 for padding columns),
+// rem = positions left in its label segment after p, head = p starts a segment. The consumer
+// reads K[i][32 g + src] (a permutation of 32 consecutive words: conflict-free), reduces each
+// segment with a 5-step (or fewer, warp-uniform) shfl_down suffix scan limited by rem, and the
+// segment-head lanes add the segment sums to fp64 shared-memory accumulators acc[row][lab].
+// =====================================================================================
+namespace kkm {
+
+constexpr int SG_ROWS = 8;        // rows per work item
+constexpr int SG_CH = 1024;       // columns per chunk
+constexpr int SG_STAGES = 4;
+constexpr int SG_CWARPS = 16;
+constexpr int SG_THREADS = (SG_CWARPS + 1) * 32;
+constexpr int SG_MAX_K = 64;
+constexpr int SG_MAX_CHUNKS_PER_SPLIT = 256;  // fp64 accumulators: splits only for balance
+
+inline size_t sg_smem_bytes(int k) {
+  return (size_t)SG_STAGES * (SG_ROWS + 1) * SG_CH * 4 + (size_t)SG_CWARPS * SG_ROWS * k * 8 +
+         2 * SG_STAGES * 8 + 64;
+}
+
+// One warp per 32-column group of [0, len); labels beyond nB are padding (lab 255).
+__global__ void group_code_kernel(const int32_t *__restrict__ labels, int64_t nB, int64_t len,
+                                  uint32_t *__restrict__ codes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g * 32 >= len) return;
+  const int64_t col = g * 32 + lane;
+  const int L = col < nB ? labels[col] : 255;
+  const unsigned eq = __match_any_sync(0xffffffffu, L);
+  const int within = __popc(eq & ((1u << lane) - 1u));
+  int less = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) less += __shfl_sync(0xffffffffu, L, j) < L;
+  const int rank = less + within;
+  const int rem = less + __popc(eq) - 1 - rank;
+  const uint32_t code = (uint32_t)lane | ((uint32_t)L << 8) | ((uint32_t)rem << 16) | ((uint32_t)(within == 0) << 24);
+  codes[g * 32 + rank] = code;
+}
+
+// Spart[(s * rows_pad + i) * k + c] = sum over the split's columns j with cl_j = c of K[i][j].
+__global__ void __launch_bounds__(SG_THREADS, 1)
+    spmm_group_kernel(const float *__restrict__ K, int64_t ldk, int64_t nrows,
+                      const uint32_t *__restrict__ codes, int k, int nsplit, int chunks_per_split,
+                      int64_t rows_pad, double *__restrict__ Spart) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float *ring = reinterpret_cast<float *>(smem);  // [STAGES][ROWS + 1][CH] (last row: codes)
+  double *acc = reinterpret_cast<double *>(ring + (size_t)SG_STAGES * (SG_ROWS + 1) * SG_CH);  // [CWARPS][ROWS][k]
+  uint64_t *full = reinterpret_cast<uint64_t *>(acc + SG_CWARPS * SG_ROWS * k);
+  uint64_t *empty = full + SG_STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (ldk + SG_CH - 1) / SG_CH;
+  const int64_t ngroups = (nrows + SG_ROWS - 1) / SG_ROWS;
+  const int64_t nitems = ngroups * nsplit;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SG_CWARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  if (warp == SG_CWARPS) {
+    if (lane == 0) {
+      for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int64_t gi = item / nsplit;
+        const int s = (int)(item % nsplit);
+        const int64_t q0 = (int64_t)s * chunks_per_split;
+        const int64_t q1 = q0 + chunks_per_split < nchunks ? q0 + chunks_per_split : nchunks;
+        const int64_t r0 = gi * SG_ROWS;
+        const int nr = (int)(nrows - r0 < SG_ROWS ? nrows - r0 : SG_ROWS);
+        for (int64_t q = q0; q < q1; ++q) {
+          const int64_t col0 = q * SG_CH;
+          const uint32_t cols = (uint32_t)(ldk - col0 < SG_CH ? ldk - col0 : SG_CH);
+          mbar_wait(&empty[stage], phase ^ 1);
+          float *st = ring + (size_t)stage * (SG_ROWS + 1) * SG_CH;
+          mbar_arrive_expect_tx(&full[stage], (uint32_t)(nr + 1) * cols * 4u);
+          bulk_g2s(st + SG_ROWS * SG_CH, codes + col0, cols * 4u, &full[stage]);
+          for (int r = 0; r < nr; ++r)
+            bulk_g2s(st + r * SG_CH, K + (r0 + r) * ldk + col0, cols * 4u, &full[stage]);
+          if (++stage == SG_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  double *wacc = acc + (size_t)warp * SG_ROWS * k;
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int64_t gi = item / nsplit;
+    const int s = (int)(item % nsplit);
+    const int64_t q0 = (int64_t)s * chunks_per_split;
+    const int64_t q1 = q0 + chunks_per_split < nchunks ? q0 + chunks_per_split : nchunks;
+    for (int t = lane; t < SG_ROWS * k; t += 32) wacc[t] = 0.0;
+    __syncwarp();
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t col0 = q * SG_CH;
+      const int cols = (int)(ldk - col0 < SG_CH ? ldk - col0 : SG_CH);
+      mbar_wait(&full[stage], phase);
+      const float *st = ring + (size_t)stage * (SG_ROWS + 1) * SG_CH;
+      const uint32_t *cd = reinterpret_cast<const uint32_t *>(st + SG_ROWS * SG_CH);
+      for (int g = warp; g < (cols >> 5); g += SG_CWARPS) {
+        const uint32_t code = cd[g * 32 + lane];
+        const int src = (int)(code & 0xFFu), lab = (int)((code >> 8) & 0xFFu);
+        const int rem = (int)((code >> 16) & 0xFFu);
+        const bool head = (code >> 24) != 0u && lab < k;
+        // warp-uniform number of scan steps: enough for the group's longest segment
+        const int maxrem = __reduce_max_sync(0xffffffffu, (unsigned)rem);
+        const int steps = 32 - __clz(maxrem);  // ceil(log2(maxrem + 1))
+        const float *colp = st + g * 32 + src;
+        float v[SG_ROWS];
+#pragma unroll
+        for (int r = 0; r < SG_ROWS; ++r) v[r] = colp[r * SG_CH];
+        // segmented suffix scan, the 8 rows interleaved so their shuffles overlap
+#pragma unroll
+        for (int o = 1, st_ = 0; o < 32; o <<= 1, ++st_) {
+          if (st_ < steps) {
+            float t[SG_ROWS];
+#pragma unroll
+            for (int r = 0; r < SG_ROWS; ++r) t[r] = __shfl_down_sync(0xffffffffu, v[r], o);
+            if (o <= rem) {
+#pragma unroll
+              for (int r = 0; r < SG_ROWS; ++r) v[r] += t[r];
+            }
+          }
+        }
+        if (head) {
+#pragma unroll
+          for (int r = 0; r < SG_ROWS; ++r) wacc[r * k + lab] += (double)v[r];
+        }
+        __syncwarp();  // order this group's accumulator updates before the next group's
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == SG_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(SG_CWARPS * 32));
+    const int64_t r0 = gi * SG_ROWS;
+    for (int t = threadIdx.x; t < SG_ROWS * k; t += SG_CWARPS * 32) {
+      const int r = t / k, c = t % k;
+      if (r0 + r < nrows) {
+        double sum = 0.0;
+        for (int w = 0; w < SG_CWARPS; ++w) sum += acc[((size_t)w * SG_ROWS + r) * k + c];
+        Spart[((int64_t)s * rows_pad + r0 + r) * k + c] = sum;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(SG_CWARPS * 32));
+  }
+}
+
+}  // namespace kkm
