@@ -281,12 +281,12 @@ int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(spmm_onehot_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)spmm_smem_bytes()));
+                            (int)spmm_smem_bytes<KP>()));
     attr_set = true;
   }
-  const int64_t items = ceil_div(P.nA, SP_ROWS) * P.nsplit;
+  const int64_t items = ceil_div(P.nA, SpRows<KP>::R) * P.nsplit;
   const int grid = (int)std::min<int64_t>(items, h->num_sms);
-  spmm_onehot_kernel<KP><<<grid, SP_THREADS, spmm_smem_bytes(), h->st>>>(
+  spmm_onehot_kernel<KP><<<grid, SpRows<KP>::THREADS, spmm_smem_bytes<KP>(), h->st>>>(
       h->K, P.ldk, P.nA, labels, P.k, c0, P.nsplit, P.chunks_per_split, P.nApad, h->Spart);
   CKL();
   return KKM_OK;
@@ -392,7 +392,9 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, double *E_out, double *cn
   const int32_t *sizes = h->sizes[h->cur];
   const int k1 = P.k + 1;
   if (P.nloc > 0) {
-    finalize_kernel<<<P.nfin, FIN_THREADS, (size_t)k1 * FIN_THREADS * 8, h->st>>>(
+    int fth = FIN_THREADS;  // power of two with (k+1) * fth doubles <= 48 KB
+    while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
+    finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
         S, nsplit, P.nloc, P.pr > 1 ? P.B : P.nApad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
         E_out, h->blockpart);
     CKL();

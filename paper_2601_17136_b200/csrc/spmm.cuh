@@ -20,25 +20,38 @@
 
 namespace kkm {
 
-constexpr int SP_ROWS = 4;          // rows per work item
-constexpr int SP_CH = 2048;         // columns per chunk
-constexpr int SP_STAGES = 4;        // smem ring depth
-constexpr int SP_CWARPS = 8;        // consumer warps
-constexpr int SP_THREADS = (SP_CWARPS + 1) * 32;
-constexpr int SP_MAX_CHUNKS_PER_SPLIT = 64;  // bounds fp32 terms per lane
+constexpr int SP_CH = 1024;         // columns per chunk
+constexpr int SP_CWARPS_MAX = 8;
+constexpr int SP_MAX_CHUNKS_PER_SPLIT = 128;  // bounds fp32 terms per lane (<= 512 per lane)
 constexpr int SP_KPMAX = 16;
 
+// R rows per work item: the one-hot masks are per column and shared by all R rows, so more
+// rows amortise them; R is bounded by the 2 R KP accumulator registers.
+template <int KP>
+struct SpRows {
+  static constexpr int R = KP <= 10 ? 8 : 4;     // 2 R KP accumulator registers per thread
+  static constexpr int STAGES = R == 8 ? 4 : 7;  // ~140-150 KB of K in flight
+  // 4 consumer warps + the producer keep <= 2 warps per SM sub-partition (16K registers each),
+  // so 8-row items get their ~230 registers (measured: 4 warps also beat 8 for 4-row items)
+  static constexpr int CW = 4;
+  static constexpr int THREADS = (CW + 1) * 32;
+};
+
+template <int KP>
 constexpr size_t spmm_smem_bytes() {
-  return (size_t)SP_STAGES * (SP_ROWS + 1) * SP_CH * 4 + SP_CWARPS * SP_ROWS * SP_KPMAX * 4 +
-         2 * SP_STAGES * 8 + 64;
+  return (size_t)SpRows<KP>::STAGES * (SpRows<KP>::R + 1) * SP_CH * 4 +
+         SpRows<KP>::CW * SpRows<KP>::R * SP_KPMAX * 4 + 2 * SpRows<KP>::STAGES * 8 + 64;
 }
 
 // Spart[(s * rows_pad + i) * k + c0 + c] for clusters c0 .. c0 + KP - 1 (c0 + c < k).
 template <int KP>
-__global__ void __launch_bounds__(SP_THREADS, 1)
+__global__ void __launch_bounds__(SpRows<KP>::THREADS, 1)
     spmm_onehot_kernel(const float *__restrict__ K, int64_t ldk, int64_t nrows,
                        const int32_t *__restrict__ labels, int k, int c0, int nsplit,
                        int chunks_per_split, int64_t rows_pad, double *__restrict__ Spart) {
+  constexpr int SP_ROWS = SpRows<KP>::R;
+  constexpr int SP_STAGES = SpRows<KP>::STAGES;
+  constexpr int SP_CWARPS = SpRows<KP>::CW;
   extern __shared__ __align__(128) uint8_t smem[];
   float *ring = reinterpret_cast<float *>(smem);  // [STAGES][ROWS + 1][CH]
   float *red = ring + (size_t)SP_STAGES * (SP_ROWS + 1) * SP_CH;  // [CWARPS][ROWS][KPMAX]

@@ -15,19 +15,20 @@ namespace kkm {
 
 constexpr int FIN_THREADS = 128;
 
-// grid: nblocks; block b handles rows [b * rows_per_block, ...). Dynamic smem:
-// (k + 1) * FIN_THREADS doubles.
-__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(
+// grid: nblocks; block b handles rows [b * rows_per_block, ...). blockDim.x: a power of two
+// <= FIN_THREADS; dynamic smem: (k + 1) * blockDim.x doubles.
+__global__ void __launch_bounds__(128) finalize_kernel(
     const double *__restrict__ Spart, int nsplit, int64_t nrows, int64_t rows_pad, int k,
     const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl_local,
     const double *__restrict__ diag, int64_t rows_per_block, double *__restrict__ E,
     double *__restrict__ blockpart) {
-  extern __shared__ double sacc[];  // [(k + 1)][FIN_THREADS]
+  extern __shared__ double sacc[];  // [(k + 1)][blockDim.x]
+  const int T = blockDim.x;
   const int t = threadIdx.x;
-  for (int c = 0; c <= k; ++c) sacc[c * FIN_THREADS + t] = 0.0;
+  for (int c = 0; c <= k; ++c) sacc[c * T + t] = 0.0;
   const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
   const int64_t re = rb + rows_per_block < nrows ? rb + rows_per_block : nrows;
-  for (int64_t i = rb + t; i < re; i += FIN_THREADS) {
+  for (int64_t i = rb + t; i < re; i += T) {
     const int li = cl_local[i];
     double zi = 0.0;
     for (int c = 0; c < k; ++c) {
@@ -38,16 +39,16 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(
       E[i * k + c] = e;
       if (c == li) zi = e;
     }
-    sacc[li * FIN_THREADS + t] += zi;
-    sacc[k * FIN_THREADS + t] += diag[i] - zi;
+    sacc[li * T + t] += zi;
+    sacc[k * T + t] += diag[i] - zi;
   }
   __syncthreads();
-  for (int w = FIN_THREADS / 2; w > 0; w >>= 1) {
+  for (int w = T / 2; w > 0; w >>= 1) {
     if (t < w)
-      for (int c = 0; c <= k; ++c) sacc[c * FIN_THREADS + t] += sacc[c * FIN_THREADS + t + w];
+      for (int c = 0; c <= k; ++c) sacc[c * T + t] += sacc[c * T + t + w];
     __syncthreads();
   }
-  for (int c = t; c <= k; c += FIN_THREADS) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sacc[c * FIN_THREADS];
+  for (int c = t; c <= k; c += T) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sacc[c * T];
 }
 
 // out[c] = sum_b blockpart[b][c] in ascending b (one thread per c).

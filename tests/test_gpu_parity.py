@@ -84,11 +84,18 @@ def test_har_like_gaussian_teacher_forced(precision):
 
 @pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
 def test_many_clusters_multipass(precision):
-    """k = 21 > 16 exercises the multi-pass one-hot SpMM; linear kernel."""
+    """k = 21 > 16: the label-sorted-group SpMM (v2); linear kernel."""
     if precision[1] == kkm.PATH_STREAM:
         pytest.skip("the streaming path supports k <= 16 (KKM_EUNSUP, tested in test_abi)")
     X = synth.blobs(1500, 16, 21, seed=3, sep=4.0)
     teacher_forced(X, 21, oracle.LINEAR, iters=3, precision=precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS[:2], ids=PREC_IDS[:2])
+def test_very_many_clusters(precision):
+    """k = 70 > 64: the one-hot SpMM in ceil(k/16) passes (materialised only)."""
+    X = synth.blobs(600, 8, 70, seed=6, sep=3.0)
+    teacher_forced(X, 70, oracle.POLY, 0.2, 1.0, 2, iters=2, precision=precision)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
