@@ -399,7 +399,7 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, double *E_out, double *cn
         E_out, h->blockpart);
     CKL();
   }
-  cnorm_local_kernel<<<1, 128, 0, h->st>>>(h->blockpart, P.nloc > 0 ? P.nfin : 0, P.k,
+  cnorm_local_kernel<<<1, 32 * std::min(32, k1), 0, h->st>>>(h->blockpart, P.nloc > 0 ? P.nfin : 0, P.k,
                                            h->rankpart + (int64_t)P.rank * k1);
   CKL();
   if (P.nranks > 1)
@@ -631,6 +631,14 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   if (rc == KKM_OK && P.pr > 1) {  // process-column communicator: ranks gi + gj * pr, key gi
     ncclResult_t r = ncclCommSplit(h->comm, P.gj, P.gi, &h->colcomm, nullptr);
     if (r != ncclSuccess) rc = fail(KKM_ENCCL, "ncclCommSplit: %s", ncclGetErrorString(r));
+    // one reduce-scatter of the real size now, so the communicator's connection setup is part
+    // of the one-time init and not of the first iterations
+    if (rc == KKM_OK) {
+      cudaMemsetAsync(h->Scol, 0, (size_t)P.nApad * P.k * 8, h->st);
+      r = ncclReduceScatter(h->Scol, h->Smine, (size_t)P.B * P.k, ncclDouble, ncclSum, h->colcomm, h->st);
+      if (r != ncclSuccess) rc = fail(KKM_ENCCL, "ncclReduceScatter (warm-up): %s", ncclGetErrorString(r));
+      else if (cudaStreamSynchronize(h->st) != cudaSuccess) rc = fail(KKM_ECUDA, "warm-up sync failed");
+    }
   }
   if (rc) {
     delete h;

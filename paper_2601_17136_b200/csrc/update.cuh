@@ -51,13 +51,17 @@ __global__ void __launch_bounds__(128) finalize_kernel(
   for (int c = t; c <= k; c += T) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sacc[c * T];
 }
 
-// out[c] = sum_b blockpart[b][c] in ascending b (one thread per c).
+// out[c] = sum_b blockpart[b][c]: one warp per c, lane l sums b = l, l + 32, ... in order,
+// then a fixed shuffle tree (deterministic, independent of timing).
 __global__ void cnorm_local_kernel(const double *__restrict__ blockpart, int nblocks, int k,
                                    double *__restrict__ out) {
-  for (int c = threadIdx.x; c <= k; c += blockDim.x) {
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x >> 5; c <= k; c += nw) {
     double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += blockpart[(int64_t)b * (k + 1) + c];
-    out[c] = s;
+    for (int b = lane; b < nblocks; b += 32) s += blockpart[(int64_t)b * (k + 1) + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = s;
   }
 }
 

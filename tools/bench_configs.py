@@ -42,6 +42,18 @@ peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.absp
                                     "MEASURED_PEAKS.json")))
 path = {"auto": kkm.PATH_AUTO, "mat": kkm.PATH_MATERIALIZE, "stream": kkm.PATH_STREAM}[a.path]
 
+# warm-up: load every kernel module once on a tiny problem (lazy loading is per kernel, not per size)
+for wpath in (kkm.PATH_MATERIALIZE, kkm.PATH_STREAM):
+    for wk in (2, 6, 10):
+        wn = 2048
+        r0, r1 = kkm.shard_begin(wn, rank, world), kkm.shard_begin(wn, rank + 1, world)
+        Xw = torch.from_numpy(synth.blobs(wn, 784, wk, seed=1, rows=np.arange(r0, r1))).to(dev)
+        hw = kkm.KernelKMeans(Xw, wn, wk, kkm.KERNEL_GAUSSIAN, 1e-3, 0.0, 1, max_iter=1, rank=rank,
+                              nranks=world, comm=comm, path=wpath, grid_rows=a.grid_rows)
+        hw.fit()
+        hw.destroy()
+torch.cuda.synchronize()
+
 for name in a.configs.split(","):
     cfg = dict(synth.CONFIGS[name])
     n = a.n or cfg["n"]
