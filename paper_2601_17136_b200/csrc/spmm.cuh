@@ -20,7 +20,8 @@
 
 namespace kkm {
 
-constexpr int SP_CH = 1024;         // columns per chunk
+template <int KP>
+struct SpRows;
 constexpr int SP_CWARPS_MAX = 8;
 constexpr int SP_MAX_CHUNKS_PER_SPLIT = 128;  // bounds fp32 terms per lane (<= 512 per lane)
 constexpr int SP_KPMAX = 16;
@@ -30,7 +31,8 @@ constexpr int SP_KPMAX = 16;
 template <int KP>
 struct SpRows {
   static constexpr int R = KP <= 10 ? 8 : 4;     // 2 R KP accumulator registers per thread
-  static constexpr int STAGES = R == 8 ? 4 : 7;  // ~140-150 KB of K in flight
+  static constexpr int CH = R == 8 ? 2048 : 1024;  // columns per chunk
+  static constexpr int STAGES = R == 8 ? 3 : 7;  // ~140-220 KB of K in flight
   // 4 consumer warps + the producer keep <= 2 warps per SM sub-partition (16K registers each),
   // so 8-row items get their ~230 registers (measured: 4 warps also beat 8 for 4-row items)
   static constexpr int CW = 4;
@@ -39,7 +41,7 @@ struct SpRows {
 
 template <int KP>
 constexpr size_t spmm_smem_bytes() {
-  return (size_t)SpRows<KP>::STAGES * (SpRows<KP>::R + 1) * SP_CH * 4 +
+  return (size_t)SpRows<KP>::STAGES * (SpRows<KP>::R + 1) * SpRows<KP>::CH * 4 +
          SpRows<KP>::CW * SpRows<KP>::R * SP_KPMAX * 4 + 2 * SpRows<KP>::STAGES * 8 + 64;
 }
 
@@ -52,6 +54,7 @@ __global__ void __launch_bounds__(SpRows<KP>::THREADS, 1)
   constexpr int SP_ROWS = SpRows<KP>::R;
   constexpr int SP_STAGES = SpRows<KP>::STAGES;
   constexpr int SP_CWARPS = SpRows<KP>::CW;
+  constexpr int SP_CH = SpRows<KP>::CH;
   extern __shared__ __align__(128) uint8_t smem[];
   float *ring = reinterpret_cast<float *>(smem);  // [STAGES][ROWS + 1][CH]
   float *red = ring + (size_t)SP_STAGES * (SP_ROWS + 1) * SP_CH;  // [CWARPS][ROWS][KPMAX]
@@ -132,11 +135,11 @@ __global__ void __launch_bounds__(SpRows<KP>::THREADS, 1)
           const int cc = c0 + c;
           const float m0 = mask_eq(l.x, cc), m1 = mask_eq(l.y, cc);
           const float m2 = mask_eq(l.z, cc), m3 = mask_eq(l.w, cc);
+          // the two updates of acc[r][c] are SP_ROWS instructions apart (FFMA2 latency)
 #pragma unroll
-          for (int r = 0; r < SP_ROWS; ++r) {
-            ffma2(acc[r][c], x[r].x, x[r].y, m0, m1);
-            ffma2(acc[r][c], x[r].z, x[r].w, m2, m3);
-          }
+          for (int r = 0; r < SP_ROWS; ++r) ffma2(acc[r][c], x[r].x, x[r].y, m0, m1);
+#pragma unroll
+          for (int r = 0; r < SP_ROWS; ++r) ffma2(acc[r][c], x[r].z, x[r].w, m2, m3);
         }
       }
       __syncwarp();

@@ -136,6 +136,7 @@ __device__ __forceinline__ void t2_producer(const Sched &sc, const T2Smem &s, co
                                             const CUtensorMap *a_lo, const CUtensorMap *b_hi,
                                             const CUtensorMap *b_lo, int nkb, uint32_t cr, int hint) {
   const uint64_t keep = hint ? l2_policy_evict_last() : l2_policy_evict_normal();
+  const uint64_t bpol = keep;  // (evict_normal on the streaming B measured slower)
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   int stage = 0;
   uint32_t phase = 0;
@@ -152,8 +153,8 @@ __device__ __forceinline__ void t2_producer(const Sched &sc, const T2Smem &s, co
         const int ar = ra + (int)cr * 128, br = rb + (int)cr * 128;
         tma_load_2d_pair(st, a_hi, kc, ar, &s.full[stage], keep);
         tma_load_2d_pair(st + T2_HALF_BYTES, a_lo, kc, ar, &s.full[stage], keep);
-        tma_load_2d_pair(st + 2 * T2_HALF_BYTES, b_hi, kc, br, &s.full[stage], keep);
-        tma_load_2d_pair(st + 3 * T2_HALF_BYTES, b_lo, kc, br, &s.full[stage], keep);
+        tma_load_2d_pair(st + 2 * T2_HALF_BYTES, b_hi, kc, br, &s.full[stage], bpol);
+        tma_load_2d_pair(st + 3 * T2_HALF_BYTES, b_lo, kc, br, &s.full[stage], bpol);
         if (++stage == T2_STAGES) {
           stage = 0;
           phase ^= 1;
