@@ -135,8 +135,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.nsplit = (int)ns;
     P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
   } else if (P.materialize) {
-    // chunk width of the k-specialised one-hot kernel (spmm.cuh SpRows): 2048 for 8-row items
-    const int ch = ((P.k + 1) / 2 * 2) <= 10 ? 2048 : 1024;
+    const int ch = 2048;  // chunk width of the one-hot kernel (spmm.cuh SpRows::CH)
     const int64_t nchunks = ceil_div(P.ldk, ch);
     P.nsplit = (int)ceil_div(nchunks, SP_MAX_CHUNKS_PER_SPLIT * 1024 / ch);
     P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);

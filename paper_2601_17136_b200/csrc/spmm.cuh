@@ -31,8 +31,8 @@ constexpr int SP_KPMAX = 16;
 template <int KP>
 struct SpRows {
   static constexpr int R = KP <= 10 ? 8 : 4;     // 2 R KP accumulator registers per thread
-  static constexpr int CH = R == 8 ? 2048 : 1024;  // columns per chunk
-  static constexpr int STAGES = R == 8 ? 3 : 7;  // ~140-220 KB of K in flight
+  static constexpr int CH = 2048;                 // columns per chunk (fewer stage handshakes)
+  static constexpr int STAGES = R == 8 ? 3 : 5;  // 216 / 200 KB of K + labels in flight
   // 4 consumer warps + the producer keep <= 2 warps per SM sub-partition (16K registers each),
   // so 8-row items get their ~230 registers (measured: 4 warps also beat 8 for 4-row items)
   static constexpr int CW = 4;
