@@ -261,9 +261,11 @@ def run_ours(args):
         gemm_tfs = gemm_flops / (gemm_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "spmm_traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp):  # only a capture of this same launch shape (per-launch bytes)
             with open(tp) as f:
-                traffic = json.load(f).get("bytes_per_launch")
+                cap = json.load(f)
+            if abs(cap.get("algorithmic_bytes", 0) - spmm_bytes) <= 0.01 * spmm_bytes:
+                traffic = cap.get("bytes_per_launch")
         tensor = precision in (kkm.PREC_BF16X3, kkm.PREC_FP16X3)
         # 3 dense 16-bit MMAs per useful product: useful-flop peak = measured bf16 dense / 3
         # (fp16 and bf16 share the dense rate); SIMT: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz

@@ -62,7 +62,8 @@ extern "C" {
 #define KKM_PATH_MATERIALIZE 1 /* K rows of this rank stored fp32 in HBM once               */
 #define KKM_PATH_STREAM 2      /* K tiles recomputed every iteration by the fused tensor-core
                                   kernel and reduced in TMEM/registers; K never stored.
-                                  Needs FP16X3/BF16X3 and k <= 16 (else KKM_EUNSUP)        */
+                                  Needs FP16X3/BF16X3 (else KKM_EUNSUP). k > 16: one launch
+                                  per group of 16 clusters (host reads k+1 ints per iter.) */
 
 /* ---- precision of the a1 contraction (reading A9) ----------------------- */
 #define KKM_PREC_BF16X3 0    /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi, bf16 split of x;
@@ -167,6 +168,23 @@ int kkm_objective(kkm_handle h, double *J);
 /* Replaces the current labels (n int32 in [0,k), host or device, identical on
  * every rank): used for teacher-forced parity and for resuming. */
 int kkm_set_labels(kkm_handle h, const int32_t *labels);
+
+/* Out-of-sample assignment: assigns m new points y to the
+ * clusters of the CURRENT labels with the same distance as an iteration,
+ *   D(y, c) = kappa(y, y) - (2/|L_c|) sum_{j in L_c} kappa(y, x_j) + c(c)
+ * (Eq. d of PAPER.md §2.2 P:160-168 with Eq. e for a row of K(Y, X); c = ||mu_c||^2,
+ * Eq. c), lowest index on ties, empty clusters never chosen (A6, A7). K(Y, X) is
+ * never stored: the fused streaming kernel runs with A = Y, B = X sorted by label.
+ *   Y:          host or device, m x d fp32 row-major, row pitch ldy >= d floats.
+ *   labels_out: host or device, m int32 (out).
+ *   D_out:      host or device, m x k fp64 (out), or NULL. +inf for empty clusters.
+ * Local to the calling rank (every rank holds all of X and the labels). Needs
+ * c of the current labels: valid after kkm_fit or kkm_objective; otherwise one
+ * kkm_objective pass is run first when nranks == 1 and KKM_ESTATE is returned
+ * when nranks > 1 (that pass is collective). KKM_EUNSUP for FP32_SIMT handles.
+ * Temporary device memory (~m*(6d + 8k*splits) + n*(4d) bytes) comes from the
+ * stream-ordered allocator (KKM_ENOMEM if it fails). Synchronises the stream. */
+int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *labels_out, double *D_out);
 
 /* Copies an internal array of the last iteration (selectors KKM_DBG_*) to dst
  * (host or device). Synchronises. Test hook. */

@@ -49,6 +49,7 @@ def lib():
             "orc_objective": [P, P, i64, i32, P, P],
             "orc_assign": [P, P, P, i64, i32, P, P],
             "orc_fit": [P, P, i64, i32, i32, i32, P, P, P, P, P],
+            "orc_predict": [P, i64, P, i64, i64, P, i32, P, ctypes.c_int, f64, f64, ctypes.c_int, P, P],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -200,3 +201,18 @@ def fit(X, k, kind, gamma=1.0, coef0=0.0, degree=1, max_iter=30, init_labels=Non
     out = fit_K(K, diag, k, max_iter, init_labels, stop_on_no_change, keep_trace)
     out["K"], out["diag"] = K, diag
     return out
+
+
+def predict(X, labels, k, cn, Y, kind, gamma=1.0, coef0=0.0, degree=1):
+    """Out-of-sample assignment of Y to the clusters of (X, labels) with centroid norms cn.
+    Returns (labels_Y, Dfull_Y)."""
+    X = _X(X)
+    Y = np.ascontiguousarray(Y, dtype=np.float32)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    cn = np.ascontiguousarray(cn, dtype=np.float64)
+    m = Y.shape[0]
+    out = np.empty(m, dtype=np.int32)
+    D = np.empty((m, k), dtype=np.float64)
+    _check(lib().orc_predict(_p(X), X.shape[0], _p(Y), m, X.shape[1], _p(labels), k, _p(cn), kind,
+                             gamma, coef0, degree, _p(out), _p(D)), "predict")
+    return out, D

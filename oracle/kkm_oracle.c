@@ -275,3 +275,47 @@ int orc_fit(const double *K, const double *diag, int64_t n, int32_t k, int32_t m
   free(nl);
   return rc;
 }
+
+/* Out-of-sample assignment (reading A21 extended): for each new point y,
+ * the feature-space distance to each centroid of the training labels cl,
+ *   D(y, c) = kappa(y, y) - (2/|L_c|) sum_{j in L_c} kappa(y, x_j) + c(c),
+ * the same Eq. (d) with E(y, c) = (1/|L_c|) sum_{j in L_c} kappa(y, x_j) (Eq. e for
+ * a row of K(Y, X)) and c = ||mu_c||^2 of the training clustering (Eq. c). Lowest index wins
+ * ties, empty clusters are never chosen (A6, A7). cnorm: the k centroid norms (e.g. from
+ * orc_cnorm on the training E). Y is m x d fp32 row-major (ld d). Dfull may be NULL. */
+int orc_predict(const float *X, int64_t n, const float *Y, int64_t m, int64_t d, const int32_t *labels,
+                int32_t k, const double *cnorm, int kind, double gamma, double coef0, int degree,
+                int32_t *out_labels, double *Dfull) {
+  if (n < 1 || m < 0 || d < 1 || k < 1 || check_kernel(kind, gamma, degree)) return ORC_EINVAL;
+  int64_t *sizes = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+  if (!sizes) return ORC_ENOMEM;
+  int rc = orc_sizes(labels, n, k, sizes);
+  if (rc != ORC_OK) {
+    free(sizes);
+    return rc;
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < m; ++i) {
+    const float *y = Y + i * d;
+    const double kyy = orc_kappa(y, y, d, kind, gamma, coef0, degree);
+    int32_t best = 0;
+    double best_d = INFINITY;
+    for (int32_t c = 0; c < k; ++c) {
+      double dsh = INFINITY;
+      if (sizes[c] > 0) {
+        double s = 0.0;
+        for (int64_t j = 0; j < n; ++j)
+          if (labels[j] == c) s += orc_kappa(y, X + j * d, d, kind, gamma, coef0, degree);
+        dsh = -2.0 * (s / (double)sizes[c]) + cnorm[c];
+      }
+      if (Dfull) Dfull[i * k + c] = kyy + dsh;
+      if (dsh < best_d) {
+        best_d = dsh;
+        best = c;
+      }
+    }
+    out_labels[i] = best;
+  }
+  free(sizes);
+  return ORC_OK;
+}

@@ -121,7 +121,6 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (!P.materialize) {
     if (!P.tc)
       return fail(KKM_EUNSUP, "the streaming path needs a tensor-core precision (FP16X3 or BF16X3)");
-    if (P.k > 16) return fail(KKM_EUNSUP, "the streaming path supports k <= 16 (k=%d)", P.k);
   }
   // v1 (one-hot FFMA2) is faster for k <= 16 (5.4 TB/s at k = 10); v2 (sorted groups, shuffle
   // bound at ~3.9 TB/s for any k) replaces v1's ceil(k/16) passes over K for 16 < k <= 64.
@@ -239,6 +238,7 @@ struct kkm_ctx {
   int cur = 0;  // labels[cur] / sizes[cur] are the labels entering the next iteration
   bool poisoned = false;
   bool have_last = false;
+  bool cnorm2_valid = false;  // cnorm2 holds c of the current labels (after kkm_fit / kkm_objective)
   int64_t launches = 0;
   float phase_ms[KKM_NPHASES] = {0, 0, 0, 0, 0};
   KappaParams kp;
@@ -304,32 +304,82 @@ int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
   return KKM_OK;
 }
 
-// Streaming a1+a2: sort the B set's points by label, gather the split operands in that order,
-// then the fused tensor-core kernel writes S partials (Spart) for the A set's rows.
-int launch_stream(kkm_ctx *h, const int32_t *labels) {
+// Label-sorted copy of a point set (the B operand of the streaming kernel) and its sort.
+struct SortedSet {
+  uint16_t *hi, *lo;
+  float *norms, *rscale;
+  int32_t *perm, *pos, *seg, *bcount, *boff;
+};
+
+// Sorts the points [b0, b0 + nB) of the handle's X by label (stable counting sort) and gathers
+// their split operands, norms and scales in that order into o (rows [nB, rows) zeroed).
+int sort_gather(kkm_ctx *h, const int32_t *labB, int64_t b0, int64_t nB, int64_t rows, const SortedSet &o) {
   const Plan &P = h->P;
   const int k = P.k;
-  const int32_t *labB = labels + P.b0;
-  sort_count_kernel<<<P.sort_blocks, 256, (size_t)k * 4, h->st>>>(labB, P.nB, k, h->bcount);
+  const int nblk = (int)ceil_div(std::max<int64_t>(nB, 1), SORT_BLOCK);
+  sort_count_kernel<<<nblk, 256, (size_t)k * 4, h->st>>>(labB, nB, k, o.bcount);
   CKL();
-  sort_scan_kernel<<<k + 1, 1024, 1024 * 4, h->st>>>(h->bcount, P.sort_blocks, k, h->boff, h->seg);
+  sort_scan_kernel<<<k + 1, 1024, 1024 * 4, h->st>>>(o.bcount, nblk, k, o.boff, o.seg);
   CKL();
-  sort_scatter_kernel<<<P.sort_blocks, 256, (size_t)9 * k * 4, h->st>>>(labB, P.nB, k, h->boff, h->perm,
-                                                                        h->pos);
+  sort_scatter_kernel<<<nblk, 256, (size_t)9 * k * 4, h->st>>>(labB, nB, k, o.boff, o.perm, o.pos);
   CKL();
-  gather_rows_kernel<<<(unsigned)ceil_div(P.npad, 8), 256, 0, h->st>>>(
-      h->Xhi, h->Xlo, h->norms, h->rscale, h->perm, P.b0, P.nB, P.npad, P.dp, h->Shi, h->Slo, h->snorms,
-      h->srscale);
+  gather_rows_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, h->st>>>(h->Xhi, h->Xlo, h->norms, h->rscale, o.perm, b0,
+                                                                     nB, rows, P.dp, o.hi, o.lo, o.norms, o.rscale);
   CKL();
-  if (P.nA == 0) return KKM_OK;
-  int rc = tc2_stream_launch(h->ts, h->Xhi, h->Xlo, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.nB, P.b0, P.a0,
-                             P.nA, P.nApad, h->norms, h->rscale, h->snorms, h->srscale, h->pos, h->seg, k,
-                             h->kp, P.nsplit / 2, h->Spart, h->st, &h->launches);
-  if (rc) {
-    h->poisoned = true;
-    return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
+  return KKM_OK;
+}
+
+// The streaming kernel's A operand: rows [row0, row0 + nA) of a split operand with arows rows.
+struct StreamA {
+  const uint16_t *hi, *lo;
+  const float *norms, *rscale;
+  int64_t arows, row0, nA, rows_pad;
+};
+
+// One fused a1+a2 pass: Spart[nsplit][rows_pad][k] = per-split sums over the sorted set B (nB
+// points, brows rows) of kappa(a_i, b_p) by cluster. pos (NULL if A and B are disjoint): sorted
+// position of A row i for b0 <= i < b0 + nB (the Gaussian diagonal). k <= 16: one launch; else
+// one launch per group of 16 clusters over that group's contiguous sorted rows (same total
+// work; the host reads the k + 1 segment starts first).
+int stream_pass(kkm_ctx *h, TcStream &ts, const StreamA &A, const SortedSet &B, int64_t brows, int64_t nB,
+                int64_t b0, const int32_t *pos, int nsplit, double *Spart) {
+  const Plan &P = h->P;
+  const int k = P.k;
+  if (A.nA == 0) return KKM_OK;
+  auto launch = [&](int64_t s0, int64_t nb, int c0, int kg) -> int {
+    int rc = tc2_stream_launch(ts, A.hi, A.lo, B.hi + s0 * P.dp, B.lo + s0 * P.dp, P.fp16, A.arows, brows - s0, P.dp,
+                               nb, b0, A.row0, A.nA, A.rows_pad, A.norms, A.rscale, B.norms + s0, B.rscale + s0, pos,
+                               nB, B.seg + c0, kg, h->kp, nsplit / 2, Spart, k, c0, h->st, &h->launches);
+    if (rc) {
+      h->poisoned = true;
+      return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
+    }
+    return KKM_OK;
+  };
+  if (k <= 16) return launch(0, nB, 0, k);
+  std::vector<int32_t> seg((size_t)k + 1);
+  CK(cudaMemcpyAsync(seg.data(), B.seg, (size_t)(k + 1) * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  for (int c0 = 0; c0 < k; c0 += 16) {
+    const int kg = std::min(16, k - c0);
+    const int64_t s0 = seg[c0], nb = seg[c0 + kg] - s0;
+    if (nb == 0) {  // all clusters of the group empty: their partials are 0
+      CK(cudaMemset2DAsync(Spart + c0, (size_t)k * 8, 0, (size_t)kg * 8, (size_t)nsplit * A.rows_pad, h->st));
+      continue;
+    }
+    CKR(launch(s0, nb, c0, kg));
   }
   return KKM_OK;
+}
+
+// Streaming a1+a2 of the clustering loop: sort the B set by label, then the fused kernel writes
+// the S partials (Spart) of the A set's rows.
+int launch_stream(kkm_ctx *h, const int32_t *labels) {
+  const Plan &P = h->P;
+  const SortedSet B{h->Shi, h->Slo, h->snorms, h->srscale, h->perm, h->pos, h->seg, h->bcount, h->boff};
+  CKR(sort_gather(h, labels + P.b0, P.b0, P.nB, P.npad, B));
+  const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.a0, P.nA, P.nApad};
+  return stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nsplit, h->Spart);
 }
 
 // a2 on the materialised K tile (A set rows x B set columns).
@@ -703,6 +753,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
     int ns = 0;
     CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
     CKR(run_cnorm(h, S, ns, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
+    h->cnorm2_valid = true;
   }
   std::vector<double> J((size_t)t + 1);
   std::vector<unsigned long long> ch((size_t)std::max(t, 1));
@@ -745,6 +796,7 @@ int kkm_objective(kkm_handle h, double *J) {
   int ns = 0;
   CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
   CKR(run_cnorm(h, S, ns, h->E2, h->cnorm2, slot, nullptr, nullptr));
+  h->cnorm2_valid = true;
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return KKM_OK;
@@ -768,9 +820,88 @@ int kkm_set_labels(kkm_handle h, const int32_t *labels) {
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, h->bad, 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  if (bad) return fail(KKM_ELABEL, "%d labels outside [0, %d)", bad, P.k);
   h->have_last = false;
+  h->cnorm2_valid = false;
+  if (bad) return fail(KKM_ELABEL, "%d labels outside [0, %d)", bad, P.k);
   return KKM_OK;
+}
+
+int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *labels_out, double *D_out) {
+  if (!h) return fail(KKM_EINVAL, "handle is NULL");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  const Plan &P = h->P;
+  if (m < 0) return fail(KKM_EINVAL, "m=%lld < 0", (long long)m);
+  if (m == 0) return KKM_OK;
+  if (!Y || !labels_out) return fail(KKM_EINVAL, "NULL argument");
+  if (ldy < P.d) return fail(KKM_EINVAL, "ldy=%lld < d=%lld", (long long)ldy, (long long)P.d);
+  if (!P.tc) return fail(KKM_EUNSUP, "kkm_predict needs a tensor-core precision (FP16X3 or BF16X3)");
+  if (!h->cnorm2_valid) {  // c of the current labels: the kkm_objective pass (collective for nranks > 1)
+    if (P.nranks > 1) return fail(KKM_ESTATE, "call kkm_fit or kkm_objective on every rank before kkm_predict");
+    double J = 0.0;
+    CKR(kkm_objective(h, &J));
+  }
+  const int k = P.k;
+  const int64_t mpad = round_up(m, 256);
+  const int nblk = (int)ceil_div(P.n, SORT_BLOCK);
+  const int64_t tiles_n = ceil_div(P.n, 256);
+  const int nsplit =
+      2 * (int)std::max<int64_t>(ceil_div(tiles_n, 512), ts_choose_splits((m + 1) / 2, P.n, h->num_sms / 2));
+  // one temporary block: Y operands, sort scratch, sorted X (materialised handles), partials
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  const size_t oYf = take((size_t)mpad * P.ldf * 4), oYhi = take((size_t)mpad * P.dp * 2),
+               oYlo = take((size_t)mpad * P.dp * 2), oYn = take((size_t)mpad * 4), oYr = take((size_t)mpad * 4),
+               oYd = take((size_t)m * 8), oSp = take((size_t)nsplit * mpad * k * 8), oLab = take((size_t)m * 4),
+               oD = D_out ? take((size_t)m * k * 8) : 0, oPerm = take((size_t)P.lablen * 4),
+               oPos = take((size_t)P.lablen * 4), oSeg = take((size_t)(k + 1) * 4),
+               oBc = take((size_t)nblk * k * 4), oBo = take((size_t)nblk * k * 4);
+  const bool own_sorted = P.materialize;  // streaming handles lend their sorted-operand scratch
+  const size_t oShi = own_sorted ? take((size_t)P.npad * P.dp * 2) : 0,
+               oSlo = own_sorted ? take((size_t)P.npad * P.dp * 2) : 0,
+               oSn = own_sorted ? take((size_t)P.npad * 4) : 0, oSr = own_sorted ? take((size_t)P.npad * 4) : 0;
+  uint8_t *t = nullptr;
+  if (cudaMallocAsync((void **)&t, off, h->st) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KKM_ENOMEM, "kkm_predict: cannot allocate %zu temporary bytes", off);
+  }
+  int rc = [&]() -> int {
+    float *Yf = (float *)(t + oYf), *yn = (float *)(t + oYn), *yr = (float *)(t + oYr);
+    uint16_t *Yhi = (uint16_t *)(t + oYhi), *Ylo = (uint16_t *)(t + oYlo);
+    double *yd = (double *)(t + oYd), *Sp = (double *)(t + oSp), *Dy = D_out ? (double *)(t + oD) : nullptr;
+    int32_t *ylab = (int32_t *)(t + oLab);
+    SortedSet B{own_sorted ? (uint16_t *)(t + oShi) : h->Shi, own_sorted ? (uint16_t *)(t + oSlo) : h->Slo,
+                own_sorted ? (float *)(t + oSn) : h->snorms, own_sorted ? (float *)(t + oSr) : h->srscale,
+                (int32_t *)(t + oPerm), (int32_t *)(t + oPos), (int32_t *)(t + oSeg), (int32_t *)(t + oBc),
+                (int32_t *)(t + oBo)};
+    // a5 for the new points: split operands, norms, kappa(y, y)
+    CK(cudaMemsetAsync(Yf, 0, (size_t)mpad * P.ldf * 4, h->st));
+    CK(cudaMemcpy2DAsync(Yf, P.ldf * 4, Y, ldy * 4, P.d * 4, m, cudaMemcpyDefault, h->st));
+    prep_rows_kernel<<<(unsigned)ceil_div(mpad, 8), 256, 0, h->st>>>(Yf, P.ldf, m, mpad, P.d, yn, Yhi, Ylo, P.dp,
+                                                                     P.fp16 ? 2 : 1, yr);
+    CKL();
+    diag_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, h->st>>>(Yf, P.ldf, P.d, 0, m, h->p.kind, h->p.gamma,
+                                                              h->p.coef0, h->p.degree, yd);
+    CKL();
+    // B = all n training points sorted by their current labels; A = Y
+    CKR(sort_gather(h, h->lab[h->cur], 0, P.n, P.npad, B));
+    TcStream ts;
+    const StreamA A{Yhi, Ylo, yn, yr, mpad, 0, m, mpad};
+    CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, nsplit, Sp));
+    predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, nsplit, m, mpad, k, h->sizes[h->cur],
+                                                                  h->cnorm2, yd, ylab, Dy);
+    CKL();
+    CKR(copy_any(h, labels_out, ylab, (size_t)m * 4));
+    if (D_out) CKR(copy_any(h, D_out, Dy, (size_t)m * k * 8));
+    CK(cudaStreamSynchronize(h->st));
+    return KKM_OK;
+  }();
+  cudaFreeAsync(t, h->st);
+  if (rc == KKM_OK) CK(cudaStreamSynchronize(h->st));
+  return rc;
 }
 
 int kkm_debug_read(kkm_handle h, int32_t what, void *dst) {

@@ -4,17 +4,17 @@
 //
 // HBM-bound: every iteration streams the rank's K block (n_local x n fp32) once.
 // Design:
-//   * persistent CTAs, one per SM; a work item = 4 consecutive rows x one column
-//     split; warp 8 is a producer that streams 2048-column chunks of those 4 rows
-//     plus the matching labels into a 4-stage shared-memory ring with 1-D bulk
-//     copies (cp.async.bulk, the TMA engine) completing on mbarriers, so the HBM
-//     latency is covered by up to 160 KB in flight per SM without registers;
-//   * 8 consumer warps read the chunk from shared memory (conflict-free LDS.128)
-//     and reduce it into per-lane accumulators acc[row][cluster] with a one-hot
-//     mask: acc += K(i, j) * [cl(j) == c], two columns per FFMA2 (fma.rn.f32x2), so the
-//     cost per element is ~KP/2 FFMA2 + KP/R mask ops and no divergent indexing;
+//   * persistent CTAs, one per SM; a work item = R consecutive rows (8 for KP <= 10, else 4)
+//     x one column split; the last warp is a producer that streams 2048-column chunks of
+//     those rows plus the matching labels into a 3-stage (R = 8) / 5-stage (R = 4) shared-
+//     memory ring with 1-D bulk copies (cp.async.bulk, the TMA engine) completing on
+//     mbarriers, so ~200 KB per SM are in flight without registers;
+//   * 4 consumer warps read the chunk from shared memory (conflict-free LDS.128) and reduce
+//     it into per-lane accumulators acc[row][cluster] with a one-hot mask:
+//     acc += K(i, j) * [cl(j) == c], two columns per FFMA2 (fma.rn.f32x2), so the cost per
+//     element is ~KP/2 FFMA2 + KP/R mask ops and no divergent indexing;
 //   * fp32 within a lane (<= 512 columns per split), fixed-order shuffle tree across
-//     lanes, fp64 across the 8 warps in fixed order -> deterministic.
+//     lanes, fp64 across the consumer warps in fixed order -> deterministic.
 #pragma once
 #include "common.cuh"
 
@@ -22,7 +22,6 @@ namespace kkm {
 
 template <int KP>
 struct SpRows;
-constexpr int SP_CWARPS_MAX = 8;
 constexpr int SP_MAX_CHUNKS_PER_SPLIT = 128;  // bounds fp32 terms per lane (<= 512 per lane)
 constexpr int SP_KPMAX = 16;
 

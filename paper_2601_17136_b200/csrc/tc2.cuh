@@ -422,8 +422,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                       uint32_t idesc, int nkb, int64_t n, int64_t b0, int64_t nloc, int64_t rows_pad,
                       const float *__restrict__ norms, const float *__restrict__ rscale,
                       const float *__restrict__ snorms, const float *__restrict__ srscale,
-                      const int32_t *__restrict__ pos, const int32_t *__restrict__ seg_g, int k,
-                      KappaParams kp, T2StreamSched sc, double *__restrict__ Spart) {
+                      const int32_t *__restrict__ pos, int64_t npos, const int32_t *__restrict__ seg_g, int k,
+                      KappaParams kp, T2StreamSched sc, double *__restrict__ Spart, int kstride, int c0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *extra;
   const T2Smem s = t2_carve(smem_raw, (uint32_t)T2_STREAM_EXTRA, &extra);
@@ -432,7 +432,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cr = cluster_ctarank();
   const bool fp16 = rscale != nullptr;
-  for (int c = threadIdx.x; c <= k; c += blockDim.x) seg[c] = seg_g[c];
+  // B holds the clusters [c0, c0 + k) of the sorted operand, starting at sorted row seg_g[0]
+  const int32_t sbase = seg_g[0];
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) seg[c] = seg_g[c] - sbase;
   t2_setup(s, warp);  // (its cluster barrier also publishes seg)
   const uint32_t tmem_base = *s.tmem_slot;
 
@@ -457,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
       const float ni = row_ok ? norms[i] : 0.f;
       const float rsi = (fp16 && row_ok) ? rscale[i] : 1.f;
       const RowK rk = make_rowk(kp, rsi, ni);
-      const int64_t mypos = (row_ok && kp.kind == 2 && i >= b0 && i < b0 + n) ? pos[i - b0] : -1;
+      const int64_t mypos = (row_ok && kp.kind == 2 && pos && i >= b0 && i < b0 + npos) ? pos[i - b0] - sbase : -1;
       double acc[KMAX];
 #pragma unroll
       for (int c = 0; c < KMAX; ++c) acc[c] = 0.0;
@@ -511,12 +513,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
       }
       if (row_ok && tn1 > tn0) {
-        double *dst = Spart + ((int64_t)(2 * sp + half) * rows_pad + r) * k;
+        double *dst = Spart + ((int64_t)(2 * sp + half) * rows_pad + r) * kstride + c0;
 #pragma unroll
         for (int c = 0; c < KMAX; ++c)
           if (c < k) dst[c] = acc[c];
       } else if (row_ok) {
-        double *dst = Spart + ((int64_t)(2 * sp + half) * rows_pad + r) * k;
+        double *dst = Spart + ((int64_t)(2 * sp + half) * rows_pad + r) * kstride + c0;
         for (int c = 0; c < k; ++c) dst[c] = 0.0;
       }
     }
@@ -574,8 +576,8 @@ template <int KMAX>
 inline int t2s_launch_k(bool &attr, unsigned grid, cudaStream_t st, const TcStream &g, uint32_t idesc, int nkb,
                         int64_t n, int64_t b0, int64_t nloc, int64_t rows_pad, const float *norms,
                         const float *rscale, const float *snorms, const float *srscale, const int32_t *pos,
-                        const int32_t *seg, int k, const KappaParams &kp, const T2StreamSched &sc,
-                        double *Spart) {
+                        int64_t npos, const int32_t *seg, int k, const KappaParams &kp, const T2StreamSched &sc,
+                        double *Spart, int kstride, int c0) {
   if (!attr) {
     if (cudaFuncSetAttribute(tc2_stream_kernel<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)T2_STREAM_SMEM) != cudaSuccess) {
@@ -586,30 +588,38 @@ inline int t2s_launch_k(bool &attr, unsigned grid, cudaStream_t st, const TcStre
   }
   tc2_stream_kernel<KMAX><<<grid, T2_THREADS, T2_STREAM_SMEM, st>>>(g.a_hi, g.a_lo, g.b_hi, g.b_lo, idesc, nkb, n,
                                                                     b0, nloc, rows_pad, norms, rscale, snorms,
-                                                                    srscale, pos, seg, k, kp, sc, Spart);
+                                                                    srscale, pos, npos, seg, k, kp, sc, Spart,
+                                                                    kstride, c0);
   return 0;
 }
 
-// Streaming: same contract as tc_stream_launch (stream.cuh), on CTA pairs.
+// Streaming on CTA pairs. A: rows_a rows (Xhi/Xlo, norms, rscale), output rows [row0, row0 + nloc).
+// B: the label-sorted operand (Shi/Slo, snorms, srscale; rows_b rows from its base) holding the
+// clusters [c0, c0 + k) in n rows; seg = the cluster starts of those clusters (seg[0] = the
+// sorted row of B's base). pos (may be NULL): sorted position of A row i for b0 <= i < b0 + npos
+// (the Gaussian diagonal). Spart: [2 * nsplit][rows_pad][kstride], columns c0 .. c0 + k - 1.
 inline int tc2_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *Xlo, const uint16_t *Shi,
-                             const uint16_t *Slo, bool fp16, int64_t rows, int64_t dp, int64_t n, int64_t b0,
-                             int64_t row0, int64_t nloc, int64_t rows_pad, const float *norms,
+                             const uint16_t *Slo, bool fp16, int64_t rows_a, int64_t rows_b, int64_t dp, int64_t n,
+                             int64_t b0, int64_t row0, int64_t nloc, int64_t rows_pad, const float *norms,
                              const float *rscale, const float *snorms, const float *srscale, const int32_t *pos,
-                             const int32_t *seg, int k, const KappaParams &kp, int nsplit, double *Spart,
-                             cudaStream_t st, int64_t *launches) {
+                             int64_t npos, const int32_t *seg, int k, const KappaParams &kp, int nsplit,
+                             double *Spart, int kstride, int c0, cudaStream_t st, int64_t *launches) {
   if (!tc_encode_fn()) {
     TcGemm tmp;
-    if (tc_make_maps(tmp, Xhi, Xlo, fp16, rows, dp)) return 1;
+    if (tc_make_maps(tmp, Xhi, Xlo, fp16, rows_a, dp)) return 1;
   }
-  if (g.ahi != Xhi || g.alo != Xlo || g.bhi != Shi || g.blo != Slo || g.fp16 != fp16) {
-    if (ts_encode(&g.a_hi, Xhi, fp16, rows, dp) || ts_encode(&g.a_lo, Xlo, fp16, rows, dp) ||
-        ts_encode(&g.b_hi, Shi, fp16, rows, dp) || ts_encode(&g.b_lo, Slo, fp16, rows, dp))
+  if (g.ahi != Xhi || g.alo != Xlo || g.bhi != Shi || g.blo != Slo || g.fp16 != fp16 || g.arows != rows_a ||
+      g.brows != rows_b) {
+    if (ts_encode(&g.a_hi, Xhi, fp16, rows_a, dp) || ts_encode(&g.a_lo, Xlo, fp16, rows_a, dp) ||
+        ts_encode(&g.b_hi, Shi, fp16, rows_b, dp) || ts_encode(&g.b_lo, Slo, fp16, rows_b, dp))
       return 1;
     g.ahi = Xhi;
     g.alo = Xlo;
     g.bhi = Shi;
     g.blo = Slo;
     g.fp16 = fp16;
+    g.arows = rows_a;
+    g.brows = rows_b;
   }
   if (!g.num_sms) {
     int dev = 0;
@@ -633,15 +643,19 @@ inline int tc2_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
   static bool a4 = false, a8 = false, a16 = false;
   const float *rs = fp16 ? rscale : nullptr;
   int rc;
+  if (k > 16) {
+    tc_err_slot() = "tc2_stream_launch: at most 16 clusters per launch";
+    return 1;
+  }
   if (k <= 4)
-    rc = t2s_launch_k<4>(a4, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, seg,
-                         k, kp, sc, Spart);
+    rc = t2s_launch_k<4>(a4, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, npos,
+                         seg, k, kp, sc, Spart, kstride, c0);
   else if (k <= 8)
-    rc = t2s_launch_k<8>(a8, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, seg,
-                         k, kp, sc, Spart);
+    rc = t2s_launch_k<8>(a8, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, npos,
+                         seg, k, kp, sc, Spart, kstride, c0);
   else
     rc = t2s_launch_k<16>(a16, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos,
-                          seg, k, kp, sc, Spart);
+                          npos, seg, k, kp, sc, Spart, kstride, c0);
   if (rc) return rc;
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();

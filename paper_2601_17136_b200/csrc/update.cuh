@@ -119,4 +119,31 @@ __global__ void assign_kernel(const double *__restrict__ E, int64_t nrows, int k
     if (hist[c]) atomicAdd(&sizes_next[c], hist[c]);
 }
 
+// Out-of-sample assignment (kkm_predict): one thread per new point y.
+// E(y, c) = S(y, c) / |L_c| from the streaming partials, D(y, c) = K(y, y) - 2 E(y, c) + c(c)
+// (Eq. d), lowest-index argmin on -2E + c exactly as assign_kernel (A6, A7).
+__global__ void predict_kernel(const double *__restrict__ Spart, int nsplit, int64_t m, int64_t rows_pad, int k,
+                               const int32_t *__restrict__ sizes, const double *__restrict__ cnorm,
+                               const double *__restrict__ diag, int32_t *__restrict__ labels,
+                               double *__restrict__ Dfull) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int best = 0;
+  double bd = __longlong_as_double(0x7ff0000000000000LL);
+  for (int c = 0; c < k; ++c) {
+    double s = 0.0;
+    for (int p = 0; p < nsplit; ++p) s += Spart[((int64_t)p * rows_pad + i) * k + c];
+    const int32_t sz = sizes[c];
+    const double e = sz > 0 ? s / (double)sz : 0.0;
+    const double cn = cnorm[c];
+    const double dsh = isinf(cn) ? cn : fma(-2.0, e, cn);
+    if (Dfull) Dfull[i * k + c] = diag[i] + dsh;
+    if (dsh < bd) {
+      bd = dsh;
+      best = c;
+    }
+  }
+  labels[i] = best;
+}
+
 }  // namespace kkm

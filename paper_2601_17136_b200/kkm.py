@@ -60,6 +60,7 @@ def lib():
             "kkm_assign": [P, P],
             "kkm_objective": [P, P],
             "kkm_set_labels": [P, P],
+            "kkm_predict": [P, P, i64, i64, P, P],
             "kkm_debug_read": [P, i32, P],
             "kkm_kernel_tile": [P, i64, i64, i32, i32, P],
             "kkm_phase_ms": [P, P],
@@ -191,6 +192,30 @@ class KernelKMeans:
         if isinstance(labels, np.ndarray):
             labels = np.ascontiguousarray(labels, dtype=np.int32)
         _check(lib().kkm_set_labels(self.h, _ptr(labels)))
+
+    def predict(self, Y, return_distances: bool = False):
+        """Out-of-sample assignment of the rows of Y (host numpy or device tensor, m x d fp32)
+        to the clusters of the current labels (kkm_predict). Returns int32 labels (numpy for
+        numpy input, else a tensor on the handle's device), plus the m x k fp64 distances."""
+        on_host = isinstance(Y, np.ndarray)
+        if on_host:
+            Y = np.ascontiguousarray(Y, dtype=np.float32)
+            m, ldy = Y.shape[0], (Y.shape[1] if Y.ndim == 2 else 0)
+        else:
+            if Y.dtype != self.torch.float32 or Y.stride(-1) != 1:
+                raise ValueError("Y must be fp32 with unit column stride")
+            m, ldy = Y.shape[0], Y.stride(0)
+        if Y.ndim != 2 or Y.shape[1] != self.d:
+            raise ValueError(f"Y must be m x {self.d}")
+        if on_host:
+            lab = np.empty(m, dtype=np.int32)
+            D = np.empty((m, self.k), dtype=np.float64) if return_distances else None
+        else:
+            lab = self.torch.empty(m, dtype=self.torch.int32, device=self.device)
+            D = (self.torch.empty((m, self.k), dtype=self.torch.float64, device=self.device)
+                 if return_distances else None)
+        _check(lib().kkm_predict(self.h, _ptr(Y), m, ldy, _ptr(lab), _ptr(D)))
+        return (lab, D) if return_distances else lab
 
     def debug_read(self, what: int) -> np.ndarray:
         shapes = {DBG_E: ((self.n_local, self.k), np.float64), DBG_CNORM: ((self.k,), np.float64),

@@ -67,9 +67,8 @@ def test_workspace_size_and_errors():
     with pytest.raises(kkm.KKMError, match="EUNSUP"):
         kkm.workspace_size(q, 100, 4)  # streaming needs a tensor-core precision
     q = kkm.default_params()
-    q.k, q.path = 17, kkm.PATH_STREAM
-    with pytest.raises(kkm.KKMError, match="EUNSUP"):
-        kkm.workspace_size(q, 100, 4)  # streaming supports k <= 16
+    q.k, q.path = 70, kkm.PATH_STREAM  # k > 16 streams in groups of 16 clusters
+    assert kkm.workspace_size(q, 100, 4) > 0
     q = kkm.default_params()
     q.k = 10
     nb_stream = kkm.workspace_size(q, 1_000_000, 784)  # 4 TB of K: AUTO streams

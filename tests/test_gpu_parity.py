@@ -84,16 +84,14 @@ def test_har_like_gaussian_teacher_forced(precision):
 
 @pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
 def test_many_clusters_multipass(precision):
-    """k = 21 > 16: the label-sorted-group SpMM (v2); linear kernel."""
-    if precision[1] == kkm.PATH_STREAM:
-        pytest.skip("the streaming path supports k <= 16 (KKM_EUNSUP, tested in test_abi)")
+    """k = 21 > 16: the label-sorted-group SpMM (v2); streaming: 2 launches of <= 16 clusters."""
     X = synth.blobs(1500, 16, 21, seed=3, sep=4.0)
     teacher_forced(X, 21, oracle.LINEAR, iters=3, precision=precision)
 
 
-@pytest.mark.parametrize("precision", PRECISIONS[:2], ids=PREC_IDS[:2])
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
 def test_very_many_clusters(precision):
-    """k = 70 > 64: the one-hot SpMM in ceil(k/16) passes (materialised only)."""
+    """k = 70 > 64: the one-hot SpMM in ceil(k/16) passes; streaming: 5 cluster-group launches."""
     X = synth.blobs(600, 8, 70, seed=6, sep=3.0)
     teacher_forced(X, 70, oracle.POLY, 0.2, 1.0, 2, iters=2, precision=precision)
 
@@ -102,10 +100,7 @@ def test_very_many_clusters(precision):
 def test_edge_k1_kn_and_tiny(precision):
     X = synth.blobs(37, 3, 2, seed=5)
     teacher_forced(X, 1, oracle.POLY, 0.5, 1.0, 3, iters=2, precision=precision)
-    if precision[1] != kkm.PATH_STREAM:  # k = 37 > 16
-        teacher_forced(X, 37, oracle.GAUSSIAN, 0.3, iters=2, precision=precision)
-    else:
-        teacher_forced(X[:11], 11, oracle.GAUSSIAN, 0.3, iters=2, precision=precision)
+    teacher_forced(X, 37, oracle.GAUSSIAN, 0.3, iters=2, precision=precision)  # k = n singletons
     teacher_forced(X[:2], 2, oracle.LINEAR, iters=2, precision=precision)
 
 

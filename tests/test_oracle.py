@@ -308,3 +308,48 @@ def test_thread_count_independence(monkeypatch):
                                     env=dict(os.environ, OMP_NUM_THREADS=str(t))).strip()
             for t in (1, 3)}
     assert len(outs) == 1
+
+
+# ---------------------------------------------------------------- f4: out-of-sample assignment
+def test_predict_on_training_points_equals_assign():
+    """Predicting the training points reproduces the iteration's distances (Eq. d) exactly."""
+    X = synth.blobs(80, 4, 3, seed=31, sep=3.0)
+    K = oracle.kernel_matrix(X, oracle.POLY, 0.5, 1.0, 2)
+    diag = np.diag(K).copy()
+    lab = oracle.round_robin(80, 3)
+    it = oracle.iteration(K, diag, lab, 3)
+    nl, D = oracle.predict(X, lab, 3, it["cnorm"], X, oracle.POLY, 0.5, 1.0, 2)
+    assert np.array_equal(nl, it["new_labels"])
+    assert np.allclose(D, it["Dfull"], rtol=1e-12, atol=1e-9)
+
+
+def test_predict_linear_is_nearest_centroid():
+    """Linear kernel: D(y, c) = ||y - mu_c||^2 with explicit centroids (textbook)."""
+    X = synth.blobs(120, 5, 4, seed=32, sep=4.0)
+    Y = synth.blobs(50, 5, 4, seed=33, sep=4.0)
+    lab = (np.arange(120) * 7) % 4
+    K = oracle.kernel_matrix(X, oracle.LINEAR)
+    cn = oracle.cnorm(oracle.E_rows(K, lab, 4), lab, 4)
+    nl, D = oracle.predict(X, lab, 4, cn, Y, oracle.LINEAR)
+    mu = np.stack([X[lab == c].astype(np.float64).mean(axis=0) for c in range(4)])
+    ref = ((Y.astype(np.float64)[:, None, :] - mu[None]) ** 2).sum(axis=2)
+    assert np.allclose(D, ref, rtol=1e-10, atol=1e-9)
+    assert np.array_equal(nl, ref.argmin(axis=1))
+
+
+def test_predict_empty_cluster_and_gaussian():
+    X = synth.rings(60, seed=8)
+    lab = np.zeros(60, dtype=np.int32)
+    lab[30:] = 2  # cluster 1 empty
+    K = oracle.kernel_matrix(X, oracle.GAUSSIAN, 0.7)
+    cn = oracle.cnorm(oracle.E_rows(K, lab, 3), lab, 3)
+    Y = synth.rings(20, seed=9)
+    nl, D = oracle.predict(X, lab, 3, cn, Y, oracle.GAUSSIAN, 0.7)
+    assert not (nl == 1).any() and np.isinf(D[:, 1]).all()
+    # Gaussian: D(y, c) = 1 - 2 mean_j K(y, x_j) + (1/|L|^2) sum K  (closed form via scipy cdist)
+    from scipy.spatial.distance import cdist
+    Ky = np.exp(-0.7 * cdist(Y.astype(np.float64), X.astype(np.float64), "sqeuclidean"))
+    for c in (0, 2):
+        m = lab == c
+        ref = 1.0 - 2.0 * Ky[:, m].mean(axis=1) + K[np.ix_(m, m)].sum() / m.sum() ** 2
+        assert np.allclose(D[:, c], ref, rtol=0, atol=1e-12)
