@@ -39,7 +39,8 @@ METRIC = "sec/iteration"
 
 def workload_desc(cfg, iters):
     return (f"{WORKLOAD}: MNIST-shaped synthetic n={cfg['n']} d=784 k={cfg['k']} "
-            f"poly(gamma=1,c=1,deg=2), K materialised, {iters} iterations (BASELINE.json configs[1])")
+            f"poly(gamma=1,c=1,deg=2), K materialised (upper-triangle bands unless --symmetric off), "
+            f"{iters} iterations (BASELINE.json configs[1])")
 
 
 def measured_peaks():
@@ -48,6 +49,22 @@ def measured_peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def sym_band_share(n, world, rank, TB=1024):
+    """f1 band storage (csrc/sym.cuh, make_plan): bands of TB rows x ceil32(n - I TB) columns,
+    largest first to the least-loaded rank. Returns (stored floats, useful flops / d / 2) of
+    `rank` = its K bytes / 4 and GEMM products."""
+    load = [0.0] * world
+    mine = 0
+    for I in range(-(-n // TB)):
+        rows = min(TB, n - I * TB)
+        ldb = -(-(n - I * TB) // 32) * 32
+        r = min(range(world), key=lambda q: (load[q], q))
+        load[r] += rows * ldb
+        if r == rank:
+            mine += rows * ldb
+    return mine
 
 
 def cores():
@@ -187,9 +204,11 @@ def run_ours(args):
     precision = {"bf16x3": kkm.PREC_BF16X3, "fp16x3": kkm.PREC_FP16X3,
                  "fp32": kkm.PREC_FP32_SIMT}[args.precision]
     kw = dict(kind=cfg["kind"], gamma=1.0, coef0=1.0, degree=2, max_iter=iters,
-              precision=precision, rank=rank, nranks=world, comm=comm, timing=True)
+              precision=precision, rank=rank, nranks=world, comm=comm, timing=True,
+              symmetric=kkm.SYM_AUTO if args.symmetric == "auto" else kkm.SYM_OFF)
     p = kkm.default_params()
     p.kind, p.k, p.max_iter, p.precision = cfg["kind"], k, iters, precision
+    p.symmetric = kw["symmetric"]
     ws = torch.empty(kkm.workspace_size(p, n, d, rank, world), dtype=torch.uint8, device=dev)
     Xd = torch.from_numpy(X_local).to(dev)
     Xh = torch.from_numpy(X_local).pin_memory()
@@ -255,17 +274,25 @@ def run_ours(args):
         B = -(-n // world)
         nloc = min(B, n - 0)
         ldk = -(-n // 32) * 32
-        spmm_bytes = nloc * ldk * 4 + ldk * 4 + nloc * k * 8  # K block + labels + S partials
+        sym = args.symmetric == "auto" and k <= 16
+        if sym:  # f1: the rank's upper-triangle bands (K read once; the column partials are
+            # implementation traffic, visible in `traffic`) + S partials of all rows
+            kfl = sym_band_share(n, world, 0)
+            spmm_bytes = kfl * 4 + n * k * 8
+            gemm_flops = 2.0 * kfl * d
+        else:
+            spmm_bytes = nloc * ldk * 4 + ldk * 4 + nloc * k * 8  # K block + labels + S partials
+            gemm_flops = 2.0 * nloc * n * d
         spmm_gbs = spmm_bytes / (spmm_ms * 1e-3) / 1e9
-        gemm_flops = 2.0 * nloc * n * d
         gemm_tfs = gemm_flops / (gemm_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "spmm_traffic.json")
-        if os.path.exists(tp):  # only a capture of this same launch shape (per-launch bytes)
+        if os.path.exists(tp):  # only an ncu capture of this same launch shape (per-launch bytes)
             with open(tp) as f:
-                cap = json.load(f)
-            if abs(cap.get("algorithmic_bytes", 0) - spmm_bytes) <= 0.01 * spmm_bytes:
-                traffic = cap.get("bytes_per_launch")
+                caps = json.load(f).get("captures", [])
+            for cap in caps:
+                if abs(cap.get("algorithmic_bytes", 0) - spmm_bytes) <= 0.01 * spmm_bytes:
+                    traffic = cap.get("bytes_per_launch")
         tensor = precision in (kkm.PREC_BF16X3, kkm.PREC_FP16X3)
         # 3 dense 16-bit MMAs per useful product: useful-flop peak = measured bf16 dense / 3
         # (fp16 and bf16 share the dense rate); SIMT: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz
@@ -280,7 +307,10 @@ def run_ours(args):
                        "iterations": iters, "precision_a1": args.precision,
                        "parallelism": f"1D row shards x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (14.4/N GB of K streamed per iteration)"},
-            "roofline": {"kernel": "spmm_onehot (a2)", "bound": "hbm", "achieved": spmm_gbs,
+            "roofline": {"kernel": "a2 phase: band_sort + spmm_sym + sym_colsum + sym_reduce (f1 bands; "
+                                   "spmm_sym is ~86 % of it, profiles/r01_launches_sym_config2.txt)"
+                                   if sym else "spmm_onehot (a2)",
+                         "bound": "hbm", "achieved": spmm_gbs,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": spmm_gbs / peaks["hbm_gbs"],
                          "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_launch": spmm_bytes, "launch_ms": spmm_ms},
@@ -323,6 +353,8 @@ def main():
     ap.add_argument("--iters", type=int, default=0, help="override iterations per step")
     ap.add_argument("--precision", choices=["fp16x3", "bf16x3", "fp32"], default="fp16x3")
     ap.add_argument("--ref-rows", type=int, default=1024)
+    ap.add_argument("--symmetric", choices=["auto", "off"], default="auto",
+                    help="auto: upper-triangle K bands (f1); off: full K rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

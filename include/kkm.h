@@ -65,6 +65,11 @@ extern "C" {
                                   Needs FP16X3/BF16X3 (else KKM_EUNSUP). k > 16: one launch
                                   per group of 16 clusters (host reads k+1 ints per iter.) */
 
+/* ---- symmetric storage of a materialised K (f1) ---------------------------- */
+#define KKM_SYM_AUTO 0
+#define KKM_SYM_OFF 1
+#define KKM_SYM_ON 2
+
 /* ---- precision of the a1 contraction (reading A9) ----------------------- */
 #define KKM_PREC_BF16X3 0    /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi, bf16 split of x;
                                  product error ~2^-17 |x||y|                               */
@@ -102,7 +107,14 @@ typedef struct kkm_params {
   int32_t grid_rows;       /* 1.5D process grid pr x (nranks/pr), column-major ranks
                               (P:604); 0 or 1 = the 1D algorithm (Alg. 1). Must divide
                               nranks. See kkm_init.                                   */
-  int32_t reserved[5];     /* must be zero                                         */
+  int32_t symmetric;       /* f1, 1D runs with k <= 16 only: compute / store only the upper
+                              triangle of K (half the K bytes and GEMM flops when
+                              materialised, half the MMA work when streaming).
+                              KKM_SYM_AUTO (0): streaming always; materialised when
+                              n >= 8192 (below, the extra kernels cost more than the
+                              halved K read saves). KKM_SYM_ON (2): whenever eligible.
+                              KKM_SYM_OFF (1): never.                                 */
+  int32_t reserved[4];     /* must be zero                                         */
 } kkm_params;
 
 typedef struct kkm_ctx *kkm_handle;
@@ -118,8 +130,10 @@ int kkm_default_params(kkm_params *p);
 int64_t kkm_shard_begin(int64_t n, int32_t rank, int32_t nranks);
 
 /* Bytes of device workspace kkm_init needs for this rank (pure; no CUDA).
- * Includes the materialised K block (n_local x ceil32(n) fp32) when the
- * effective path is MATERIALIZE. */
+ * Includes the materialised K block when the effective path is MATERIALIZE: the
+ * rank's n_local x ceil32(n) fp32 rows, or with symmetric storage (KKM_SYM_AUTO, 1D,
+ * k <= 16) its share of the upper-triangle bands (1024 rows x ceil32(n - 1024 I)
+ * columns each, bands spread over the ranks by area): ~n^2/(2P) floats. */
 int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks,
                        size_t *bytes);
 
@@ -178,13 +192,21 @@ int kkm_set_labels(kkm_handle h, const int32_t *labels);
  *   Y:          host or device, m x d fp32 row-major, row pitch ldy >= d floats.
  *   labels_out: host or device, m int32 (out).
  *   D_out:      host or device, m x k fp64 (out), or NULL. +inf for empty clusters.
+ *   workspace:  device scratch of >= kkm_predict_workspace_size(h, m) bytes, 256-B
+ *               aligned, owned by the caller; or NULL: the library then takes it from
+ *               the stream-ordered allocator for this call (slower: the pages are
+ *               mapped on every call; KKM_ENOMEM if that fails).
  * Local to the calling rank (every rank holds all of X and the labels). Needs
  * c of the current labels: valid after kkm_fit or kkm_objective; otherwise one
  * kkm_objective pass is run first when nranks == 1 and KKM_ESTATE is returned
  * when nranks > 1 (that pass is collective). KKM_EUNSUP for FP32_SIMT handles.
- * Temporary device memory (~m*(6d + 8k*splits) + n*(4d) bytes) comes from the
- * stream-ordered allocator (KKM_ENOMEM if it fails). Synchronises the stream. */
-int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *labels_out, double *D_out);
+ * Synchronises the stream. */
+int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *labels_out, double *D_out,
+                void *workspace, size_t ws_bytes);
+
+/* Bytes of device scratch kkm_predict needs for m points (about m*(4*ld + 4*dp + 8*k*splits)
+ * + n*4*dp for materialising handles; ld = d rounded up to 4, dp = d rounded up to 64). */
+int kkm_predict_workspace_size(kkm_handle h, int64_t m, size_t *bytes);
 
 /* Copies an internal array of the last iteration (selectors KKM_DBG_*) to dst
  * (host or device). Synchronises. Test hook. */

@@ -21,6 +21,7 @@
 #include "sort.cuh"
 #include "spmm.cuh"
 #include "stream.cuh"
+#include "sym.cuh"
 #include "tc2.cuh"
 #include "update.cuh"
 
@@ -56,11 +57,20 @@ struct Plan {
   bool spmm_v2;                 // materialised a2 with label-sorted 32-column groups (k <= 64)
   int nsplit, chunks_per_split, nfin, nspmm_pass;
   int64_t rows_per_block;
+  int64_t s_rows_pad;  // row pitch of the S (or S partials) finalize reads
+  // f1 symmetric storage (sym.cuh): bands of SYM_TB rows, the rank's share spread by area
+  bool sym;
+  int T, sym_gmax;
+  int64_t sym_items;
+  std::vector<SymBand> bands;       // owned bands, ascending I
+  std::vector<int32_t> band_desc;   // band -> index into bands, or -1
+  bool ssym;                        // f1 on the streaming path (tc2_stream_sym_kernel)
+  std::vector<int4> units;          // its work units on this rank
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, total;
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -78,8 +88,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT &&
       p->precision != KKM_PREC_FP16X3)
     return fail(KKM_EINVAL, "unknown precision %d", p->precision);
-  for (int i = 0; i < 5; ++i)
+  for (int i = 0; i < 4; ++i)
     if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
+  if (p->symmetric != KKM_SYM_AUTO && p->symmetric != KKM_SYM_OFF && p->symmetric != KKM_SYM_ON)
+    return fail(KKM_EINVAL, "unknown symmetric mode %d", p->symmetric);
   const int pr = p->grid_rows <= 1 ? 1 : p->grid_rows;
   if (nranks % pr) return fail(KKM_EUNSUP, "grid_rows=%d does not divide nranks=%d", pr, nranks);
   Plan &P = *pl;
@@ -108,7 +120,46 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.lablen = round_up(std::max(P.npad, round_up(n, 32)), 32);
   P.tc = p->precision == KKM_PREC_BF16X3 || p->precision == KKM_PREC_FP16X3;
   P.fp16 = p->precision == KKM_PREC_FP16X3;
-  const double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
+  // f1: symmetric band storage (1D, k <= 16). Bands go to ranks largest first, each to the
+  // least-loaded rank (lowest rank on ties): deterministic, area-balanced.
+  const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= SP_KPMAX;
+  const bool sym_ok = sym_elig && (p->symmetric == KKM_SYM_ON || n >= 8 * SYM_TB);
+  double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
+  P.T = (int)ceil_div(n, SYM_TB);
+  P.sym_gmax = sym_gmax(P.k);
+  P.bands.clear();
+  P.band_desc.assign(P.T, -1);
+  P.sym_items = 0;
+  if (sym_ok) {
+    std::vector<double> load(nranks, 0.0);
+    int64_t koff = 0, cpoff = 0, csoff = 0;
+    for (int I = 0; I < P.T; ++I) {
+      const int64_t rows = std::min<int64_t>(SYM_TB, n - (int64_t)I * SYM_TB);
+      const int64_t ldb = round_up(n - (int64_t)I * SYM_TB, 32);
+      int owner = 0;
+      for (int r = 1; r < nranks; ++r)
+        if (load[r] < load[owner]) owner = r;
+      load[owner] += (double)rows * (double)ldb;
+      if (owner != rank) continue;
+      SymBand b;
+      b.band = I;
+      b.ldb = (int32_t)ldb;
+      b.koff = koff;
+      b.cpoff = cpoff;
+      b.csoff = csoff;
+      const int64_t chunks = ceil_div(ldb, 2048);  // spmm_sym chunk width (SpRows::CH)
+      b.nsplit = (int32_t)ceil_div(chunks, SP_MAX_CHUNKS_PER_SPLIT * 1024 / 2048);
+      b.cps = (int32_t)ceil_div(chunks, b.nsplit);
+      b.item0 = P.sym_items;
+      P.sym_items += (int64_t)P.sym_gmax * b.nsplit;
+      koff += rows * ldb;
+      cpoff += (int64_t)P.sym_gmax * std::max<int64_t>(0, ldb - SYM_TB);
+      csoff += (int64_t)P.k * std::max<int64_t>(0, ldb - SYM_TB);
+      P.band_desc[I] = (int32_t)P.bands.size();
+      P.bands.push_back(b);
+    }
+    kbytes = (double)koff * 4.0;
+  }
   if (p->path == KKM_PATH_MATERIALIZE) {
     P.materialize = true;
   } else if (p->path == KKM_PATH_STREAM) {
@@ -154,6 +205,51 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.nsplit = 2 * (int)std::max<int64_t>(s_l2, s_bal);
     P.chunks_per_split = 0;
   }
+  P.sym = P.materialize && sym_ok;
+  // f1 on the streaming path: upper-triangle pair tiles of the label-sorted K, work units
+  // (row tile, first column tile, count) of <= 512 tiles, spread over the ranks largest first
+  P.ssym = !P.materialize && sym_elig && P.tc;
+  P.units.clear();
+  if (P.ssym) {
+    const int64_t Tt = ceil_div(n, 256);
+    std::vector<int4> all;
+    // enough units for the 74 CTA pairs of every rank: split rows into pieces of <= cap tiles
+    const int64_t tri = Tt * (Tt + 1) / 2;
+    int64_t cap = std::max<int64_t>(1, std::min<int64_t>(512, tri / (4 * 74 * (int64_t)nranks)));
+    for (int64_t tm = 0; tm < Tt; ++tm) {
+      const int64_t len = Tt - tm, np = ceil_div(len, cap);
+      for (int64_t q = 0; q < np; ++q) {
+        const int64_t a = tm + q * len / np, b = tm + (q + 1) * len / np;
+        all.push_back(make_int4((int)tm, (int)a, (int)(b - a), 0));
+      }
+    }
+    std::vector<int64_t> load(nranks, 0);
+    std::vector<int> order(all.size());
+    for (size_t i = 0; i < all.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return all[x].z > all[y].z; });
+    std::vector<char> mine(all.size(), 0);
+    for (int i : order) {
+      int r = 0;
+      for (int q = 1; q < nranks; ++q)
+        if (load[q] < load[r]) r = q;
+      load[r] += all[i].z;
+      if (r == rank) mine[i] = 1;
+    }
+    for (size_t i = 0; i < all.size(); ++i)  // tile-major order on the rank (A reuse in L2)
+      if (mine[i]) P.units.push_back(all[i]);
+    P.nsplit = 1;
+  }
+  if (P.sym) {  // S partials over all rows (owned bands lie anywhere)
+    P.nApad = P.npad;
+    P.nsplit = 1;
+    for (const SymBand &b : P.bands) P.nsplit = std::max(P.nsplit, (int)b.nsplit);
+    P.chunks_per_split = 0;
+  } else {
+    P.bands.clear();
+    P.band_desc.clear();
+  }
+  if (P.ssym) P.nApad = P.npad;
+  P.s_rows_pad = (P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1)) ? P.B : P.nApad;
   P.sort_blocks = (int)ceil_div(std::max<int64_t>(P.nB, 1), SORT_BLOCK);
   P.nspmm_pass = (int)ceil_div(P.k, SP_KPMAX);
   P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.nloc, 1), FIN_THREADS));
@@ -171,7 +267,17 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.o_rscale = take((size_t)P.npad * 4);
   P.o_norms = take((size_t)P.npad * 4);
   P.o_diag = take((size_t)P.B * 8);
-  P.o_K = P.materialize ? take((size_t)P.nApad * P.ldk * 4) : 0;
+  size_t kfloats = (size_t)P.nApad * P.ldk;
+  size_t cpfloats = 0, csdoubles = 0;
+  if (P.sym) {
+    kfloats = 0;
+    for (const SymBand &b : P.bands) {
+      kfloats += (size_t)std::min<int64_t>(SYM_TB, n - (int64_t)b.band * SYM_TB) * b.ldb;
+      cpfloats += (size_t)P.sym_gmax * std::max<int64_t>(0, b.ldb - SYM_TB);
+      csdoubles += (size_t)P.k * std::max<int64_t>(0, b.ldb - SYM_TB);
+    }
+  }
+  P.o_K = P.materialize ? take(std::max<size_t>(kfloats, 1) * 4) : 0;
   P.o_lab[0] = take((size_t)P.lablen * 4);
   P.o_lab[1] = take((size_t)P.lablen * 4);
   P.o_sizes[0] = take((size_t)P.k * 4);
@@ -202,7 +308,25 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (P.pr > 1) {
     P.o_labB = take((size_t)P.ldk * 4);
     P.o_Scol = take((size_t)P.nApad * P.k * 8);
-    P.o_Smine = take((size_t)P.B * P.k * 8);
+  }
+  if (P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1)) P.o_Smine = take((size_t)P.B * P.k * 8);
+  if (P.ssym) {
+    P.o_units = take(std::max<size_t>(P.units.size(), 1) * sizeof(int4));
+    P.o_Sfix = take((size_t)P.npad * P.k * 8);
+    P.o_Sorig = P.nranks > 1 ? take((size_t)P.npad * P.k * 8) : 0;
+    P.o_Sfmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
+    P.o_fxmax = take(16);
+  }
+  if (P.sym) {
+    P.o_perm_b = take((size_t)P.T * SYM_TB * 4);
+    P.o_groups = take((size_t)P.T * P.sym_gmax * sizeof(SymGroup));
+    P.o_ngroups = take((size_t)P.T * 4);
+    P.o_bands = take(std::max<size_t>(P.bands.size(), 1) * sizeof(SymBand));
+    P.o_band_desc = take((size_t)P.T * 4);
+    P.o_colpart = take(std::max<size_t>(cpfloats, 1) * 4);
+    P.o_colsum = take(std::max<size_t>(csdoubles, 1) * 8);
+    P.o_gfirst = take((size_t)P.T * (P.k + 1) * 4);
+    P.o_Sfin = take((size_t)P.npad * P.k * 8);
   }
   P.total = off;
   return KKM_OK;
@@ -226,11 +350,22 @@ struct kkm_ctx {
   uint16_t *Shi = nullptr, *Slo = nullptr;
   float *snorms = nullptr, *srscale = nullptr;
   int32_t *perm = nullptr, *pos = nullptr, *seg = nullptr, *bcount = nullptr, *boff = nullptr;
-  TcStream ts;
+  TcStream ts, ts_predict;  // tensor maps of the clustering loop / of kkm_predict
   // 1.5D: padded labels of the B set, column-block partials, own-block sums; column comm
   int32_t *labB = nullptr;
   double *Scol = nullptr, *Smine = nullptr;
   uint32_t *codes = nullptr;  // SpMM v2 per-iteration group codes
+  // f1 symmetric storage
+  int32_t *perm_b = nullptr, *ngroups = nullptr, *band_desc = nullptr, *gfirst = nullptr;
+  SymGroup *groups = nullptr;
+  SymBand *bands = nullptr;
+  float *colpart = nullptr;
+  double *colsum = nullptr, *Sfin = nullptr;
+  // f1 streaming: units, int64 fixed-point S (sorted order), its original-order copy
+  int4 *units = nullptr;
+  long long *Sfix = nullptr, *Sorig = nullptr, *Sfmine = nullptr;
+  float *fxmax = nullptr;
+  double fx_scale = 1.0, fx_inv = 1.0;
   ncclComm_t colcomm = nullptr;
   int32_t *lab[2], *sizes[2];
   unsigned long long *changed;
@@ -425,10 +560,109 @@ int launch_spmm_mat(kkm_ctx *h, const int32_t *labels) {
   }
 }
 
+template <int KP>
+int launch_spmm_sym_kp(kkm_ctx *h, const int32_t *labels) {
+  const Plan &P = h->P;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(spmm_sym_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)spmm_sym_smem_bytes()));
+    attr_set = true;
+  }
+  if (P.sym_items == 0) return KKM_OK;
+  const int grid = (int)std::min<int64_t>(P.sym_items, h->num_sms);
+  spmm_sym_kernel<KP><<<grid, SYM_THREADS, spmm_sym_smem_bytes(), h->st>>>(
+      h->K, h->bands, (int)P.bands.size(), P.sym_items, labels, h->perm_b, h->groups, P.sym_gmax, P.k, P.nApad,
+      h->Spart, h->colpart);
+  CKL();
+  return KKM_OK;
+}
+
+// f1: a2 over the symmetric band storage -> the rank's contributions to S of all rows (Sfin),
+// reduce-scattered over the ranks for P > 1 (each rank then holds S of its own 1D block).
+int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
+  const Plan &P = h->P;
+  const int k = P.k;
+  band_sort_kernel<<<P.T, SYM_TB, (size_t)(32 * k + 2 * (k + 1)) * 4, h->st>>>(
+      labels, P.n, k, sym_rows(k), P.sym_gmax, h->perm_b, h->groups, h->ngroups, h->gfirst);
+  CKL();
+  int rc;
+  switch ((k + 1) / 2 * 2) {
+    case 2: rc = launch_spmm_sym_kp<2>(h, labels); break;
+    case 4: rc = launch_spmm_sym_kp<4>(h, labels); break;
+    case 6: rc = launch_spmm_sym_kp<6>(h, labels); break;
+    case 8: rc = launch_spmm_sym_kp<8>(h, labels); break;
+    case 10: rc = launch_spmm_sym_kp<10>(h, labels); break;
+    case 12: rc = launch_spmm_sym_kp<12>(h, labels); break;
+    case 14: rc = launch_spmm_sym_kp<14>(h, labels); break;
+    default: rc = launch_spmm_sym_kp<16>(h, labels); break;
+  }
+  CKR(rc);
+  int64_t wmax = 0;
+  for (const SymBand &b : P.bands) wmax = std::max<int64_t>(wmax, b.ldb - SYM_TB);
+  if (wmax > 0 && !P.bands.empty()) {
+    sym_colsum_kernel<<<dim3((unsigned)ceil_div(wmax, 4 * 128), (unsigned)P.bands.size(), (unsigned)k), 128, 0,
+                        h->st>>>(
+        h->colpart, h->bands, h->gfirst, k, h->colsum);
+    CKL();
+  }
+  sym_reduce_kernel<<<dim3((unsigned)ceil_div(P.npad, 256), (unsigned)k), 256, 0, h->st>>>(
+      h->Spart, h->colsum, h->bands, h->band_desc, P.n, P.npad, k, h->Sfin);
+  CKL();
+  if (P.nranks == 1) {
+    *s_out = h->Sfin;
+    return KKM_OK;
+  }
+  CKN(ncclReduceScatter(h->Sfin, h->Smine, (size_t)P.B * k, ncclDouble, ncclSum, h->comm, h->st));
+  *s_out = h->Smine;
+  return KKM_OK;
+}
+
+// f1 streaming a1+a2: sort all points by label, the upper-triangle kernel accumulates S of
+// the sorted points in int64 fixed point; back to original order (exact), reduce-scattered
+// in int64 for P > 1 (exact: any reduction order gives the same bits), then fp64.
+int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
+  const Plan &P = h->P;
+  const int k = P.k;
+  const SortedSet B{h->Shi, h->Slo, h->snorms, h->srscale, h->perm, h->pos, h->seg, h->bcount, h->boff};
+  CKR(sort_gather(h, labels, 0, P.n, P.npad, B));
+  CK(cudaMemsetAsync(h->Sfix, 0, (size_t)P.npad * k * 8, h->st));
+  int rc = tc2_stream_sym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg,
+                                 k, h->kp, h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st,
+                                 &h->launches);
+  if (rc) {
+    h->poisoned = true;
+    return fail(KKM_ECUDA, "symmetric streaming kernel launch failed: %s", tc_gemm_error());
+  }
+  const unsigned g = (unsigned)ceil_div(P.npad * k, 256);
+  double *Sd = h->Spart;  // P.nsplit = 1: [npad][k] fp64
+  if (P.nranks == 1) {
+    fx_unpermute_kernel<<<g, 256, 0, h->st>>>(h->Sfix, h->pos, P.n, P.npad, k, h->fx_inv, nullptr, Sd);
+    CKL();
+    *s_out = Sd;
+    return KKM_OK;
+  }
+  fx_unpermute_kernel<<<g, 256, 0, h->st>>>(h->Sfix, h->pos, P.n, P.npad, k, h->fx_inv, h->Sorig, nullptr);
+  CKL();
+  CKN(ncclReduceScatter(h->Sorig, h->Sfmine, (size_t)P.B * k, ncclInt64, ncclSum, h->comm, h->st));
+  fx_to_double_kernel<<<(unsigned)ceil_div(P.B * k, 256), 256, 0, h->st>>>(h->Sfmine, P.B * k, h->fx_inv, h->Smine);
+  CKL();
+  *s_out = h->Smine;
+  return KKM_OK;
+}
+
 // a2 + the 1.5D column-split reduce-scatter: afterwards the S partials of this rank's own 1D
 // block are in s_out[nsplit_out][B][k] (the 1D case reduces nothing: s_out = Spart).
 int launch_spmm(kkm_ctx *h, const int32_t *labels, const double **s_out, int *nsplit_out) {
   const Plan &P = h->P;
+  if (P.sym) {
+    *nsplit_out = 1;
+    return launch_spmm_sym(h, labels, s_out);
+  }
+  if (P.ssym) {
+    *nsplit_out = 1;
+    return launch_stream_sym(h, labels, s_out);
+  }
   CKR(P.materialize ? launch_spmm_mat(h, labels) : launch_stream(h, labels));
   if (P.pr == 1) {
     *s_out = h->Spart;
@@ -457,7 +691,7 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, double *E_out, double *cn
     int fth = FIN_THREADS;  // power of two with (k+1) * fth doubles <= 48 KB
     while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
-        S, nsplit, P.nloc, P.pr > 1 ? P.B : P.nApad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
+        S, nsplit, P.nloc, P.s_rows_pad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
         E_out, h->blockpart);
     CKL();
   }
@@ -615,7 +849,27 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   if (P.pr > 1) {
     h->labB = (int32_t *)(w + P.o_labB);
     h->Scol = (double *)(w + P.o_Scol);
-    h->Smine = (double *)(w + P.o_Smine);
+  }
+  if (P.pr > 1 || (P.sym && P.nranks > 1)) h->Smine = (double *)(w + P.o_Smine);
+  if (P.ssym) {
+    h->units = (int4 *)(w + P.o_units);
+    h->Sfix = (long long *)(w + P.o_Sfix);
+    if (P.nranks > 1) {
+      h->Sorig = (long long *)(w + P.o_Sorig);
+      h->Sfmine = (long long *)(w + P.o_Sfmine);
+    }
+    h->fxmax = (float *)(w + P.o_fxmax);
+  }
+  if (P.sym) {
+    h->perm_b = (int32_t *)(w + P.o_perm_b);
+    h->groups = (SymGroup *)(w + P.o_groups);
+    h->ngroups = (int32_t *)(w + P.o_ngroups);
+    h->bands = (SymBand *)(w + P.o_bands);
+    h->band_desc = (int32_t *)(w + P.o_band_desc);
+    h->colpart = (float *)(w + P.o_colpart);
+    h->colsum = (double *)(w + P.o_colsum);
+    h->gfirst = (int32_t *)(w + P.o_gfirst);
+    h->Sfin = (double *)(w + P.o_Sfin);
   }
   h->kp.kind = p->kind;
   h->kp.degree = p->degree;
@@ -674,8 +928,36 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         h->lab[0], P.n, P.k, h->sizes[0]);
     CKL();
     CK(cudaEventRecord(e1, h->st));
-    // ---- a1: K tile [A set, B set] = kappa(X X^T), materialised once
-    if (P.materialize) CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));
+    // ---- a1: K tile [A set, B set] = kappa(X X^T), materialised once; with
+    // symmetric storage (f1) the owned upper-triangle bands, one launch each
+    if (P.ssym) {  // units, and the fixed-point scale 2^s with n * max|K| * 2^s < 2^61
+      if (!P.units.empty())
+        CK(cudaMemcpyAsync(h->units, P.units.data(), P.units.size() * sizeof(int4), cudaMemcpyHostToDevice, h->st));
+      max_norm_kernel<<<1, 1024, 0, h->st>>>(h->norms, P.n, h->fxmax);
+      CKL();
+      float mx = 0.f;
+      CK(cudaMemcpyAsync(&mx, h->fxmax, 4, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      // |K_ij| <= max_i K_ii (K is a Gram matrix of phi); K_ii from the squared norm
+      double kmax = 1.0;
+      if (p->kind == KKM_KERNEL_LINEAR) kmax = std::max(1e-30, (double)mx);
+      if (p->kind == KKM_KERNEL_POLY) kmax = std::pow(p->gamma * mx + std::fabs(p->coef0), (double)p->degree);
+      const int sh = (int)std::floor(61.0 - std::log2(std::max(1e-300, (double)P.n * kmax * 1.0001)));
+      h->fx_scale = std::ldexp(1.0, sh);
+      h->fx_inv = std::ldexp(1.0, -sh);
+    }
+    if (P.sym) {
+      if (!P.bands.empty())
+        CK(cudaMemcpyAsync(h->bands, P.bands.data(), P.bands.size() * sizeof(SymBand), cudaMemcpyHostToDevice,
+                           h->st));
+      CK(cudaMemcpyAsync(h->band_desc, P.band_desc.data(), (size_t)P.T * 4, cudaMemcpyHostToDevice, h->st));
+      for (const SymBand &b : P.bands) {
+        const int64_t i0 = (int64_t)b.band * SYM_TB;
+        CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, h->K + b.koff, b.ldb));
+      }
+    } else if (P.materialize) {
+      CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));
+    }
     CK(cudaEventRecord(e2, h->st));
     CK(cudaStreamSynchronize(h->st));
     if (h->p.timing) {
@@ -826,7 +1108,106 @@ int kkm_set_labels(kkm_handle h, const int32_t *labels) {
   return KKM_OK;
 }
 
-int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *labels_out, double *D_out) {
+}  // extern "C"
+
+namespace {
+
+// Layout of kkm_predict's scratch: Y operands, sort scratch, sorted X (materialised handles
+// only: streaming handles lend their own), the partials and the outputs.
+struct PredictPlan {
+  int64_t mpad;
+  int nsplit, nblk;
+  bool own_sorted;
+  size_t oYf, oYhi, oYlo, oYn, oYr, oYd, oSp, oLab, oD, oPerm, oPos, oSeg, oBc, oBo, oShi, oSlo, oSn, oSr, total;
+};
+
+PredictPlan predict_plan(const kkm_ctx *h, int64_t m) {
+  const Plan &P = h->P;
+  PredictPlan q;
+  q.mpad = round_up(std::max<int64_t>(m, 1), 256);
+  q.nblk = (int)ceil_div(P.n, SORT_BLOCK);
+  const int64_t tiles_n = ceil_div(P.n, 256);
+  q.nsplit = 2 * (int)std::max<int64_t>(ceil_div(tiles_n, 512),
+                                        ts_choose_splits((m + 1) / 2, P.n, h->num_sms / 2));
+  q.own_sorted = P.materialize;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  const int k = P.k;
+  q.oYf = take((size_t)q.mpad * P.ldf * 4);
+  q.oYhi = take((size_t)q.mpad * P.dp * 2);
+  q.oYlo = take((size_t)q.mpad * P.dp * 2);
+  q.oYn = take((size_t)q.mpad * 4);
+  q.oYr = take((size_t)q.mpad * 4);
+  q.oYd = take((size_t)q.mpad * 8);
+  q.oSp = take((size_t)q.nsplit * q.mpad * k * 8);
+  q.oLab = take((size_t)q.mpad * 4);
+  q.oD = take((size_t)q.mpad * k * 8);
+  q.oPerm = take((size_t)P.lablen * 4);
+  q.oPos = take((size_t)P.lablen * 4);
+  q.oSeg = take((size_t)(k + 1) * 4);
+  q.oBc = take((size_t)q.nblk * k * 4);
+  q.oBo = take((size_t)q.nblk * k * 4);
+  q.oShi = q.own_sorted ? take((size_t)P.npad * P.dp * 2) : 0;
+  q.oSlo = q.own_sorted ? take((size_t)P.npad * P.dp * 2) : 0;
+  q.oSn = q.own_sorted ? take((size_t)P.npad * 4) : 0;
+  q.oSr = q.own_sorted ? take((size_t)P.npad * 4) : 0;
+  q.total = off;
+  return q;
+}
+
+int predict_run(kkm_ctx *h, const PredictPlan &q, uint8_t *t, const float *Y, int64_t m, int64_t ldy,
+                int32_t *labels_out, double *D_out) {
+  const Plan &P = h->P;
+  const int k = P.k;
+  float *Yf = (float *)(t + q.oYf), *yn = (float *)(t + q.oYn), *yr = (float *)(t + q.oYr);
+  uint16_t *Yhi = (uint16_t *)(t + q.oYhi), *Ylo = (uint16_t *)(t + q.oYlo);
+  double *yd = (double *)(t + q.oYd), *Sp = (double *)(t + q.oSp), *Dy = D_out ? (double *)(t + q.oD) : nullptr;
+  int32_t *ylab = (int32_t *)(t + q.oLab);
+  const bool own = q.own_sorted;
+  SortedSet B{own ? (uint16_t *)(t + q.oShi) : h->Shi, own ? (uint16_t *)(t + q.oSlo) : h->Slo,
+              own ? (float *)(t + q.oSn) : h->snorms, own ? (float *)(t + q.oSr) : h->srscale,
+              (int32_t *)(t + q.oPerm), (int32_t *)(t + q.oPos), (int32_t *)(t + q.oSeg), (int32_t *)(t + q.oBc),
+              (int32_t *)(t + q.oBo)};
+  // a5 for the new points: split operands, norms, kappa(y, y) (prep_rows and diag read only
+  // rows < m and columns < d of Yf, and write the split's pad rows/columns as zeros)
+  CK(cudaMemcpy2DAsync(Yf, P.ldf * 4, Y, ldy * 4, P.d * 4, m, cudaMemcpyDefault, h->st));
+  prep_rows_kernel<<<(unsigned)ceil_div(q.mpad, 8), 256, 0, h->st>>>(Yf, P.ldf, m, q.mpad, P.d, yn, Yhi, Ylo, P.dp,
+                                                                     P.fp16 ? 2 : 1, yr);
+  CKL();
+  diag_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, h->st>>>(Yf, P.ldf, P.d, 0, m, h->p.kind, h->p.gamma, h->p.coef0,
+                                                            h->p.degree, yd);
+  CKL();
+  // B = all n training points sorted by their current labels; A = Y
+  CKR(sort_gather(h, h->lab[h->cur], 0, P.n, P.npad, B));
+  TcStream &ts = h->ts_predict;
+  const StreamA A{Yhi, Ylo, yn, yr, q.mpad, 0, m, q.mpad};
+  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, q.nsplit, Sp));
+  predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, q.nsplit, m, q.mpad, k, h->sizes[h->cur],
+                                                                h->cnorm2, yd, ylab, Dy);
+  CKL();
+  CKR(copy_any(h, labels_out, ylab, (size_t)m * 4));
+  if (D_out) CKR(copy_any(h, D_out, Dy, (size_t)m * k * 8));
+  CK(cudaStreamSynchronize(h->st));
+  return KKM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kkm_predict_workspace_size(kkm_handle h, int64_t m, size_t *bytes) {
+  if (!h || !bytes) return fail(KKM_EINVAL, "NULL argument");
+  if (m < 0) return fail(KKM_EINVAL, "m=%lld < 0", (long long)m);
+  *bytes = predict_plan(h, m).total;
+  return KKM_OK;
+}
+
+int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *labels_out, double *D_out,
+                void *workspace, size_t ws_bytes) {
   if (!h) return fail(KKM_EINVAL, "handle is NULL");
   if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
   const Plan &P = h->P;
@@ -835,70 +1216,23 @@ int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *l
   if (!Y || !labels_out) return fail(KKM_EINVAL, "NULL argument");
   if (ldy < P.d) return fail(KKM_EINVAL, "ldy=%lld < d=%lld", (long long)ldy, (long long)P.d);
   if (!P.tc) return fail(KKM_EUNSUP, "kkm_predict needs a tensor-core precision (FP16X3 or BF16X3)");
+  const PredictPlan q = predict_plan(h, m);
+  if (workspace) {
+    if (((uintptr_t)workspace) & 255) return fail(KKM_EINVAL, "workspace must be 256-byte aligned");
+    if (ws_bytes < q.total) return fail(KKM_ENOMEM, "workspace %zu bytes < required %zu", ws_bytes, q.total);
+  }
   if (!h->cnorm2_valid) {  // c of the current labels: the kkm_objective pass (collective for nranks > 1)
     if (P.nranks > 1) return fail(KKM_ESTATE, "call kkm_fit or kkm_objective on every rank before kkm_predict");
     double J = 0.0;
     CKR(kkm_objective(h, &J));
   }
-  const int k = P.k;
-  const int64_t mpad = round_up(m, 256);
-  const int nblk = (int)ceil_div(P.n, SORT_BLOCK);
-  const int64_t tiles_n = ceil_div(P.n, 256);
-  const int nsplit =
-      2 * (int)std::max<int64_t>(ceil_div(tiles_n, 512), ts_choose_splits((m + 1) / 2, P.n, h->num_sms / 2));
-  // one temporary block: Y operands, sort scratch, sorted X (materialised handles), partials
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off += (bytes + 255) / 256 * 256;
-    return o;
-  };
-  const size_t oYf = take((size_t)mpad * P.ldf * 4), oYhi = take((size_t)mpad * P.dp * 2),
-               oYlo = take((size_t)mpad * P.dp * 2), oYn = take((size_t)mpad * 4), oYr = take((size_t)mpad * 4),
-               oYd = take((size_t)m * 8), oSp = take((size_t)nsplit * mpad * k * 8), oLab = take((size_t)m * 4),
-               oD = D_out ? take((size_t)m * k * 8) : 0, oPerm = take((size_t)P.lablen * 4),
-               oPos = take((size_t)P.lablen * 4), oSeg = take((size_t)(k + 1) * 4),
-               oBc = take((size_t)nblk * k * 4), oBo = take((size_t)nblk * k * 4);
-  const bool own_sorted = P.materialize;  // streaming handles lend their sorted-operand scratch
-  const size_t oShi = own_sorted ? take((size_t)P.npad * P.dp * 2) : 0,
-               oSlo = own_sorted ? take((size_t)P.npad * P.dp * 2) : 0,
-               oSn = own_sorted ? take((size_t)P.npad * 4) : 0, oSr = own_sorted ? take((size_t)P.npad * 4) : 0;
+  if (workspace) return predict_run(h, q, (uint8_t *)workspace, Y, m, ldy, labels_out, D_out);
   uint8_t *t = nullptr;
-  if (cudaMallocAsync((void **)&t, off, h->st) != cudaSuccess) {
+  if (cudaMallocAsync((void **)&t, q.total, h->st) != cudaSuccess) {
     cudaGetLastError();
-    return fail(KKM_ENOMEM, "kkm_predict: cannot allocate %zu temporary bytes", off);
+    return fail(KKM_ENOMEM, "kkm_predict: cannot allocate %zu temporary bytes", q.total);
   }
-  int rc = [&]() -> int {
-    float *Yf = (float *)(t + oYf), *yn = (float *)(t + oYn), *yr = (float *)(t + oYr);
-    uint16_t *Yhi = (uint16_t *)(t + oYhi), *Ylo = (uint16_t *)(t + oYlo);
-    double *yd = (double *)(t + oYd), *Sp = (double *)(t + oSp), *Dy = D_out ? (double *)(t + oD) : nullptr;
-    int32_t *ylab = (int32_t *)(t + oLab);
-    SortedSet B{own_sorted ? (uint16_t *)(t + oShi) : h->Shi, own_sorted ? (uint16_t *)(t + oSlo) : h->Slo,
-                own_sorted ? (float *)(t + oSn) : h->snorms, own_sorted ? (float *)(t + oSr) : h->srscale,
-                (int32_t *)(t + oPerm), (int32_t *)(t + oPos), (int32_t *)(t + oSeg), (int32_t *)(t + oBc),
-                (int32_t *)(t + oBo)};
-    // a5 for the new points: split operands, norms, kappa(y, y)
-    CK(cudaMemsetAsync(Yf, 0, (size_t)mpad * P.ldf * 4, h->st));
-    CK(cudaMemcpy2DAsync(Yf, P.ldf * 4, Y, ldy * 4, P.d * 4, m, cudaMemcpyDefault, h->st));
-    prep_rows_kernel<<<(unsigned)ceil_div(mpad, 8), 256, 0, h->st>>>(Yf, P.ldf, m, mpad, P.d, yn, Yhi, Ylo, P.dp,
-                                                                     P.fp16 ? 2 : 1, yr);
-    CKL();
-    diag_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, h->st>>>(Yf, P.ldf, P.d, 0, m, h->p.kind, h->p.gamma,
-                                                              h->p.coef0, h->p.degree, yd);
-    CKL();
-    // B = all n training points sorted by their current labels; A = Y
-    CKR(sort_gather(h, h->lab[h->cur], 0, P.n, P.npad, B));
-    TcStream ts;
-    const StreamA A{Yhi, Ylo, yn, yr, mpad, 0, m, mpad};
-    CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, nsplit, Sp));
-    predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, nsplit, m, mpad, k, h->sizes[h->cur],
-                                                                  h->cnorm2, yd, ylab, Dy);
-    CKL();
-    CKR(copy_any(h, labels_out, ylab, (size_t)m * 4));
-    if (D_out) CKR(copy_any(h, D_out, Dy, (size_t)m * k * 8));
-    CK(cudaStreamSynchronize(h->st));
-    return KKM_OK;
-  }();
+  const int rc = predict_run(h, q, t, Y, m, ldy, labels_out, D_out);
   cudaFreeAsync(t, h->st);
   if (rc == KKM_OK) CK(cudaStreamSynchronize(h->st));
   return rc;

@@ -526,6 +526,166 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
   t2_teardown(s, warp, tmem_base);
 }
 
+// ---------------------------------------------------------------- f1: symmetric streaming
+// A = B = the label-sorted points. Work unit u = units[u] = (tm, tn0, ntn, 0): pair row tile tm
+// against the column tiles tn0 .. tn0 + ntn - 1 (tn0 >= tm: the upper triangle of the sorted
+// K). Every tile adds its row sums by the column segments to Sfix[p][c] (rows p), and, unless
+// it is a diagonal tile (tn == tm, whose row sums already cover both halves), its column sums
+// by the row segments to Sfix[q][c] (columns q): K(p, q) = K(q, p). Sums are added in int64
+// fixed point (value * 2^s, red.add: associative, so the result is bitwise independent of the
+// order, of the grid and of the rank count).
+struct T2SymSched {
+  const int4 *units;
+  int64_t nitems;
+  __device__ __forceinline__ void item(int64_t u, int &ra, int &rb0, int &ntn) const {
+    const int4 U = units[u];
+    ra = U.x * T2_BM;
+    rb0 = U.y * 256;
+    ntn = U.z;
+  }
+};
+
+__device__ __forceinline__ void red_add_s64(long long *p, long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int KMAX>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
+    tc2_stream_sym_kernel(const __grid_constant__ CUtensorMap t_hi, const __grid_constant__ CUtensorMap t_lo,
+                          uint32_t idesc, int nkb, int64_t n, const float *__restrict__ snorms,
+                          const float *__restrict__ srscale, const int32_t *__restrict__ seg_g, int k,
+                          KappaParams kp, T2SymSched sc, double fx_scale, long long *__restrict__ Sfix) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *extra;
+  const T2Smem s = t2_carve(smem_raw, (uint32_t)T2_STREAM_EXTRA, &extra);
+  float *colc = reinterpret_cast<float *>(extra);
+  int32_t *seg = reinterpret_cast<int32_t *>(extra + TC_EPI_WARPS * TC_COLC_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cr = cluster_ctarank();
+  const bool fp16 = srscale != nullptr;
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) seg[c] = seg_g[c];
+  t2_setup(s, warp);
+  const uint32_t tmem_base = *s.tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) t2_producer(sc, s, &t_hi, &t_lo, &t_hi, &t_lo, nkb, cr, 1);
+  } else if (warp == 1) {
+    if (lane == 0 && cr == 0) t2_mma(sc, s, nkb, idesc, tmem_base);
+  } else {
+    const int e = warp - 2;
+    const int quarter = warp & 3;
+    const int half = e >> 2;
+    float *cn = colc + e * 256;
+    const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    int64_t it = 0;
+    for (int64_t u = cl; u < sc.nitems; u += ncl) {
+      const int4 U = sc.units[u];
+      const int tm = U.x, tn0 = U.y, tn1 = U.y + U.z;
+      const int64_t rw = (int64_t)tm * T2_BM + (int64_t)cr * 128 + quarter * 32;  // warp's first row
+      const int64_t p = rw + lane;                                                 // this thread's row
+      const bool row_ok = p < n;
+      const float ni = row_ok ? snorms[p] : 0.f;
+      const float rsi = (fp16 && row_ok) ? srscale[p] : 1.f;
+      const RowK rk = make_rowk(kp, rsi, ni);
+      // labels of the warp's 32 rows (sorted: a contiguous run of segments r0 .. r1)
+      const int64_t plast = rw + 31 < n ? rw + 31 : n - 1;
+      int r0 = 0, r1 = 0;
+      for (int cc = 1; cc < k; ++cc) {
+        if (seg[cc] <= rw) r0 = cc;
+        if (seg[cc] <= plast) r1 = cc;
+      }
+      int mylab = r0;
+      for (int cc = r0 + 1; cc <= r1; ++cc)
+        if (seg[cc] <= p) mylab = cc;
+      double acc[KMAX];
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c) acc[c] = 0.0;
+      for (int tn = tn0; tn < tn1; ++tn, ++it) {
+        const int64_t pbase = (int64_t)tn * 256 + half * 128;
+        const bool diag = tn == tm;
+        stage_column_constants(cn, snorms, fp16 ? srscale : nullptr, pbase, n, kp.kind == 2, lane);
+        mbar_wait(s.tfull, (uint32_t)(it & 1));
+        tc_fence_after();
+        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          const int col = half * 128 + c * 32;
+          float v[32], w[32];
+          tmem_ld2_32(tq + (uint32_t)col, tq + (uint32_t)(256 + col), v, w);
+          const int64_t p0 = pbase + c * 32;
+          if (p0 >= n || rw >= n) continue;
+          kappa_chunk(v, w, cn + c * 32, cn + 128 + c * 32, kp, rk);
+          if (diag && kp.kind == 2 && p >= p0 && p < p0 + 32) {  // kappa(x_p, x_p) = 1 exactly (A1)
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (p0 + q == p) v[q] = 1.f;
+          }
+          if (p0 + 32 > n) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (p0 + q >= n) v[q] = 0.f;
+          }
+          if (!row_ok) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = 0.f;
+          }
+          // row part: the chunk's columns by their segments
+          const int64_t p1 = p0 + 31 < n ? p0 + 31 : n - 1;
+          int c0 = 0, c1 = 0;
+          for (int cc = 1; cc < k; ++cc) {
+            if (seg[cc] <= p0) c0 = cc;
+            if (seg[cc] <= p1) c1 = cc;
+          }
+          if (c0 == c1) {
+            float2 s2 = make_float2(v[0], v[1]);
+#pragma unroll
+            for (int q = 2; q < 32; q += 2) s2 = f2add(s2, make_float2(v[q], v[q + 1]));
+            acc_add<KMAX>(acc, c0, (double)(s2.x + s2.y));
+          } else {
+            for (int cc = c0; cc <= c1; ++cc) {
+              const int64_t lo = seg[cc] - p0, hi = seg[cc + 1] - p0;
+              float sum = 0.f;
+#pragma unroll
+              for (int q = 0; q < 32; ++q) sum += (q >= lo && q < hi) ? v[q] : 0.f;
+              acc_add<KMAX>(acc, cc, (double)sum);
+            }
+          }
+          if (diag) continue;
+          // column part: column p0 + lane gets the sum over the warp's rows of each label
+          for (int cc = r0; cc <= r1; ++cc) {
+            float t[32];
+            const bool mine = mylab == cc;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) t[q] = mine ? v[q] : 0.f;
+            // reduce-scatter butterfly: afterwards lane l holds the sum over the lanes of t[l]
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int q = 0; q < o; ++q) {
+                const float send = up ? t[q] : t[q + o];
+                const float keep = up ? t[q + o] : t[q];
+                t[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+              }
+            }
+            if (p0 + lane < n)
+              red_add_s64(Sfix + (p0 + lane) * k + cc, __double2ll_rn((double)t[0] * fx_scale));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int c = 0; c < KMAX; ++c)
+          if (c < k) red_add_s64(Sfix + p * k + c, __double2ll_rn(acc[c] * fx_scale));
+      }
+    }
+  }
+  t2_teardown(s, warp, tmem_base);
+}
+
 // ---------------------------------------------------------------- host launchers
 // Materialised: same contract as tc_gemm_launch (gemm_tc.cuh), on CTA pairs.
 inline int tc2_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16,
@@ -665,5 +825,77 @@ inline int tc2_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
   }
   return 0;
 }
+
+// f1 streaming launcher: A = B = the sorted operand (Shi/Slo, rows rows). units: device array
+// of nunits int4 (tm, tn0, ntn, 0). Sfix (n x k int64) must be zeroed by the caller.
+template <int KMAX>
+inline int t2sym_launch_k(bool &attr, unsigned grid, cudaStream_t st, const TcStream &g, uint32_t idesc, int nkb,
+                          int64_t n, const float *snorms, const float *rs, const int32_t *seg, int k,
+                          const KappaParams &kp, const T2SymSched &sc, double fx_scale, long long *Sfix) {
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc2_stream_sym_kernel<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)T2_STREAM_SMEM) != cudaSuccess) {
+      tc_err_slot() = "cudaFuncSetAttribute(tc2_stream_sym_kernel) failed";
+      return 1;
+    }
+    attr = true;
+  }
+  tc2_stream_sym_kernel<KMAX><<<grid, T2_THREADS, T2_STREAM_SMEM, st>>>(g.a_hi, g.a_lo, idesc, nkb, n, snorms, rs,
+                                                                        seg, k, kp, sc, fx_scale, Sfix);
+  return 0;
+}
+
+inline int tc2_stream_sym_launch(TcStream &g, const uint16_t *Shi, const uint16_t *Slo, bool fp16, int64_t rows,
+                                 int64_t dp, int64_t n, const float *snorms, const float *srscale,
+                                 const int32_t *seg, int k, const KappaParams &kp, const int4 *units,
+                                 int64_t nunits, double fx_scale, long long *Sfix, cudaStream_t st,
+                                 int64_t *launches) {
+  if (!tc_encode_fn()) {
+    TcGemm tmp;
+    if (tc_make_maps(tmp, Shi, Slo, fp16, rows, dp)) return 1;
+  }
+  if (g.ahi != Shi || g.alo != Slo || g.bhi != Shi || g.blo != Slo || g.fp16 != fp16 || g.arows != rows ||
+      g.brows != rows) {
+    if (ts_encode(&g.a_hi, Shi, fp16, rows, dp) || ts_encode(&g.a_lo, Slo, fp16, rows, dp)) return 1;
+    g.b_hi = g.a_hi;
+    g.b_lo = g.a_lo;
+    g.ahi = g.bhi = Shi;
+    g.alo = g.blo = Slo;
+    g.fp16 = fp16;
+    g.arows = g.brows = rows;
+  }
+  if (!g.num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (nunits <= 0) return 0;
+  if (k > 16) {
+    tc_err_slot() = "tc2_stream_sym_launch: k <= 16";
+    return 1;
+  }
+  T2SymSched sc;
+  sc.units = units;
+  sc.nitems = nunits;
+  const int64_t clusters = nunits < g.num_sms / 2 ? nunits : g.num_sms / 2;
+  const unsigned grid = (unsigned)(2 * clusters);
+  const uint32_t idesc = t2_idesc(fp16);
+  const int nkb = (int)(dp / TC_BK);
+  const float *rs = fp16 ? srscale : nullptr;
+  static bool a4 = false, a8 = false, a16 = false;
+  int rc;
+  if (k <= 4) rc = t2sym_launch_k<4>(a4, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  else if (k <= 8) rc = t2sym_launch_k<8>(a8, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  else rc = t2sym_launch_k<16>(a16, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  if (rc) return rc;
+  if (launches) ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    tc_err_slot() = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
 
 }  // namespace kkm

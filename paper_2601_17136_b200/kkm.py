@@ -17,6 +17,7 @@ _NAMES = {1: "KKM_EINVAL", 2: "KKM_ELABEL", 3: "KKM_ENOMEM", 4: "KKM_EUNSUP", 5:
 KERNEL_LINEAR, KERNEL_POLY, KERNEL_GAUSSIAN = 0, 1, 2
 PATH_AUTO, PATH_MATERIALIZE, PATH_STREAM = 0, 1, 2
 PREC_BF16X3, PREC_FP32_SIMT, PREC_FP16X3 = 0, 1, 2
+SYM_AUTO, SYM_OFF, SYM_ON = 0, 1, 2
 DBG_E, DBG_CNORM, DBG_SIZES, DBG_DIAG, DBG_DFULL, DBG_LABELS_PREV = range(6)
 PHASES = ("init_prep", "init_gemm", "spmm", "cnorm", "assign")
 
@@ -32,7 +33,8 @@ class KKMParams(ctypes.Structure):
                 ("degree", ctypes.c_int32), ("k", ctypes.c_int32), ("max_iter", ctypes.c_int32),
                 ("stop_on_no_change", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("timing", ctypes.c_int32),
-                ("grid_rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("grid_rows", ctypes.c_int32), ("symmetric", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 _lib = None
@@ -60,7 +62,8 @@ def lib():
             "kkm_assign": [P, P],
             "kkm_objective": [P, P],
             "kkm_set_labels": [P, P],
-            "kkm_predict": [P, P, i64, i64, P, P],
+            "kkm_predict": [P, P, i64, i64, P, P, P, ctypes.c_size_t],
+            "kkm_predict_workspace_size": [P, i64, P],
             "kkm_debug_read": [P, i32, P],
             "kkm_kernel_tile": [P, i64, i64, i32, i32, P],
             "kkm_phase_ms": [P, P],
@@ -138,7 +141,7 @@ class KernelKMeans:
                  stop_on_no_change: bool = False, path: int = PATH_AUTO,
                  precision: int = PREC_FP16X3, timing: bool = False, init_labels=None,
                  rank: int = 0, nranks: int = 1, comm=None, stream=None, device=None,
-                 workspace=None, grid_rows: int = 1):
+                 workspace=None, grid_rows: int = 1, symmetric: int = SYM_AUTO):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
@@ -151,6 +154,7 @@ class KernelKMeans:
         p.k, p.max_iter, p.stop_on_no_change = k, max_iter, int(stop_on_no_change)
         p.path, p.precision, p.timing = path, precision, int(timing)
         p.grid_rows = grid_rows
+        p.symmetric = symmetric
         self.params = p
         self.max_iter = max_iter
         nb = workspace_size(p, self.n, self.d, rank, nranks)
@@ -193,10 +197,12 @@ class KernelKMeans:
             labels = np.ascontiguousarray(labels, dtype=np.int32)
         _check(lib().kkm_set_labels(self.h, _ptr(labels)))
 
-    def predict(self, Y, return_distances: bool = False):
+    def predict(self, Y, return_distances: bool = False, use_workspace: bool = True):
         """Out-of-sample assignment of the rows of Y (host numpy or device tensor, m x d fp32)
         to the clusters of the current labels (kkm_predict). Returns int32 labels (numpy for
-        numpy input, else a tensor on the handle's device), plus the m x k fp64 distances."""
+        numpy input, else a tensor on the handle's device), plus the m x k fp64 distances.
+        The scratch is a cached device buffer (use_workspace=False: the library allocates
+        stream-ordered scratch per call instead)."""
         on_host = isinstance(Y, np.ndarray)
         if on_host:
             Y = np.ascontiguousarray(Y, dtype=np.float32)
@@ -214,7 +220,17 @@ class KernelKMeans:
             lab = self.torch.empty(m, dtype=self.torch.int32, device=self.device)
             D = (self.torch.empty((m, self.k), dtype=self.torch.float64, device=self.device)
                  if return_distances else None)
-        _check(lib().kkm_predict(self.h, _ptr(Y), m, ldy, _ptr(lab), _ptr(D)))
+        ws, nws = None, 0
+        if use_workspace:
+            nb = ctypes.c_size_t(0)
+            _check(lib().kkm_predict_workspace_size(self.h, m, ctypes.byref(nb)))
+            ws = getattr(self, "_predict_ws", None)
+            if ws is None or ws.numel() < nb.value:  # kept across calls
+                self._predict_ws = None
+                ws = self._predict_ws = self.torch.empty(max(nb.value, 256), dtype=self.torch.uint8,
+                                                         device=self.device)
+            nws = ws.numel()
+        _check(lib().kkm_predict(self.h, _ptr(Y), m, ldy, _ptr(lab), _ptr(D), _ptr(ws), nws))
         return (lab, D) if return_distances else lab
 
     def debug_read(self, what: int) -> np.ndarray:

@@ -49,7 +49,7 @@ def test_workspace_size_and_errors():
     p.k = 10
     nb = kkm.workspace_size(p, 60000, 784)
     ldk = 60000
-    assert nb >= 60000 * ldk * 4  # K block materialised
+    assert nb >= 60000 * ldk * 4 / 2  # K materialised (upper-triangle bands by default, f1)
     nb2 = kkm.workspace_size(p, 60000, 784, rank=1, nranks=4)
     assert nb2 < nb / 3
     with pytest.raises(kkm.KKMError, match="EINVAL"):
@@ -84,8 +84,24 @@ def test_workspace_size_and_errors():
     q.grid_rows = 2  # 2 x 2 grid: K tile = column block (2 of 4 blocks) x row block (2 of 4)
     nb_15 = kkm.workspace_size(q, 60000, 784, rank=1, nranks=4)
     q.grid_rows = 1
+    q.symmetric = kkm.SYM_OFF
     nb_1d = kkm.workspace_size(q, 60000, 784, rank=1, nranks=4)
     assert abs(nb_15 - nb_1d) < 0.05 * nb_1d  # same K-tile size, n^2 / P
+    # f1: the symmetric bands hold ~n^2/2 floats (+ 1/R of them as column partials), spread
+    # over the ranks by area
+    q.symmetric = kkm.SYM_AUTO
+    kfull = 60000 * 60000 * 4
+    nb_sym1 = kkm.workspace_size(q, 60000, 784)
+    q.symmetric = kkm.SYM_OFF
+    nb_full1 = kkm.workspace_size(q, 60000, 784)
+    assert nb_full1 - kfull < 0.05 * kfull  # + X, its split copies and the small arrays
+    assert 0.5 * kfull < nb_sym1 < 0.62 * kfull
+    q.symmetric = kkm.SYM_AUTO
+    shares = [kkm.workspace_size(q, 60000, 784, rank=r, nranks=4) for r in range(4)]
+    assert max(shares) < 1.1 * min(shares) and sum(shares) < 0.7 * kfull
+    q.symmetric = 3
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(q, 100, 4)
     q = kkm.default_params()
     q.reserved[2] = 1
     with pytest.raises(kkm.KKMError, match="EINVAL"):

@@ -20,14 +20,20 @@ import paper_2601_17136_b200 as kkm  # noqa: E402
 # tolerance, so it is tested at the K level only (test_bf16x3_kernel_level, A9).
 # modes = (precision, path): the SIMT baseline and the tensor-core path, materialised and
 # streaming (K never stored; SURVEY §8 a1/a2 "recomputed per tile per iteration")
+# f1 (symmetric K): materialised runs store upper-triangle bands from n >= 8192 on (AUTO), so
+# "fp16x3-sym" forces them at the test sizes; streaming runs use the upper-triangle kernel by
+# default ("fp16x3-stream"), "fp16x3-stream-full" keeps the full streaming kernel covered.
 PRECISIONS = [(kkm.PREC_FP32_SIMT, kkm.PATH_MATERIALIZE), (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE),
-              (kkm.PREC_FP16X3, kkm.PATH_STREAM)]
-PREC_IDS = ["fp32", "fp16x3", "fp16x3-stream"]
+              (kkm.PREC_FP16X3, kkm.PATH_STREAM), (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON),
+              (kkm.PREC_FP16X3, kkm.PATH_STREAM, kkm.SYM_OFF)]
+PREC_IDS = ["fp32", "fp16x3", "fp16x3-stream", "fp16x3-sym", "fp16x3-stream-full"]
 
 
 def _handle(X, k, kind, gamma, coef0, degree, max_iter, precision, **kw):
     if isinstance(precision, tuple):
-        precision, kw["path"] = precision
+        if len(precision) == 3:
+            kw["symmetric"] = precision[2]
+        precision, kw["path"] = precision[:2]
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
     return kkm.KernelKMeans(Xd, X.shape[0], k, kind, gamma, coef0, degree, max_iter=max_iter,
                             precision=precision, **kw)
@@ -162,7 +168,8 @@ def test_host_buffers_e2e(precision):
     ref = oracle.fit(X, 4, oracle.GAUSSIAN, 0.01, max_iter=5)
     Xh = torch.from_numpy(X).pin_memory()
     h = kkm.KernelKMeans(Xh, 1000, 4, kkm.KERNEL_GAUSSIAN, 0.01, 0.0, 1, max_iter=5,
-                         precision=precision[0], path=precision[1])
+                         precision=precision[0], path=precision[1],
+                         symmetric=precision[2] if len(precision) > 2 else kkm.SYM_AUTO)
     h.fit()
     out = torch.empty(1000, dtype=torch.int32).pin_memory()
     h.assign(out)
@@ -182,6 +189,25 @@ def test_stream_equals_materialised():
     assert np.array_equal(la, lb)
     assert np.allclose(Ja, Jb, rtol=1e-6, atol=0)
     assert np.allclose(a.debug_read(kkm.DBG_E), b.debug_read(kkm.DBG_E), rtol=1e-5, atol=1e-3)
+    # f1: upper-triangle storage / upper-triangle streaming against the full K (a)
+    for mode in ((kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON),
+                 (kkm.PREC_FP16X3, kkm.PATH_STREAM, kkm.SYM_OFF)):
+        c = _handle(X, 10, *args, 12, mode)
+        ic, Jc, cc = c.fit()
+        assert np.array_equal(la, c.assign().cpu().numpy())
+        assert np.allclose(Ja, Jc, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("k", [3, 11, 16])
+@pytest.mark.parametrize("kind", [oracle.LINEAR, oracle.GAUSSIAN])
+def test_symmetric_bands(k, kind):
+    """f1: band storage with 5 bands of 1024 rows, the last one 37 rows (no column part of its
+    own), and the upper-triangle streaming kernel over 17 pair tiles (the last one 37 rows);
+    k = 3, 11, 16; teacher-forced against the oracle."""
+    X = synth.blobs(4133, 6, k, seed=60 + k, sep=2.5)
+    gamma = 0.05 if kind == oracle.GAUSSIAN else 1.0
+    teacher_forced(X, k, kind, gamma, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON))
+    teacher_forced(X, k, kind, gamma, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_STREAM))
 
 
 def test_errors_and_poison_free():

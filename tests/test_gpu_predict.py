@@ -40,12 +40,15 @@ def _check_predict(h, Xtr, Y, k, kind, gamma, coef0, degree):
     assert np.array_equal(np.isfinite(Dg), np.isfinite(D))
     E = np.where(np.isfinite(D), (kyy[:, None] + np.where(fin, cn, 0)[None] - np.where(np.isfinite(D), D, 0)) / 2, 0)
     scale = np.abs(kyy) + 2 * np.abs(E).max(axis=1) + abs(cn[fin].max())
-    err = np.where(np.isfinite(D), np.abs(Dg - D), 0)
+    with np.errstate(invalid="ignore"):
+        err = np.where(np.isfinite(D), np.abs(Dg - D), 0)
     assert (err <= TAU * scale[:, None]).all(), (err / scale[:, None]).max()
     check_labels(lg, nl, np.where(np.isfinite(D), D, np.inf), scale)
-    # device input / device output give the same answer
+    # device input / device output, and library-allocated scratch, give the same answer
     lg2 = h.predict(torch.from_numpy(Y).cuda()).cpu().numpy()
     assert np.array_equal(lg2, lg)
+    lg3, Dg3 = h.predict(Y, return_distances=True, use_workspace=False)
+    assert np.array_equal(lg3, lg) and np.array_equal(Dg3, Dg)
     return lg, nl
 
 
