@@ -267,6 +267,41 @@ __device__ __forceinline__ void kappa_chunk(float (&v)[32], const float (&w)[32]
   }
 }
 
+// kappa_chunk for a chunk whose main + correction sum is already in v (same fp32 operations).
+__device__ __forceinline__ void kappa_chunk_sum(float (&v)[32], const float *cnj, const float *crs,
+                                                const KappaParams &kp, const RowK &rk) {
+#pragma unroll
+  for (int q4 = 0; q4 < 8; ++q4) {
+    const float4 rj = reinterpret_cast<const float4 *>(crs)[q4];
+    float2 t01 = f2mul(make_float2(v[4 * q4], v[4 * q4 + 1]), make_float2(rj.x, rj.y));
+    float2 t23 = f2mul(make_float2(v[4 * q4 + 2], v[4 * q4 + 3]), make_float2(rj.z, rj.w));
+    if (kp.kind == 1) {
+      const float2 b01 = f2fma(rk.g, t01, rk.c), b23 = f2fma(rk.g, t23, rk.c);
+      t01 = b01;
+      t23 = b23;
+      for (int e = 1; e < kp.degree; ++e) {
+        t01 = f2mul(t01, b01);
+        t23 = f2mul(t23, b23);
+      }
+    } else if (kp.kind == 2) {
+      const float4 nj = reinterpret_cast<const float4 *>(cnj)[q4];
+      const float2 nn01 = f2add(rk.c, make_float2(nj.x, nj.y)), nn23 = f2add(rk.c, make_float2(nj.z, nj.w));
+      float2 r01 = f2fma(rk.g, t01, nn01), r23 = f2fma(rk.g, t23, nn23);
+      r01 = f2mul(make_float2(fmaxf(r01.x, 0.f), fmaxf(r01.y, 0.f)), make_float2(rk.scale, rk.scale));
+      r23 = f2mul(make_float2(fmaxf(r23.x, 0.f), fmaxf(r23.y, 0.f)), make_float2(rk.scale, rk.scale));
+      t01 = make_float2(ex2_approx(r01.x), ex2_approx(r01.y));
+      t23 = make_float2(ex2_approx(r23.x), ex2_approx(r23.y));
+    } else {
+      t01 = f2mul(t01, rk.g);
+      t23 = f2mul(t23, rk.g);
+    }
+    v[4 * q4] = t01.x;
+    v[4 * q4 + 1] = t01.y;
+    v[4 * q4 + 2] = t23.x;
+    v[4 * q4 + 3] = t23.y;
+  }
+}
+
 __device__ __forceinline__ void tmem_ld2_32(uint32_t t_main, uint32_t t_corr, float (&v)[32], float (&w)[32]) {
   tmem_ld32_nowait(t_main, v);
   tmem_ld32_nowait(t_corr, w);
@@ -469,11 +504,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         mbar_wait(s.tfull, (uint32_t)(it & 1));
         tc_fence_after();
         const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int col = half * 128 + c * 32;
           float v[32], w[32];
           tmem_ld2_32(tq + (uint32_t)col, tq + (uint32_t)(256 + col), v, w);
+          if (c == 3) {  // all of the tile is in registers: TMEM back to the MMA warp now
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
+          }
           const int64_t p0 = pbase + c * 32;
           if (p0 >= n) continue;
           kappa_chunk(v, w, cn + c * 32, cn + 128 + c * 32, kp, rk);
@@ -508,9 +548,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             }
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
       }
       if (row_ok && tn1 > tn0) {
         double *dst = Spart + ((int64_t)(2 * sp + half) * rows_pad + r) * kstride + c0;
@@ -544,6 +581,22 @@ struct T2SymSched {
     ntn = U.z;
   }
 };
+
+// Reduce-scatter butterfly over the warp: returns, on lane l, the sum over the 32 lanes of
+// t[l] (t is consumed). 31 shuffles; fixed order, deterministic.
+__device__ __forceinline__ float lane_column_sum(float (&t)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int q = 0; q < o; ++q) {
+      const float send = up ? t[q] : t[q + o];
+      const float keep = up ? t[q + o] : t[q];
+      t[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return t[0];
+}
 
 __device__ __forceinline__ void red_add_s64(long long *p, long long v) {
   asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -607,14 +660,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         mbar_wait(s.tfull, (uint32_t)(it & 1));
         tc_fence_after();
         const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll 1
+        // chunk by chunk (main + correction summed in registers); TMEM goes back to the MMA
+        // warp as soon as the last chunk is in registers, before its kappa / sums (single-
+        // buffered TMEM: this shortens the serial drain; a one-chunk-ahead prefetch measured
+        // slower, its third buffer spills)
+        float m[32], r[32];
+#pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int col = half * 128 + c * 32;
-          float v[32], w[32];
-          tmem_ld2_32(tq + (uint32_t)col, tq + (uint32_t)(256 + col), v, w);
+          const int colc = half * 128 + c * 32;
+          tmem_ld32_nowait(tq + (uint32_t)colc, m);
+          tmem_ld32_nowait(tq + (uint32_t)(256 + colc), r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 32; q += 2) {
+            const float2 t = f2add(make_float2(m[q], m[q + 1]), make_float2(r[q], r[q + 1]));
+            m[q] = t.x;
+            m[q + 1] = t.y;
+          }
+          if (c == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
+          }
+          float(&v)[32] = m;
           const int64_t p0 = pbase + c * 32;
           if (p0 >= n || rw >= n) continue;
-          kappa_chunk(v, w, cn + c * 32, cn + 128 + c * 32, kp, rk);
+          kappa_chunk_sum(v, cn + c * 32, cn + 128 + c * 32, kp, rk);
           if (diag && kp.kind == 2 && p >= p0 && p < p0 + 32) {  // kappa(x_p, x_p) = 1 exactly (A1)
 #pragma unroll
             for (int q = 0; q < 32; ++q)
@@ -652,29 +723,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
           }
           if (diag) continue;
           // column part: column p0 + lane gets the sum over the warp's rows of each label
-          for (int cc = r0; cc <= r1; ++cc) {
-            float t[32];
-            const bool mine = mylab == cc;
+          if (r0 == r1) {  // one label (almost always): the butterfly may consume v
+            const float cs = lane_column_sum(v, lane);
+            if (p0 + lane < n) red_add_s64(Sfix + (p0 + lane) * k + r0, __double2ll_rn((double)cs * fx_scale));
+          } else {  // the warp straddles a segment boundary: one masked pass per label
+            for (int cc = r0; cc <= r1; ++cc) {
+              float t[32];
+              const bool mine = mylab == cc;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) t[q] = mine ? v[q] : 0.f;
-            // reduce-scatter butterfly: afterwards lane l holds the sum over the lanes of t[l]
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-              const bool up = (lane & o) != 0;
-#pragma unroll
-              for (int q = 0; q < o; ++q) {
-                const float send = up ? t[q] : t[q + o];
-                const float keep = up ? t[q + o] : t[q];
-                t[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-              }
+              for (int q = 0; q < 32; ++q) t[q] = mine ? v[q] : 0.f;
+              const float cs = lane_column_sum(t, lane);
+              if (p0 + lane < n)
+                red_add_s64(Sfix + (p0 + lane) * k + cc, __double2ll_rn((double)cs * fx_scale));
             }
-            if (p0 + lane < n)
-              red_add_s64(Sfix + (p0 + lane) * k + cc, __double2ll_rn((double)t[0] * fx_scale));
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
       }
       if (row_ok) {
 #pragma unroll
@@ -882,10 +945,12 @@ inline int tc2_stream_sym_launch(TcStream &g, const uint16_t *Shi, const uint16_
   const uint32_t idesc = t2_idesc(fp16);
   const int nkb = (int)(dp / TC_BK);
   const float *rs = fp16 ? srscale : nullptr;
-  static bool a4 = false, a8 = false, a16 = false;
+  static bool a4 = false, a8 = false, a12 = false, a16 = false;
   int rc;
   if (k <= 4) rc = t2sym_launch_k<4>(a4, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
   else if (k <= 8) rc = t2sym_launch_k<8>(a8, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  else if (k <= 12)
+    rc = t2sym_launch_k<12>(a12, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
   else rc = t2sym_launch_k<16>(a16, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
   if (rc) return rc;
   if (launches) ++*launches;

@@ -83,7 +83,8 @@ for name in a.configs.split(","):
     mat = h.params.path == kkm.PATH_MATERIALIZE or (
         h.params.path == kkm.PATH_AUTO
         and kkm.workspace_size(h.params, n, Xl.shape[1], rank, world) > 0.3 * kfull)
-    sym = mat and h.params.symmetric == kkm.SYM_AUTO and cfg["k"] <= 16 and a.grid_rows <= 1
+    sym = (mat and cfg["k"] <= 16 and a.grid_rows <= 1 and h.params.symmetric != kkm.SYM_OFF
+           and (h.params.symmetric == kkm.SYM_ON or n >= 8192))  # make_plan's rule
     vals = torch.tensor([init_ms, fit_ms, ph["spmm"], ph["cnorm"], ph["assign"], ph["init_gemm"]],
                         dtype=torch.float64, device=dev)
     if world > 1:
@@ -95,7 +96,9 @@ for name in a.configs.split(","):
         loop_ms = (spmm_ms + cn_ms + as_ms) / it
         out = {"config": name, "n": n, "d": d, "k": cfg["k"], "n_gpus": world,
                "grid": f"{a.grid_rows}x{world // a.grid_rows}", "iterations": it,
-               "path": ("materialised (f1 bands)" if sym else "materialised") if mat else "streaming",
+               "path": (("materialised (f1 bands)" if sym else "materialised") if mat else
+                        ("streaming (f1 upper triangle)" if cfg["k"] <= 16 and a.grid_rows <= 1
+                         else "streaming")),
                "sec_per_iter": loop_ms / 1e3, "total_clustering_s": (init_ms + fit_ms) / 1e3,
                "init_s": init_ms / 1e3, "phases_ms_per_iter": {"a2": spmm_ms / it, "a3": cn_ms / it,
                                                              "a4": as_ms / it},
