@@ -114,7 +114,15 @@ typedef struct kkm_params {
                               n >= 8192 (below, the extra kernels cost more than the
                               halved K read saves). KKM_SYM_ON (2): whenever eligible.
                               KKM_SYM_OFF (1): never.                                 */
-  int32_t reserved[4];     /* must be zero                                         */
+  int32_t incremental;     /* f3 (time to solution). 0: recompute S = K V^T every
+                              iteration (Alg. 1; default). 1: after an iteration in
+                              which m <= n/16 labels changed, update S of the own rows
+                              by the moved points only -- the fused streaming kernel
+                              over them, added with their new and subtracted with
+                              their old label (~4 m n d flops instead of a full pass;
+                              exact up to rounding, S kept in fp64); otherwise a full
+                              pass. 1D and a tensor-core precision only (KKM_EUNSUP). */
+  int32_t reserved[3];     /* must be zero                                         */
 } kkm_params;
 
 typedef struct kkm_ctx *kkm_handle;

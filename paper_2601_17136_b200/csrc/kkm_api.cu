@@ -59,6 +59,9 @@ struct Plan {
   int64_t rows_per_block;
   int64_t s_rows_pad;  // row pitch of the S (or S partials) finalize reads
   bool need_smine;     // a reduce-scatter delivers S of the own 1D block (Smine)
+  // f3 incremental S: moved-point set of at most dmax points
+  bool inc;
+  int64_t dmax, dpad;
   // f1 symmetric storage (sym.cuh): bands of SYM_TB rows, the rank's share spread by area
   bool sym;
   int T, sym_gmax;
@@ -71,7 +74,8 @@ struct Plan {
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, total;
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -89,8 +93,9 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT &&
       p->precision != KKM_PREC_FP16X3)
     return fail(KKM_EINVAL, "unknown precision %d", p->precision);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 3; ++i)
     if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
+  if (p->incremental != 0 && p->incremental != 1) return fail(KKM_EINVAL, "incremental must be 0 or 1");
   if (p->symmetric != KKM_SYM_AUTO && p->symmetric != KKM_SYM_OFF && p->symmetric != KKM_SYM_ON)
     return fail(KKM_EINVAL, "unknown symmetric mode %d", p->symmetric);
   const int pr = p->grid_rows <= 1 ? 1 : p->grid_rows;
@@ -251,6 +256,11 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   }
   if (P.ssym) P.nApad = P.npad;
   P.s_rows_pad = (P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1)) ? P.B : P.nApad;  // == need_smine
+  P.inc = p->incremental == 1;
+  if (P.inc && (P.pr > 1 || !P.tc))
+    return fail(KKM_EUNSUP, "incremental S needs the 1D algorithm and a tensor-core precision");
+  P.dmax = std::max<int64_t>(1, n / 16);
+  P.dpad = round_up(P.dmax, 256);
   P.sort_blocks = (int)ceil_div(std::max<int64_t>(P.nB, 1), SORT_BLOCK);
   P.nspmm_pass = (int)ceil_div(P.k, SP_KPMAX);
   P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.nloc, 1), FIN_THREADS));
@@ -319,6 +329,21 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_Sfmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
     P.o_fxmax = take(16);
   }
+  if (P.inc) {
+    const int64_t nblk = ceil_div(P.n, SORT_BLOCK);
+    P.o_Sinc = take((size_t)P.B * P.k * 8);
+    P.o_dkey = take((size_t)P.lablen * 4);
+    P.o_dperm = take((size_t)P.lablen * 4);
+    P.o_dpos = take((size_t)P.lablen * 4);
+    P.o_dseg = take((size_t)(P.k + 2) * 4);
+    P.o_dbc = take((size_t)nblk * (P.k + 1) * 4);
+    P.o_dbo = take((size_t)nblk * (P.k + 1) * 4);
+    P.o_Dhi = take((size_t)P.dpad * P.dp * 2);
+    P.o_Dlo = take((size_t)P.dpad * P.dp * 2);
+    P.o_Dn = take((size_t)P.dpad * 4);
+    P.o_Dr = take((size_t)P.dpad * 4);
+    P.o_Sd = take((size_t)16 * P.B * P.k * 8);
+  }
   if (P.sym) {
     P.o_perm_b = take((size_t)P.T * SYM_TB * 4);
     P.o_groups = take((size_t)P.T * P.sym_gmax * sizeof(SymGroup));
@@ -335,6 +360,13 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
 }
 
 }  // namespace
+
+// Label-sorted copy of a point set (the B operand of the streaming kernel) and its sort.
+struct SortedSet {
+  uint16_t *hi, *lo;
+  float *norms, *rscale;
+  int32_t *perm, *pos, *seg, *bcount, *boff;
+};
 
 struct kkm_ctx {
   kkm_params p;
@@ -368,6 +400,12 @@ struct kkm_ctx {
   long long *Sfix = nullptr, *Sorig = nullptr, *Sfmine = nullptr;
   float *fxmax = nullptr;
   double fx_scale = 1.0, fx_inv = 1.0;
+  // f3 incremental S
+  double *Sinc = nullptr, *Sd = nullptr;
+  int32_t *dkey = nullptr;
+  SortedSet dset{};
+  bool s_valid = false;  // Sinc holds S of the current labels
+  TcStream ts_delta;
   ncclComm_t colcomm = nullptr;
   int32_t *lab[2], *sizes[2];
   unsigned long long *changed;
@@ -441,13 +479,6 @@ int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
   return KKM_OK;
 }
 
-// Label-sorted copy of a point set (the B operand of the streaming kernel) and its sort.
-struct SortedSet {
-  uint16_t *hi, *lo;
-  float *norms, *rscale;
-  int32_t *perm, *pos, *seg, *bcount, *boff;
-};
-
 // Sorts the points [b0, b0 + nB) of the handle's X by label (stable counting sort) and gathers
 // their split operands, norms and scales in that order into o (rows [nB, rows) zeroed).
 int sort_gather(kkm_ctx *h, const int32_t *labB, int64_t b0, int64_t nB, int64_t rows, const SortedSet &o) {
@@ -479,14 +510,14 @@ struct StreamA {
 // one launch per group of 16 clusters over that group's contiguous sorted rows (same total
 // work; the host reads the k + 1 segment starts first).
 int stream_pass(kkm_ctx *h, TcStream &ts, const StreamA &A, const SortedSet &B, int64_t brows, int64_t nB,
-                int64_t b0, const int32_t *pos, int nsplit, double *Spart) {
+                int64_t b0, const int32_t *pos, int64_t npos, int nsplit, double *Spart) {
   const Plan &P = h->P;
   const int k = P.k;
   if (A.nA == 0) return KKM_OK;
   auto launch = [&](int64_t s0, int64_t nb, int c0, int kg) -> int {
     int rc = tc2_stream_launch(ts, A.hi, A.lo, B.hi + s0 * P.dp, B.lo + s0 * P.dp, P.fp16, A.arows, brows - s0, P.dp,
                                nb, b0, A.row0, A.nA, A.rows_pad, A.norms, A.rscale, B.norms + s0, B.rscale + s0, pos,
-                               nB, B.seg + c0, kg, h->kp, nsplit / 2, Spart, k, c0, h->st, &h->launches);
+                               npos, B.seg + c0, kg, h->kp, nsplit / 2, Spart, k, c0, h->st, &h->launches);
     if (rc) {
       h->poisoned = true;
       return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
@@ -516,7 +547,7 @@ int launch_stream(kkm_ctx *h, const int32_t *labels) {
   const SortedSet B{h->Shi, h->Slo, h->snorms, h->srscale, h->perm, h->pos, h->seg, h->bcount, h->boff};
   CKR(sort_gather(h, labels + P.b0, P.b0, P.nB, P.npad, B));
   const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.a0, P.nA, P.nApad};
-  return stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nsplit, h->Spart);
+  return stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, P.nsplit, h->Spart);
 }
 
 // a2 on the materialised K tile (A set rows x B set columns).
@@ -683,8 +714,8 @@ int launch_spmm(kkm_ctx *h, const int32_t *labels, const double **s_out, int *ns
 
 // a3: E, z, c (cnorm) and J for the labels entering the iteration -> E_out, cnorm_out,
 // J_out. sizes_next / changed_out (may be NULL) are zeroed for the following assign.
-int run_cnorm(kkm_ctx *h, const double *S, int nsplit, double *E_out, double *cnorm_out, double *J_out,
-              int32_t *sizes_next, unsigned long long *changed_out) {
+int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double *E_out, double *cnorm_out,
+              double *J_out, int32_t *sizes_next, unsigned long long *changed_out) {
   const Plan &P = h->P;
   const int32_t *labels = h->lab[h->cur];
   const int32_t *sizes = h->sizes[h->cur];
@@ -693,7 +724,7 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, double *E_out, double *cn
     int fth = FIN_THREADS;  // power of two with (k+1) * fth doubles <= 48 KB
     while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
-        S, nsplit, P.nloc, P.s_rows_pad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
+        S, nsplit, P.nloc, rows_pad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
         E_out, h->blockpart);
     CKL();
   }
@@ -744,6 +775,41 @@ int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, flo
   gemm_simt_kernel<<<grid, 256, 0, h->st>>>(h->Xf, P.ldf, P.n, P.d, i0, m, j0, ncov, h->norms,
                                              h->kp, out, ldo);
   CKL();
+  return KKM_OK;
+}
+
+// f3: S of the own rows for the labels lab[cur ^ 1] from S (Sinc) of lab[cur]: the points
+// that moved, sorted by new label, added; sorted by old label, subtracted (the fused
+// streaming kernel, A = own rows, B = the moved points). m = number of moved points.
+int delta_update(kkm_ctx *h, int64_t m) {
+  const Plan &P = h->P;
+  const int k = P.k;
+  const int32_t *cl_old = h->lab[h->cur], *cl_new = h->lab[h->cur ^ 1];
+  const int nblk = (int)ceil_div(P.n, SORT_BLOCK);
+  const int64_t mpad = round_up(m, 256);
+  const int nsplit = 2 * std::min(8, ts_choose_splits((P.nloc + 1) / 2, m, h->num_sms / 2));
+  const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.row0, P.nloc, P.B};
+  for (int pass = 0; pass < 2; ++pass) {  // 0: + new labels, 1: - old labels
+    moved_key_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(cl_old, cl_new, P.n, P.lablen, k,
+                                                                           pass == 0, h->dkey);
+    CKL();
+    const SortedSet &D = h->dset;
+    sort_count_kernel<<<nblk, 256, (size_t)(k + 1) * 4, h->st>>>(h->dkey, P.n, k + 1, D.bcount);
+    CKL();
+    sort_scan_kernel<<<k + 2, 1024, 1024 * 4, h->st>>>(D.bcount, nblk, k + 1, D.boff, D.seg);
+    CKL();
+    sort_scatter_kernel<<<nblk, 256, (size_t)9 * (k + 1) * 4, h->st>>>(h->dkey, P.n, k + 1, D.boff, D.perm, D.pos);
+    CKL();
+    gather_rows_kernel<<<(unsigned)ceil_div(mpad, 8), 256, 0, h->st>>>(h->Xhi, h->Xlo, h->norms, h->rscale, D.perm, 0,
+                                                                       m, mpad, P.dp, D.hi, D.lo, D.norms, D.rscale);
+    CKL();
+    // B = the m moved points (clusters 0..k-1 of the k+1 buckets); pos: sorted position of
+    // each point (>= m for the points that did not move) for the Gaussian diagonal
+    CKR(stream_pass(h, h->ts_delta, A, D, mpad, m, 0, D.pos, P.n, nsplit, h->Sd));
+    sinc_add_kernel<<<(unsigned)ceil_div(P.nloc * k, 256), 256, 0, h->st>>>(h->Sd, nsplit, P.B, P.nloc, k,
+                                                                            pass == 0 ? 1.0 : -1.0, h->Sinc);
+    CKL();
+  }
   return KKM_OK;
 }
 
@@ -853,6 +919,14 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->Scol = (double *)(w + P.o_Scol);
   }
   if (P.need_smine) h->Smine = (double *)(w + P.o_Smine);
+  if (P.inc) {
+    h->Sinc = (double *)(w + P.o_Sinc);
+    h->Sd = (double *)(w + P.o_Sd);
+    h->dkey = (int32_t *)(w + P.o_dkey);
+    h->dset = SortedSet{(uint16_t *)(w + P.o_Dhi), (uint16_t *)(w + P.o_Dlo), (float *)(w + P.o_Dn),
+                        (float *)(w + P.o_Dr),      (int32_t *)(w + P.o_dperm), (int32_t *)(w + P.o_dpos),
+                        (int32_t *)(w + P.o_dseg),  (int32_t *)(w + P.o_dbc),   (int32_t *)(w + P.o_dbo)};
+  }
   if (P.ssym) {
     h->units = (int4 *)(w + P.o_units);
     h->Sfix = (long long *)(w + P.o_Sfix);
@@ -1013,30 +1087,58 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
     if (timing) CKR(rec(ev));
     const double *S = nullptr;
     int ns = 0;
-    CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));                         // a2 (+ 1.5D reduce-scatter)
+    int64_t rows_pad = P.s_rows_pad;
+    if (P.inc && h->s_valid) {  // f3: S of the current labels maintained incrementally
+      S = h->Sinc;
+      ns = 1;
+      rows_pad = P.B;
+    } else {
+      CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));  // a2 (+ 1.5D reduce-scatter)
+      if (P.inc && P.nloc > 0) {
+        sinc_set_kernel<<<(unsigned)ceil_div(P.nloc * P.k, 256), 256, 0, h->st>>>(S, ns, rows_pad, P.nloc, P.k,
+                                                                                   h->Sinc);
+        CKL();
+      }
+    }
     if (timing) CKR(rec(ev));
-    CKR(run_cnorm(h, S, ns, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
+    CKR(run_cnorm(h, S, ns, rows_pad, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
     if (timing) CKR(rec(ev));
     CKR(run_assign(h, h->changed + t));                                   // a4
     if (timing) CKR(rec(ev));
-    h->cur ^= 1;
-    h->have_last = true;
-    if (h->p.stop_on_no_change) {
-      unsigned long long c = 0;
+    unsigned long long c = 1;
+    if (h->p.stop_on_no_change || P.inc) {
       CK(cudaMemcpyAsync(&c, h->changed + t, 8, cudaMemcpyDeviceToHost, h->st));
       CK(cudaStreamSynchronize(h->st));
-      if (c == 0) {
-        ++t;
-        break;
+    }
+    if (P.inc) {  // S for the new labels: unchanged, by the moved points, or a full pass next time
+      if (c > 0 && (int64_t)c <= P.dmax) {
+        CKR(delta_update(h, (int64_t)c));
+        h->s_valid = true;
+      } else {
+        h->s_valid = c == 0;
       }
+    }
+    if (timing) CKR(rec(ev));
+    h->cur ^= 1;
+    h->have_last = true;
+    if (h->p.stop_on_no_change && c == 0) {
+      ++t;
+      break;
     }
   }
   // J of the final labels (one more a2 + a3 pass, as the oracle's J_trace[iters])
   {
     const double *S = nullptr;
     int ns = 0;
-    CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
-    CKR(run_cnorm(h, S, ns, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
+    int64_t rows_pad = P.s_rows_pad;
+    if (P.inc && h->s_valid) {
+      S = h->Sinc;
+      ns = 1;
+      rows_pad = P.B;
+    } else {
+      CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
+    }
+    CKR(run_cnorm(h, S, ns, rows_pad, h->E2, h->cnorm2, h->J + t, nullptr, nullptr));
     h->cnorm2_valid = true;
   }
   std::vector<double> J((size_t)t + 1);
@@ -1045,12 +1147,13 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (timing) {
-    for (size_t i = 0; i + 3 < ev.size(); i += 4) {
-      float a, b, c;
+    for (size_t i = 0; i + 4 < ev.size(); i += 5) {  // the a2 phase includes the f3 S update
+      float a, b, c, d;
       CK(cudaEventElapsedTime(&a, ev[i], ev[i + 1]));
       CK(cudaEventElapsedTime(&b, ev[i + 1], ev[i + 2]));
       CK(cudaEventElapsedTime(&c, ev[i + 2], ev[i + 3]));
-      h->phase_ms[KKM_PH_SPMM] += a;
+      CK(cudaEventElapsedTime(&d, ev[i + 3], ev[i + 4]));
+      h->phase_ms[KKM_PH_SPMM] += a + d;
       h->phase_ms[KKM_PH_CNORM] += b;
       h->phase_ms[KKM_PH_ASSIGN] += c;
     }
@@ -1079,7 +1182,7 @@ int kkm_objective(kkm_handle h, double *J) {
   const double *S = nullptr;
   int ns = 0;
   CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));
-  CKR(run_cnorm(h, S, ns, h->E2, h->cnorm2, slot, nullptr, nullptr));
+  CKR(run_cnorm(h, S, ns, h->P.s_rows_pad, h->E2, h->cnorm2, slot, nullptr, nullptr));
   h->cnorm2_valid = true;
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -1106,6 +1209,7 @@ int kkm_set_labels(kkm_handle h, const int32_t *labels) {
   CK(cudaStreamSynchronize(h->st));
   h->have_last = false;
   h->cnorm2_valid = false;
+  h->s_valid = false;
   if (bad) return fail(KKM_ELABEL, "%d labels outside [0, %d)", bad, P.k);
   return KKM_OK;
 }
@@ -1187,7 +1291,7 @@ int predict_run(kkm_ctx *h, const PredictPlan &q, uint8_t *t, const float *Y, in
   CKR(sort_gather(h, h->lab[h->cur], 0, P.n, P.npad, B));
   TcStream &ts = h->ts_predict;
   const StreamA A{Yhi, Ylo, yn, yr, q.mpad, 0, m, q.mpad};
-  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, q.nsplit, Sp));
+  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, 0, q.nsplit, Sp));
   predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, q.nsplit, m, q.mpad, k, h->sizes[h->cur],
                                                                 h->cnorm2, yd, ylab, Dy);
   CKL();

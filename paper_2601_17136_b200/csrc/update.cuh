@@ -147,3 +147,43 @@ __global__ void predict_kernel(const double *__restrict__ Spart, int nsplit, int
 }
 
 }  // namespace kkm
+
+namespace kkm {
+
+// ---- f3: incremental S (kkm_params.incremental)
+// S1[i][c] = sum_s S[(s * rows_pad + i) * k + c] (fixed order) for the own rows i < nrows.
+__global__ void sinc_set_kernel(const double *__restrict__ S, int nsplit, int64_t rows_pad, int64_t nrows, int k,
+                                double *__restrict__ S1) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows * k) return;
+  const int64_t i = t / k;
+  const int c = (int)(t % k);
+  double s = 0.0;
+  for (int p = 0; p < nsplit; ++p) s += S[((int64_t)p * rows_pad + i) * k + c];
+  S1[t] = s;
+}
+
+// S1[i][c] += sign * sum_s Sd[s][i][c] (fixed order) for the own rows i < nrows.
+__global__ void sinc_add_kernel(const double *__restrict__ Sd, int nsplit, int64_t rows_pad, int64_t nrows, int k,
+                                double sign, double *__restrict__ S1) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows * k) return;
+  const int64_t i = t / k;
+  const int c = (int)(t % k);
+  double s = 0.0;
+  for (int p = 0; p < nsplit; ++p) s += Sd[((int64_t)p * rows_pad + i) * k + c];
+  S1[t] += sign * s;
+}
+
+// Sort key of the moved points: key[i] = new (or old) label if cl_old[i] != cl_new[i], else k
+// (the bucket after the last cluster: not moved); -1 beyond n.
+__global__ void moved_key_kernel(const int32_t *__restrict__ cl_old, const int32_t *__restrict__ cl_new, int64_t n,
+                                 int64_t len, int k, int use_new, int32_t *__restrict__ key) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  int32_t v = -1;
+  if (i < n) v = cl_old[i] != cl_new[i] ? (use_new ? cl_new[i] : cl_old[i]) : k;
+  key[i] = v;
+}
+
+}  // namespace kkm

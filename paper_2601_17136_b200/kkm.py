@@ -34,7 +34,7 @@ class KKMParams(ctypes.Structure):
                 ("stop_on_no_change", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("timing", ctypes.c_int32),
                 ("grid_rows", ctypes.c_int32), ("symmetric", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("incremental", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 _lib = None
@@ -141,7 +141,7 @@ class KernelKMeans:
                  stop_on_no_change: bool = False, path: int = PATH_AUTO,
                  precision: int = PREC_FP16X3, timing: bool = False, init_labels=None,
                  rank: int = 0, nranks: int = 1, comm=None, stream=None, device=None,
-                 workspace=None, grid_rows: int = 1, symmetric: int = SYM_AUTO):
+                 workspace=None, grid_rows: int = 1, symmetric: int = SYM_AUTO, incremental: bool = False):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
@@ -155,6 +155,7 @@ class KernelKMeans:
         p.path, p.precision, p.timing = path, precision, int(timing)
         p.grid_rows = grid_rows
         p.symmetric = symmetric
+        p.incremental = int(incremental)
         self.params = p
         self.max_iter = max_iter
         nb = workspace_size(p, self.n, self.d, rank, nranks)

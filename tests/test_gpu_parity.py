@@ -279,3 +279,29 @@ def test_bf16x3_rings_limit():
     h = _handle(X, 2, *args, 1, kkm.PREC_BF16X3)
     diag = oracle.kernel_diag(X, *args)
     check_kernel_values(h.kernel_tile(0, 0, 1000, 1000), oracle.kernel_matrix(X, *args), diag, diag)
+
+
+@pytest.mark.parametrize("mode", [(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE), (kkm.PREC_FP16X3, kkm.PATH_STREAM),
+                                  (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON)],
+                         ids=["mat", "stream", "sym"])
+@pytest.mark.parametrize("name,n,k", [("mnist60k", 3000, 10), ("har200k", 2500, 6), ("mnist60k", 2000, 21)])
+def test_incremental_matches_full(mode, name, n, k):
+    """f3: S maintained by the moved points (kkm_params.incremental) gives the same label trace
+    as the full recompute, and its J trace agrees with the oracle's."""
+    X, cfg = synth.make_config(name, n=n)
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    iters = 25
+    a = _handle(X, k, *args, iters, mode)
+    b = _handle(X, k, *args, iters, mode, incremental=True)
+    ia, Ja, ca = a.fit()
+    ib, Jb, cb = b.fit()
+    assert ia == ib and np.array_equal(ca, cb)
+    assert np.array_equal(a.assign().cpu().numpy(), b.assign().cpu().numpy())
+    assert np.allclose(Ja, Jb, rtol=1e-6, atol=0)
+    assert (cb[1:] <= n // 16).any()  # the delta path was exercised
+    ref = oracle.fit(X, k, *args, max_iter=iters)
+    tol = max(1e-5 * abs(ref["J_trace"][-1]), 1e-7 * float(np.abs(ref["diag"]).sum()))
+    assert abs(Jb[-1] - ref["J_trace"][-1]) <= tol
+    # a second fit call continues from the maintained S
+    i2, J2, c2 = b.fit()
+    assert np.isfinite(J2).all()
