@@ -216,6 +216,18 @@ int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *l
  * + n*4*dp for materialising handles; ld = d rounded up to 4, dp = d rounded up to 64). */
 int kkm_predict_workspace_size(kkm_handle h, int64_t m, size_t *bytes);
 
+/* K-means++ seeding in feature space (the paper's P:567 leaves it as
+ * future work): c_0 = floor(u[0] n); then c_t = the smallest index i whose running sum of
+ * D = min_{s<t} ||phi(x) - phi(c_s)||^2 = K(x,x) - 2 K(x,c_s) + K(c_s,c_s) exceeds u[t] * sum D
+ * (D^2 sampling; the previous center again if every D is 0). Distances are evaluated in fp64
+ * from the fp32 points. The labels become the lowest-index nearest center of every point
+ * (as kkm_set_labels: replaces the current labels).
+ *   u:           host, k uniforms in [0, 1) -- the random draws are the caller's.
+ *   centers_out: host or device, k int64 point indices (out), or NULL.
+ * Every rank computes the same result locally (X is replicated); no communication.
+ * Temporary device memory ~12 n bytes (stream-ordered). Synchronises the stream. */
+int kkm_seed_kmeanspp(kkm_handle h, const double *u, int64_t *centers_out);
+
 /* Copies an internal array of the last iteration (selectors KKM_DBG_*) to dst
  * (host or device). Synchronises. Test hook. */
 int kkm_debug_read(kkm_handle h, int32_t what, void *dst);

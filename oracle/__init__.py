@@ -50,6 +50,7 @@ def lib():
             "orc_assign": [P, P, P, i64, i32, P, P],
             "orc_fit": [P, P, i64, i32, i32, i32, P, P, P, P, P],
             "orc_predict": [P, i64, P, i64, i64, P, i32, P, ctypes.c_int, f64, f64, ctypes.c_int, P, P],
+            "orc_kmeanspp": [P, i64, i64, i32, ctypes.c_int, f64, f64, ctypes.c_int, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -216,3 +217,15 @@ def predict(X, labels, k, cn, Y, kind, gamma=1.0, coef0=0.0, degree=1):
     _check(lib().orc_predict(_p(X), X.shape[0], _p(Y), m, X.shape[1], _p(labels), k, _p(cn), kind,
                              gamma, coef0, degree, _p(out), _p(D)), "predict")
     return out, D
+
+
+def kmeanspp(X, k, u, kind, gamma=1.0, coef0=0.0, degree=1):
+    """K-means++ seeding in feature space with the caller's uniforms u[0..k-1].
+    Returns (centers int64[k], labels int32[n])."""
+    X = _X(X)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    centers = np.empty(k, dtype=np.int64)
+    labels = np.empty(X.shape[0], dtype=np.int32)
+    _check(lib().orc_kmeanspp(_p(X), X.shape[0], X.shape[1], k, kind, gamma, coef0, degree, _p(u),
+                              _p(centers), _p(labels)), "kmeanspp")
+    return centers, labels

@@ -319,3 +319,61 @@ int orc_predict(const float *X, int64_t n, const float *Y, int64_t m, int64_t d,
   free(sizes);
   return ORC_OK;
 }
+
+/* K-means++ seeding in feature space ("K-means++ ... future work";
+ * Arthur & Vassilvitskii's D^2 sampling with ||phi(x) - phi(c)||^2 = K(x,x) - 2 K(x,c) + K(c,c)).
+ * u[0..k-1]: uniforms in [0,1) supplied by the caller (the random draws are inputs).
+ *   c_0 = floor(u[0] * n);
+ *   for t = 1..k-1: D(x) = min_{s<t} dist(x, c_s); c_t = the smallest index i with
+ *     sum_{j<=i} D(j) > u[t] * sum_j D(j)   (inverse CDF, sums in index order, fp64);
+ *     if every D is 0 (fewer than t distinct points), c_t = c_{t-1}.
+ *   labels(x) = the lowest s attaining min_s dist(x, c_s) (A6).
+ * centers: k int64 out; labels: n int32 out. */
+int orc_kmeanspp(const float *X, int64_t n, int64_t d, int32_t k, int kind, double gamma, double coef0, int degree,
+                 const double *u, int64_t *centers, int32_t *labels) {
+  if (n < 1 || d < 1 || k < 1 || k > n || check_kernel(kind, gamma, degree)) return ORC_EINVAL;
+  double *D = (double *)malloc(sizeof(double) * (size_t)n);
+  if (!D) return ORC_ENOMEM;
+  int64_t c = (int64_t)(u[0] * (double)n);
+  if (c >= n) c = n - 1;
+  centers[0] = c;
+  for (int32_t t = 0; t < k; ++t) {
+    const float *xc = X + centers[t] * d;
+    const double kcc = orc_kappa(xc, xc, d, kind, gamma, coef0, degree);
+    for (int64_t i = 0; i < n; ++i) {
+      const float *xi = X + i * d;
+      const double dist = orc_kappa(xi, xi, d, kind, gamma, coef0, degree) -
+                          2.0 * orc_kappa(xi, xc, d, kind, gamma, coef0, degree) + kcc;
+      if (t == 0 || dist < D[i]) {
+        D[i] = dist;
+        labels[i] = t;
+      }
+    }
+    if (t + 1 == k) break;
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) total += D[i] > 0.0 ? D[i] : 0.0;
+    int64_t pick = centers[t];
+    if (total > 0.0) {
+      const double target = u[t + 1] * total;
+      double run = 0.0;
+      pick = -1;
+      for (int64_t i = 0; i < n; ++i) {
+        run += D[i] > 0.0 ? D[i] : 0.0;
+        if (run > target) {
+          pick = i;
+          break;
+        }
+      }
+      if (pick < 0) {  /* rounding at the top end: the last point with D > 0 */
+        for (int64_t i = n - 1; i >= 0; --i)
+          if (D[i] > 0.0) {
+            pick = i;
+            break;
+          }
+      }
+    }
+    centers[t + 1] = pick;
+  }
+  free(D);
+  return ORC_OK;
+}

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
+#include "kpp.cuh"
 #include "prep.cuh"
 #include "sort.cuh"
 #include "spmm.cuh"
@@ -153,8 +154,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       b.koff = koff;
       b.cpoff = cpoff;
       b.csoff = csoff;
-      const int64_t chunks = ceil_div(ldb, 2048);  // spmm_sym chunk width (SpRows::CH)
-      b.nsplit = (int32_t)ceil_div(chunks, SP_MAX_CHUNKS_PER_SPLIT * 1024 / 2048);
+      const int64_t chunks = ceil_div(ldb, SYM_CH);  // spmm_sym chunk width
+      b.nsplit = (int32_t)ceil_div(chunks, SP_MAX_CHUNKS_PER_SPLIT * 1024 / SYM_CH);  // <= ~1024 fp32 terms per lane
       b.cps = (int32_t)ceil_div(chunks, b.nsplit);
       b.item0 = P.sym_items;
       P.sym_items += (int64_t)P.sym_gmax * b.nsplit;
@@ -1341,6 +1342,45 @@ int kkm_predict(kkm_handle h, const float *Y, int64_t m, int64_t ldy, int32_t *l
   const int rc = predict_run(h, q, t, Y, m, ldy, labels_out, D_out);
   cudaFreeAsync(t, h->st);
   if (rc == KKM_OK) CK(cudaStreamSynchronize(h->st));
+  return rc;
+}
+
+int kkm_seed_kmeanspp(kkm_handle h, const double *u, int64_t *centers_out) {
+  if (!h || !u) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  const Plan &P = h->P;
+  const int k = P.k;
+  for (int t = 0; t < k; ++t)
+    if (!(u[t] >= 0.0 && u[t] < 1.0)) return fail(KKM_EINVAL, "u[%d] = %g outside [0, 1)", t, u[t]);
+  int64_t c0 = (int64_t)(u[0] * (double)P.n);
+  if (c0 >= P.n) c0 = P.n - 1;
+  uint8_t *t0 = nullptr;
+  const size_t oD = 0, oL = round_up((int64_t)P.n * 8, 256), oC = oL + round_up((int64_t)P.n * 4, 256),
+               total = oC + round_up((int64_t)k * 8, 256);
+  if (cudaMallocAsync((void **)&t0, total, h->st) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KKM_ENOMEM, "kkm_seed_kmeanspp: cannot allocate %zu temporary bytes", total);
+  }
+  double *D = (double *)(t0 + oD);
+  int32_t *lab = (int32_t *)(t0 + oL);
+  int64_t *cen = (int64_t *)(t0 + oC);
+  int rc = [&]() -> int {
+    CK(cudaMemcpyAsync(cen, &c0, 8, cudaMemcpyHostToDevice, h->st));
+    for (int t = 0; t < k; ++t) {
+      kpp_dist_kernel<<<(unsigned)ceil_div(P.n, 8), 256, 0, h->st>>>(h->Xf, P.ldf, P.n, P.d, cen, t, h->p.kind,
+                                                                      h->p.gamma, h->p.coef0, h->p.degree, D, lab);
+      CKL();
+      if (t + 1 < k) {
+        kpp_pick_kernel<<<1, 1024, 0, h->st>>>(D, P.n, u[t + 1], t, cen);
+        CKL();
+      }
+    }
+    if (centers_out) CKR(copy_any(h, centers_out, cen, (size_t)k * 8));
+    CK(cudaStreamSynchronize(h->st));
+    return kkm_set_labels(h, lab);  // validates, sets sizes, invalidates the derived state
+  }();
+  cudaFreeAsync(t0, h->st);
+  cudaStreamSynchronize(h->st);
   return rc;
 }
 

@@ -64,6 +64,7 @@ def lib():
             "kkm_set_labels": [P, P],
             "kkm_predict": [P, P, i64, i64, P, P, P, ctypes.c_size_t],
             "kkm_predict_workspace_size": [P, i64, P],
+            "kkm_seed_kmeanspp": [P, P, P],
             "kkm_debug_read": [P, i32, P],
             "kkm_kernel_tile": [P, i64, i64, i32, i32, P],
             "kkm_phase_ms": [P, P],
@@ -197,6 +198,18 @@ class KernelKMeans:
         if isinstance(labels, np.ndarray):
             labels = np.ascontiguousarray(labels, dtype=np.int32)
         _check(lib().kkm_set_labels(self.h, _ptr(labels)))
+
+    def seed_kmeanspp(self, seed: int = 0, u=None) -> np.ndarray:
+        """K-means++ seeding in feature space (kkm_seed_kmeanspp); replaces the current labels.
+        u: the k uniforms in [0, 1) (default: numpy's generator seeded with `seed`). Returns the
+        k center indices."""
+        u = np.random.default_rng(seed).random(self.k) if u is None else u
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.shape != (self.k,):
+            raise ValueError(f"u must hold k = {self.k} uniforms")
+        centers = np.empty(self.k, dtype=np.int64)
+        _check(lib().kkm_seed_kmeanspp(self.h, _ptr(u), _ptr(centers)))
+        return centers
 
     def predict(self, Y, return_distances: bool = False, use_workspace: bool = True):
         """Out-of-sample assignment of the rows of Y (host numpy or device tensor, m x d fp32)

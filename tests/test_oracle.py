@@ -353,3 +353,47 @@ def test_predict_empty_cluster_and_gaussian():
         m = lab == c
         ref = 1.0 - 2.0 * Ky[:, m].mean(axis=1) + K[np.ix_(m, m)].sum() / m.sum() ** 2
         assert np.allclose(D[:, c], ref, rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- f3: K-means++ seeding
+def _kpp_numpy(F, k, u):
+    """Textbook k-means++ (Arthur & Vassilvitskii) on explicit features F with the given
+    uniforms: inverse CDF by numpy cumsum + searchsorted."""
+    n = F.shape[0]
+    cen = [min(int(u[0] * n), n - 1)]
+    D = ((F - F[cen[0]]) ** 2).sum(axis=1)
+    for t in range(1, k):
+        Dp = np.maximum(D, 0.0)
+        cdf = np.cumsum(Dp)
+        cen.append(int(np.searchsorted(cdf, u[t] * cdf[-1], side="right")) if cdf[-1] > 0 else cen[-1])
+        D = np.minimum(D, ((F - F[cen[-1]]) ** 2).sum(axis=1))
+    dist = np.stack([((F - F[c]) ** 2).sum(axis=1) for c in cen], axis=1)
+    return np.array(cen), dist.argmin(axis=1)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_kmeanspp_linear_is_textbook(seed):
+    X = synth.blobs(300, 4, 6, seed=70 + seed, sep=3.0)
+    u = np.random.default_rng(seed).random(6)
+    c, lab = oracle.kmeanspp(X, 6, u, oracle.LINEAR)
+    c_ref, lab_ref = _kpp_numpy(X.astype(np.float64), 6, u)
+    assert np.array_equal(c, c_ref)
+    assert np.array_equal(lab, lab_ref)
+
+
+def test_kmeanspp_poly2_feature_map_and_special_cases():
+    X = synth.rings(200, seed=11)
+    u = np.random.default_rng(5).random(4)
+    c, lab = oracle.kmeanspp(X, 4, u, oracle.POLY, 0.8, 1.3, 2)
+    c_ref, lab_ref = _kpp_numpy(feature_map_poly2(X, 0.8, 1.3), 4, u)
+    assert np.array_equal(c, c_ref) and np.array_equal(lab, lab_ref)
+    # k = 1: the first draw picks the center, every point in cluster 0
+    c1, l1 = oracle.kmeanspp(X, 1, [0.5], oracle.GAUSSIAN, 0.7)
+    assert c1.tolist() == [100] and (l1 == 0).all()
+    # each center is its own nearest center (distance 0) and centers are distinct while D > 0
+    assert len(set(c.tolist())) == 4 and all(lab[ci] == t for t, ci in enumerate(c))
+    # duplicate points: D = 0 points are never drawn; with all points equal, centers repeat
+    Xd = np.repeat(X[:3], 5, axis=0)
+    cd, ld = oracle.kmeanspp(Xd, 5, np.random.default_rng(1).random(5), oracle.GAUSSIAN, 0.7)
+    assert len(set(map(tuple, Xd[cd[:3]]))) == 3
+    assert (cd[3:] == cd[2]).all()

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+make -B > /dev/null 2>&1 || exit 1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "symmetric or sym or config2" 2>&1 | tail -1
+for i in 1 2; do timeout 300 python tools/profile_run.py --config mnist60k --iters 10 2>&1 | tail -1; done
+timeout 300 python tools/profile_run.py --config har200k --iters 5 2>&1 | tail -1
