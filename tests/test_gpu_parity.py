@@ -305,3 +305,24 @@ def test_incremental_matches_full(mode, name, n, k):
     # a second fit call continues from the maintained S
     i2, J2, c2 = b.fit()
     assert np.isfinite(J2).all()
+
+
+@pytest.mark.parametrize("name,iters", [("rings", 30), ("mnist60k", 100), ("har200k", 30)])
+def test_full_size_objective_at_convergence(name, iters):
+    """north_star: "final objective within 1e-5 relative" -- at the configs' full sizes, run to
+    convergence on the tensor-core path (the bench configuration) and evaluate J of the final
+    labels on the fp32 CUDA-core path, which has no systematic accumulation bias (DESIGN A9)."""
+    X, cfg = synth.make_config(name)
+    n, k = X.shape[0], cfg["k"]
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    Xd = torch.from_numpy(X).cuda()
+    h = kkm.KernelKMeans(Xd, n, k, *args, max_iter=iters)
+    h.fit()
+    lab = h.assign().cpu().numpy()
+    J = h.objective()
+    h.destroy()
+    torch.cuda.empty_cache()
+    hs = kkm.KernelKMeans(Xd, n, k, *args, max_iter=1, precision=kkm.PREC_FP32_SIMT, init_labels=lab)
+    Jref = hs.objective()
+    hs.destroy()
+    assert abs(J - Jref) <= 1e-5 * abs(Jref), (J, Jref)
