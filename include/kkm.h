@@ -188,7 +188,8 @@ int kkm_assign(kkm_handle h, int32_t *labels_out);
 int kkm_objective(kkm_handle h, double *J);
 
 /* Replaces the current labels (n int32 in [0,k), host or device, identical on
- * every rank): used for teacher-forced parity and for resuming. */
+ * every rank): used for teacher-forced parity and for resuming. KKM_ELABEL if any
+ * label is outside [0, k); the handle then keeps its current labels. */
 int kkm_set_labels(kkm_handle h, const int32_t *labels);
 
 /* Out-of-sample assignment: assigns m new points y to the

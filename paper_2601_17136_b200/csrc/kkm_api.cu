@@ -62,6 +62,7 @@ struct Plan {
   bool need_smine;     // a reduce-scatter delivers S of the own 1D block (Smine)
   // f3 incremental S: moved-point set of at most dmax points
   bool inc;
+  bool fused;  // a3 + a4 as one single-CTA kernel (one rank, small n, k <= 16)
   int64_t dmax, dpad;
   // f1 symmetric storage (sym.cuh): bands of SYM_TB rows, the rank's share spread by area
   bool sym;
@@ -258,6 +259,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (P.ssym) P.nApad = P.npad;
   P.s_rows_pad = (P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1)) ? P.B : P.nApad;  // == need_smine
   P.inc = p->incremental == 1;
+  P.fused = nranks == 1 && n <= FUSED_MAX_ROWS && P.k <= 16;
   if (P.inc && (P.pr > 1 || !P.tc))
     return fail(KKM_EUNSUP, "incremental S needs the 1D algorithm and a tensor-core precision");
   P.dmax = std::max<int64_t>(1, n / 16);
@@ -955,6 +957,14 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   h->kp.neg_gamma_log2e = (float)(-p->gamma * 1.4426950408889634);
 
   int rc = [&]() -> int {
+    if (P.fused) {
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(fused_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(17 * FUSED_THREADS * 8 + 16 * 8)));
+        attr = true;
+      }
+    }
     cudaEvent_t e0, e1, e2;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1102,9 +1112,17 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
       }
     }
     if (timing) CKR(rec(ev));
-    CKR(run_cnorm(h, S, ns, rows_pad, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
-    if (timing) CKR(rec(ev));
-    CKR(run_assign(h, h->changed + t));                                   // a4
+    if (P.fused) {  // a3 + a4 in one launch (the phase split is reported as a3)
+      fused_update_kernel<<<1, FUSED_THREADS, (size_t)(P.k + 1) * FUSED_THREADS * 8 + P.k * 8, h->st>>>(
+          S, ns, P.n, rows_pad, P.k, h->sizes[h->cur], h->lab[h->cur], h->diag, h->E, h->cnorm, h->J + t, 1,
+          h->lab[h->cur ^ 1], h->sizes[h->cur ^ 1], h->changed + t, h->Dfull);
+      CKL();
+      if (timing) CKR(rec(ev));
+    } else {
+      CKR(run_cnorm(h, S, ns, rows_pad, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
+      if (timing) CKR(rec(ev));
+      CKR(run_assign(h, h->changed + t));                                   // a4
+    }
     if (timing) CKR(rec(ev));
     unsigned long long c = 1;
     if (h->p.stop_on_no_change || P.inc) {
@@ -1194,24 +1212,30 @@ int kkm_set_labels(kkm_handle h, const int32_t *labels) {
   if (!h || !labels) return fail(KKM_EINVAL, "NULL argument");
   if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
   const Plan &P = h->P;
+  // validated in the scratch buffer first: a rejected call leaves the current labels untouched
   int32_t *dst = h->lab[h->cur], *tmp = h->lab[h->cur ^ 1];
   CK(cudaMemsetAsync(h->bad, 0, 4, h->st));
   CK(cudaMemcpyAsync(tmp, labels, (size_t)P.n * 4, cudaMemcpyDefault, h->st));
-  load_labels_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, dst, P.n, P.lablen, P.k, h->bad);
-  CKL();
-  round_robin_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, P.n, P.lablen, P.k);
-  CKL();
-  CK(cudaMemsetAsync(h->sizes[h->cur], 0, (size_t)P.k * 4, h->st));
-  histogram_kernel<<<std::min<int64_t>(ceil_div(P.n, 256), 1024), 256, (size_t)P.k * 4, h->st>>>(
-      dst, P.n, P.k, h->sizes[h->cur]);
+  check_labels_kernel<<<(unsigned)ceil_div(P.n, 256), 256, 0, h->st>>>(tmp, P.n, P.k, h->bad);
   CKL();
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, h->bad, 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  if (!bad) {
+    load_labels_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, dst, P.n, P.lablen, P.k, h->bad);
+    CKL();
+    CK(cudaMemsetAsync(h->sizes[h->cur], 0, (size_t)P.k * 4, h->st));
+    histogram_kernel<<<std::min<int64_t>(ceil_div(P.n, 256), 1024), 256, (size_t)P.k * 4, h->st>>>(
+        dst, P.n, P.k, h->sizes[h->cur]);
+    CKL();
+  }
+  round_robin_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(tmp, P.n, P.lablen, P.k);
+  CKL();
+  CK(cudaStreamSynchronize(h->st));
+  if (bad) return fail(KKM_ELABEL, "%d labels outside [0, %d); current labels kept", bad, P.k);
   h->have_last = false;
   h->cnorm2_valid = false;
   h->s_valid = false;
-  if (bad) return fail(KKM_ELABEL, "%d labels outside [0, %d)", bad, P.k);
   return KKM_OK;
 }
 

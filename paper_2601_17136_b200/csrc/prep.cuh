@@ -112,6 +112,15 @@ __global__ void load_labels_kernel(const int32_t *__restrict__ src, int32_t *__r
   }
 }
 
+// *bad += #{j < n : labels[j] outside [0, k)} (validation before anything is replaced).
+__global__ void check_labels_kernel(const int32_t *__restrict__ labels, int64_t n, int k, int *__restrict__ bad) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    const int32_t v = labels[j];
+    if (v < 0 || v >= k) atomicAdd(bad, 1);
+  }
+}
+
 // sizes[c] = |L_c| over labels[0, n) (exact integer histogram).
 __global__ void histogram_kernel(const int32_t *__restrict__ labels, int64_t n, int k,
                                  int32_t *__restrict__ sizes) {

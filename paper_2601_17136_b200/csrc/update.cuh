@@ -187,3 +187,81 @@ __global__ void moved_key_kernel(const int32_t *__restrict__ cl_old, const int32
 }
 
 }  // namespace kkm
+
+namespace kkm {
+
+// ---- a3 + a4 in one CTA (single rank, n <= FUSED_MAX_ROWS, k <= 16): the launch-latency bound
+// regime (config 1). Same arithmetic as finalize / cnorm_* / assign (fixed-order sums: thread
+// partials over rows t, t + T, ..., then a fixed tree; exact integer histogram), one launch
+// instead of four. Writes E, cnorm, *J_out; with do_assign also Dfull, the new labels,
+// sizes_next (stored, not accumulated) and *changed_out.
+constexpr int FUSED_THREADS = 512;
+constexpr int64_t FUSED_MAX_ROWS = 32768;
+
+__global__ void __launch_bounds__(FUSED_THREADS) fused_update_kernel(
+    const double *__restrict__ S, int nsplit, int64_t n, int64_t rows_pad, int k, const int32_t *__restrict__ sizes,
+    const int32_t *__restrict__ cl, const double *__restrict__ diag, double *__restrict__ E,
+    double *__restrict__ cnorm, double *__restrict__ J_out, int do_assign, int32_t *__restrict__ cl_new,
+    int32_t *__restrict__ sizes_next, unsigned long long *__restrict__ changed_out, double *__restrict__ Dfull) {
+  extern __shared__ double sacc[];  // [(k + 1)][T], then cn[k]
+  __shared__ int hist[16];
+  __shared__ unsigned long long nchg;
+  const int T = blockDim.x, t = threadIdx.x;
+  double *cn = sacc + (size_t)(k + 1) * T;
+  for (int c = 0; c <= k; ++c) sacc[c * T + t] = 0.0;
+  if (t < 16) hist[t] = 0;
+  if (t == 0) nchg = 0ull;
+  for (int64_t i = t; i < n; i += T) {
+    const int li = cl[i];
+    double zi = 0.0;
+    for (int c = 0; c < k; ++c) {
+      double s = 0.0;
+      for (int p = 0; p < nsplit; ++p) s += S[((int64_t)p * rows_pad + i) * k + c];
+      const int32_t sz = sizes[c];
+      const double e = sz > 0 ? s / (double)sz : 0.0;
+      E[i * k + c] = e;
+      if (c == li) zi = e;
+    }
+    sacc[li * T + t] += zi;
+    sacc[k * T + t] += diag[i] - zi;
+  }
+  __syncthreads();
+  for (int w = T / 2; w > 0; w >>= 1) {
+    if (t < w)
+      for (int c = 0; c <= k; ++c) sacc[c * T + t] += sacc[c * T + t + w];
+    __syncthreads();
+  }
+  if (t < k) {
+    const int32_t sz = sizes[t];
+    const double v = sz > 0 ? sacc[t * T] / (double)sz : __longlong_as_double(0x7ff0000000000000LL);
+    cnorm[t] = v;
+    cn[t] = v;
+  }
+  if (t == 0) *J_out = sacc[k * T];
+  __syncthreads();
+  if (!do_assign) return;
+  unsigned changed = 0;
+  for (int64_t i = t; i < n; i += T) {
+    int best = 0;
+    double bd = __longlong_as_double(0x7ff0000000000000LL);
+    for (int c = 0; c < k; ++c) {
+      const double cv = cn[c];
+      const double dsh = isinf(cv) ? cv : fma(-2.0, E[i * k + c], cv);
+      if (Dfull) Dfull[i * k + c] = diag[i] + dsh;
+      if (dsh < bd) {
+        bd = dsh;
+        best = c;
+      }
+    }
+    cl_new[i] = best;
+    changed += best != cl[i];
+    atomicAdd(&hist[best], 1);
+  }
+  const unsigned wc = __reduce_add_sync(0xffffffffu, changed);
+  if ((t & 31) == 0 && wc) atomicAdd(&nchg, (unsigned long long)wc);
+  __syncthreads();
+  if (t < k) sizes_next[t] = hist[t];
+  if (t == 0) *changed_out = nchg;
+}
+
+}  // namespace kkm

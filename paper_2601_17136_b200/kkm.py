@@ -273,9 +273,13 @@ class KernelKMeans:
         return c.value
 
     def destroy(self):
+        """Destroys the handle and drops the binding's device buffers (the workspace it
+        allocated, the predict scratch), so their memory returns to torch's allocator."""
         if getattr(self, "h", None):
             _check(lib().kkm_destroy(self.h))
             self.h = None
+        self.workspace = None
+        self._predict_ws = None
 
     def __del__(self):
         try:

@@ -218,6 +218,7 @@ def test_errors_and_poison_free():
     h = _handle(X, 3, oracle.LINEAR, 1.0, 0.0, 1, 2, kkm.PREC_FP32_SIMT)
     with pytest.raises(kkm.KKMError, match="ELABEL"):
         h.set_labels(np.full(100, -1, dtype=np.int32))
+    assert np.array_equal(h.assign().cpu().numpy(), oracle.round_robin(100, 3))  # labels kept
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         h.kernel_tile(90, 0, 20, 5)
     h.fit()  # still usable after argument errors
