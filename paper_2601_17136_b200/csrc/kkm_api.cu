@@ -753,10 +753,11 @@ int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
         h->sizes[nx], changed_out, h->Dfull);
     CKL();
   }
-  if (P.nranks > 1) {
+  if (P.nranks > 1) {  // the changed count is global too: every rank takes the same control path
     CKN(ncclGroupStart());
     CKN(ncclAllGather(h->lab[nx] + P.row0, h->lab[nx], P.B, ncclInt32, h->comm, h->st));
     CKN(ncclAllReduce(h->sizes[nx], h->sizes[nx], P.k, ncclInt32, ncclSum, h->comm, h->st));
+    CKN(ncclAllReduce(changed_out, changed_out, 1, ncclUint64, ncclSum, h->comm, h->st));
     CKN(ncclGroupEnd());
   }
   return KKM_OK;

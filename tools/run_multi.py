@@ -20,15 +20,23 @@ dist.broadcast_object_list(uid, src=0)
 comm = kkm.comm_init(world, rank, uid[0])
 ok = True
 grids = [g for g in (1, 2, 4) if world % g == 0 and g <= world]
-cases = [(name, n, iters, path, g) for (name, n, iters) in [("har200k", 3001, 6), ("mnist60k", 2500, 5),
-                                                          ("rings", 1000, 10)]
+# (name, n, iters, path, grid_rows, extra KernelKMeans options)
+cases = [(name, n, iters, path, g, {}) for (name, n, iters) in [("har200k", 3001, 6), ("mnist60k", 2500, 5),
+                                                              ("rings", 1000, 10)]
          for path in (kkm.PATH_MATERIALIZE, kkm.PATH_STREAM) for g in grids]
-for name, n, iters, path, g in cases:
+# 1D extras: f1 bands at a small n, incremental S (f3) and stop-on-no-change -- the latter two
+# branch on the (global) changed count, so every rank must take the same path
+cases += [("har200k", 3001, 6, kkm.PATH_MATERIALIZE, 1, dict(symmetric=kkm.SYM_ON)),
+          ("mnist60k", 2500, 12, kkm.PATH_MATERIALIZE, 1, dict(incremental=True)),
+          ("mnist60k", 2500, 12, kkm.PATH_STREAM, 1, dict(incremental=True)),
+          ("rings", 1000, 60, kkm.PATH_MATERIALIZE, 1, dict(stop_on_no_change=True)),
+          ("rings", 1000, 60, kkm.PATH_STREAM, 1, dict(stop_on_no_change=True, incremental=True))]
+for name, n, iters, path, g, opt in cases:
     X, cfg = synth.make_config(name, n=n)
     args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
     r0, r1 = kkm.shard_begin(n, rank, world), kkm.shard_begin(n, rank + 1, world)
     h = kkm.KernelKMeans(torch.from_numpy(X[r0:r1]).cuda(), n, cfg["k"], *args, max_iter=iters,
-                         rank=rank, nranks=world, comm=comm, path=path, grid_rows=g)
+                         rank=rank, nranks=world, comm=comm, path=path, grid_rows=g, **opt)
     it, J, ch = h.fit()
     lab = h.assign().cpu().numpy()
     cn = h.debug_read(kkm.DBG_CNORM)
@@ -37,17 +45,20 @@ for name, n, iters, path, g in cases:
     if rank == 0:
         same = all(np.array_equal(g[0], lab) and np.array_equal(g[1], cn) and np.array_equal(g[2], J)
                    for g in gl)
-        one = kkm.KernelKMeans(torch.from_numpy(X).cuda(), n, cfg["k"], *args, max_iter=iters, path=path)
+        one = kkm.KernelKMeans(torch.from_numpy(X).cuda(), n, cfg["k"], *args, max_iter=iters, path=path, **opt)
         it1, J1, _ = one.fit()
         lab1 = one.assign().cpu().numpy()
-        ref = oracle.fit(X, cfg["k"], *args, max_iter=iters)
-        msg = (f"{name} n={n} P={world} grid {g}x{world // g} {'stream' if path == kkm.PATH_STREAM else 'mat'}: "
+        ref = oracle.fit(X, cfg["k"], *args, max_iter=iters, stop_on_no_change=bool(opt.get("stop_on_no_change")))
+        same &= it == it1
+        msg = (f"{name} n={n} P={world} grid {g}x{world // g} {'stream' if path == kkm.PATH_STREAM else 'mat'} "
+               f"{opt}: iters {it}/{it1} "
                f"ranks identical={same} labels==1gpu {np.array_equal(lab, lab1)} "
                f"labels==oracle {np.array_equal(lab, ref['labels'])} "
                f"maxrel J vs 1gpu {np.max(np.abs(J - J1) / np.abs(J1)):.2e} "
                f"vs oracle {np.max(np.abs(J - ref['J_trace']) / np.abs(ref['J_trace'])):.2e}")
         print(msg, flush=True)
-        ok &= same and np.array_equal(lab, lab1) and np.max(np.abs(J - J1) / np.abs(J1)) < 1e-6  # 1.5D reorders the fp32 chunk sums
+        ok &= bool(same) and J.shape == J1.shape and np.array_equal(lab, lab1) and \
+            np.max(np.abs(J - J1) / np.abs(J1)) < 1e-6  # 1.5D reorders the fp32 chunk sums
     h.destroy()
     dist.barrier()
 kkm.comm_destroy(comm)
