@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(SYM_THREADS, 1)
     const int q0 = s * cps;
     const int q1 = q0 + cps < nchunks ? q0 + cps : nchunks;
     float *cp = colpart + bands[b].cpoff + (int64_t)g * (ldb - SYM_TB) - SYM_TB;  // indexed by band column
-    const bool colsums = half == 0;
     float2 acc[R][KH];
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -222,7 +221,11 @@ __global__ void __launch_bounds__(SYM_THREADS, 1)
       const float *st = ring + (size_t)stage * (R + 1) * CH;
       const int4 *lab4 = reinterpret_cast<const int4 *>(st + R * CH);
       const int nquads = cols >> 2;
-      for (int v = quarter * 32 + lane; v < nquads; v += 4 * 32) {
+      // the column sums alternate between the cluster halves by (warp-uniform) quad step, so
+      // both halves carry the same work
+      int step = q;
+      for (int v = quarter * 32 + lane; v < nquads; v += 4 * 32, ++step) {
+        const bool colsums = (step & 1) == half;
         const int4 l = lab4[v];
         float4 x[R];
 #pragma unroll
