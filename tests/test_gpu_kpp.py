@@ -81,3 +81,22 @@ def test_kmeanspp_duplicates_and_errors():
     with pytest.raises(ValueError):
         h.seed_kmeanspp(u=np.zeros(3))
     h.destroy()
+
+
+def test_quality_rings_and_blobs_recovered_on_gpu():
+    """SURVEY P13 quality on the CUDA path: K-means++ seeding + the clustering loop recover the
+    two rings (Gaussian, gamma = 1) and five separated blobs (linear) exactly (ARI = 1)."""
+    from sklearn.metrics import adjusted_rand_score
+    X, truth = synth.rings(1000, seed=1, return_truth=True)
+    h = kkm.KernelKMeans(torch.from_numpy(X).cuda(), 1000, 2, kkm.KERNEL_GAUSSIAN, 1.0, 0.0, 1, max_iter=30)
+    h.seed_kmeanspp(u=np.random.default_rng(0).random(2))
+    h.fit()
+    assert adjusted_rand_score(truth, h.assign().cpu().numpy()) == 1.0
+    h.destroy()
+    Xb, tb = synth.blobs(600, 8, 5, seed=2, sep=10.0, return_truth=True)
+    hb = kkm.KernelKMeans(torch.from_numpy(Xb).cuda(), 600, 5, kkm.KERNEL_LINEAR, 1.0, 0.0, 1, max_iter=30,
+                          path=kkm.PATH_STREAM)
+    hb.seed_kmeanspp(u=np.random.default_rng(1).random(5))
+    hb.fit()
+    assert adjusted_rand_score(tb, hb.assign().cpu().numpy()) == 1.0
+    hb.destroy()

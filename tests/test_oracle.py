@@ -397,3 +397,18 @@ def test_kmeanspp_poly2_feature_map_and_special_cases():
     cd, ld = oracle.kmeanspp(Xd, 5, np.random.default_rng(1).random(5), oracle.GAUSSIAN, 0.7)
     assert len(set(map(tuple, Xd[cd[:3]]))) == 3
     assert (cd[3:] == cd[2]).all()
+
+
+# ---------------------------------------------------------------- P13 quality (not parity)
+def test_quality_rings_and_blobs_recovered():
+    """blobs recovered, rings ARI -- with K-means++ seeding (the
+    round-robin start of A5 lands in another local optimum of J on the rings, ARI ~0.27)."""
+    from sklearn.metrics import adjusted_rand_score
+    X, truth = synth.rings(1000, seed=1, return_truth=True)
+    _, lab0 = oracle.kmeanspp(X, 2, np.random.default_rng(0).random(2), oracle.GAUSSIAN, 1.0)
+    fit = oracle.fit(X, 2, oracle.GAUSSIAN, 1.0, max_iter=30, init_labels=lab0)
+    assert adjusted_rand_score(truth, fit["labels"]) == 1.0
+    Xb, tb = synth.blobs(600, 8, 5, seed=2, sep=10.0, return_truth=True)
+    _, lb = oracle.kmeanspp(Xb, 5, np.random.default_rng(1).random(5), oracle.LINEAR)
+    fb = oracle.fit(Xb, 5, oracle.LINEAR, max_iter=30, init_labels=lb)
+    assert adjusted_rand_score(tb, fb["labels"]) == 1.0
