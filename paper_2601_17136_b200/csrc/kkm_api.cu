@@ -77,7 +77,7 @@ struct Plan {
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
       o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
-      o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, total;
+      o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -276,6 +276,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   };
   const int64_t k1 = P.k + 1;
   P.o_Xf = take((size_t)P.npad * P.ldf * 4);
+  P.o_mean = take((size_t)P.ldf * 4);
+  P.o_cmpart = p->kind == KKM_KERNEL_GAUSSIAN ? take((size_t)ceil_div(n, CM_ROWS) * P.ldf * 8) : 0;
   P.o_Xhi = P.tc ? take((size_t)P.npad * P.dp * 2) : 0;
   P.o_Xlo = P.tc ? take((size_t)P.npad * P.dp * 2) : 0;
   P.o_rscale = take((size_t)P.npad * 4);
@@ -379,6 +381,7 @@ struct kkm_ctx {
   int num_sms = 148;
   uint8_t *ws = nullptr;
   float *Xf = nullptr, *norms = nullptr, *K = nullptr;
+  float *mean = nullptr;  // Gaussian: the column means X was centered on (0 otherwise)
   uint16_t *Xhi = nullptr, *Xlo = nullptr;  // bf16 or fp16 split of X (P.tc)
   float *rscale = nullptr;                   // 1 / s_i of the fp16 split
   double *diag, *Spart, *E, *blockpart, *rankpart, *cnorm, *J, *Dfull;
@@ -885,6 +888,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   }
   uint8_t *w = h->ws;
   h->Xf = (float *)(w + P.o_Xf);
+  h->mean = (float *)(w + P.o_mean);
   h->Xhi = P.tc ? (uint16_t *)(w + P.o_Xhi) : nullptr;
   h->Xlo = P.tc ? (uint16_t *)(w + P.o_Xlo) : nullptr;
   h->rscale = (float *)(w + P.o_rscale);
@@ -979,6 +983,19 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     if (P.nranks > 1)
       CKN(ncclAllGather(h->Xf + (int64_t)P.rank * P.B * P.ldf, h->Xf, (size_t)P.B * P.ldf, ncclFloat,
                         h->comm, h->st));
+    // ---- Gaussian: center X on its column means (exact for kappa; smaller norms shrink the
+    // accumulation bias of r^2 on the tensor cores, DESIGN A9). Every rank holds all of X.
+    CK(cudaMemsetAsync(h->mean, 0, (size_t)P.ldf * 4, h->st));
+    if (p->kind == KKM_KERNEL_GAUSSIAN) {
+      const unsigned nch = (unsigned)ceil_div(P.n, CM_ROWS);
+      double *part = (double *)(h->ws + P.o_cmpart);
+      colmean_partial_kernel<<<dim3((unsigned)ceil_div(P.d, 128), nch), 128, 0, h->st>>>(h->Xf, P.ldf, P.n, P.d, part);
+      CKL();
+      colmean_final_kernel<<<(unsigned)ceil_div(P.d, 128), 128, 0, h->st>>>(part, (int)nch, P.n, P.d, h->mean);
+      CKL();
+      center_rows_kernel<<<(unsigned)ceil_div(P.n, 8), 256, 0, h->st>>>(h->Xf, P.ldf, P.n, P.d, h->mean);
+      CKL();
+    }
     // ---- a5: norms, bf16 split, diag
     {
       const int wpb = 8;
@@ -1307,6 +1324,10 @@ int predict_run(kkm_ctx *h, const PredictPlan &q, uint8_t *t, const float *Y, in
   // a5 for the new points: split operands, norms, kappa(y, y) (prep_rows and diag read only
   // rows < m and columns < d of Yf, and write the split's pad rows/columns as zeros)
   CK(cudaMemcpy2DAsync(Yf, P.ldf * 4, Y, ldy * 4, P.d * 4, m, cudaMemcpyDefault, h->st));
+  if (h->p.kind == KKM_KERNEL_GAUSSIAN) {  // the training points were centered (kkm_init)
+    center_rows_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, h->st>>>(Yf, P.ldf, m, P.d, h->mean);
+    CKL();
+  }
   prep_rows_kernel<<<(unsigned)ceil_div(q.mpad, 8), 256, 0, h->st>>>(Yf, P.ldf, m, q.mpad, P.d, yn, Yhi, Ylo, P.dp,
                                                                      P.fp16 ? 2 : 1, yr);
   CKL();

@@ -138,3 +138,41 @@ __global__ void histogram_kernel(const int32_t *__restrict__ labels, int64_t n, 
 }
 
 }  // namespace kkm
+
+namespace kkm {
+
+// ---- Gaussian kernel: center X on its column means before the split (exact for kappa, which
+// depends only on x - y; smaller |x| shrinks the tensor-core accumulation bias of
+// r^2 = |x|^2 + |y|^2 - 2 x.y, A9). Deterministic two-pass fp64 means.
+constexpr int CM_ROWS = 1024;  // rows per partial
+
+// part[b][t] = sum of X[r][t] over the rows r of chunk b (in order), t < d.
+__global__ void colmean_partial_kernel(const float *__restrict__ Xf, int64_t ldf, int64_t n, int64_t d,
+                                       double *__restrict__ part) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d) return;
+  const int64_t r0 = (int64_t)blockIdx.y * CM_ROWS, r1 = r0 + CM_ROWS < n ? r0 + CM_ROWS : n;
+  double s = 0.0;
+  for (int64_t r = r0; r < r1; ++r) s += (double)Xf[r * ldf + t];
+  part[(int64_t)blockIdx.y * d + t] = s;
+}
+
+// mean[t] = (sum over chunks in order) / n, rounded to fp32.
+__global__ void colmean_final_kernel(const double *__restrict__ part, int nchunks, int64_t n, int64_t d,
+                                     float *__restrict__ mean) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d) return;
+  double s = 0.0;
+  for (int b = 0; b < nchunks; ++b) s += part[(int64_t)b * d + t];
+  mean[t] = (float)(s / (double)n);
+}
+
+// X[r][t] -= mean[t] for r < n, t < d.
+__global__ void center_rows_kernel(float *__restrict__ Xf, int64_t ldf, int64_t n, int64_t d,
+                                   const float *__restrict__ mean) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // grid.x = ceil(n / 8)
+  if (r >= n) return;
+  for (int64_t t = threadIdx.x & 31; t < d; t += 32) Xf[r * ldf + t] -= mean[t];
+}
+
+}  // namespace kkm
