@@ -10,6 +10,11 @@
  *   (a4) D = -2E + C~; cl <- argmin_c D(i, c); V <- V(cl)   Eq. (d)
  * in a loop (Alg. 1). All arithmetic runs in the CUDA kernels of
  * libkkm.so (sm_100a); this header and the ctypes binding only marshal.
+ * Beyond the paper's loop: K's symmetry is exploited (f1,
+ * kkm_params.symmetric); the cluster sums can be updated by the moved points
+ * only and the labels seeded by K-means++ (f3, kkm_params.incremental,
+ * kkm_seed_kmeanspp); new points can be assigned to fitted clusters (f4,
+ * kkm_predict).
  *
  * Conventions
  *   - Every function returns an int status (KKM_OK = 0); on failure
