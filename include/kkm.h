@@ -96,7 +96,9 @@ extern "C" {
 #define KKM_PH_SPMM 2       /* a2 per fit (sum over iterations)                 */
 #define KKM_PH_CNORM 3      /* a3 incl. its collective                          */
 #define KKM_PH_ASSIGN 4     /* a4 incl. the labels allgather                    */
-#define KKM_NPHASES 5
+#define KKM_PH_A2_KERNEL 5  /* the dominant a2 kernel alone (spmm_sym / spmm_onehot /
+                               the streaming kernel), summed over the loop's launches */
+#define KKM_NPHASES 6
 
 typedef struct kkm_params {
   int32_t kind;            /* KKM_KERNEL_*                                         */

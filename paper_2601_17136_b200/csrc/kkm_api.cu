@@ -421,7 +421,9 @@ struct kkm_ctx {
   bool have_last = false;
   bool cnorm2_valid = false;  // cnorm2 holds c of the current labels (after kkm_fit / kkm_objective)
   int64_t launches = 0;
-  float phase_ms[KKM_NPHASES] = {0, 0, 0, 0, 0};
+  float phase_ms[KKM_NPHASES] = {0, 0, 0, 0, 0, 0};
+  bool time_a2 = false;             // timing mode, inside the kkm_fit loop
+  std::vector<cudaEvent_t> a2ev;    // (start, end) pairs around the dominant a2 kernel
   KappaParams kp;
   TcGemm tc;
 };
@@ -461,6 +463,16 @@ namespace {
     int rc_ = (expr);    \
     if (rc_) return rc_; \
   } while (0)
+
+// Brackets the dominant a2 kernel launch(es) with CUDA events (timing mode, kkm_fit loop).
+void a2_mark(kkm_ctx *h) {
+  if (!h->time_a2) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) == cudaSuccess) {
+    cudaEventRecord(e, h->st);
+    h->a2ev.push_back(e);
+  }
+}
 
 // Host or device pointer copy on the handle's stream.
 int copy_any(kkm_ctx *h, void *dst, const void *src, size_t bytes) {
@@ -553,11 +565,22 @@ int launch_stream(kkm_ctx *h, const int32_t *labels) {
   const SortedSet B{h->Shi, h->Slo, h->snorms, h->srscale, h->perm, h->pos, h->seg, h->bcount, h->boff};
   CKR(sort_gather(h, labels + P.b0, P.b0, P.nB, P.npad, B));
   const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.a0, P.nA, P.nApad};
-  return stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, P.nsplit, h->Spart);
+  a2_mark(h);
+  const int rc = stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, P.nsplit, h->Spart);
+  a2_mark(h);
+  return rc;
 }
 
 // a2 on the materialised K tile (A set rows x B set columns).
+int launch_spmm_mat_body(kkm_ctx *h, const int32_t *labels);
 int launch_spmm_mat(kkm_ctx *h, const int32_t *labels) {
+  a2_mark(h);
+  const int rc = launch_spmm_mat_body(h, labels);
+  a2_mark(h);
+  return rc;
+}
+
+int launch_spmm_mat_body(kkm_ctx *h, const int32_t *labels) {
   const Plan &P = h->P;
   if (P.nA == 0) return KKM_OK;
   if (P.spmm_v2) {
@@ -608,11 +631,17 @@ int launch_spmm_sym_kp(kkm_ctx *h, const int32_t *labels) {
                             (int)spmm_sym_smem_bytes()));
     attr_set = true;
   }
-  if (P.sym_items == 0) return KKM_OK;
+  if (P.sym_items == 0) {
+    a2_mark(h);
+    a2_mark(h);
+    return KKM_OK;
+  }
   const int grid = (int)std::min<int64_t>(P.sym_items, h->num_sms);
+  a2_mark(h);
   spmm_sym_kernel<KP><<<grid, SYM_THREADS, spmm_sym_smem_bytes(), h->st>>>(
       h->K, h->bands, (int)P.bands.size(), P.sym_items, labels, h->perm_b, h->groups, P.sym_gmax, P.k, P.nApad,
       h->Spart, h->colpart);
+  a2_mark(h);
   CKL();
   return KKM_OK;
 }
@@ -666,9 +695,11 @@ int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   const SortedSet B{h->Shi, h->Slo, h->snorms, h->srscale, h->perm, h->pos, h->seg, h->bcount, h->boff};
   CKR(sort_gather(h, labels, 0, P.n, P.npad, B));
   CK(cudaMemsetAsync(h->Sfix, 0, (size_t)P.npad * k * 8, h->st));
+  a2_mark(h);
   int rc = tc2_stream_sym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg,
                                  k, h->kp, h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st,
                                  &h->launches);
+  a2_mark(h);
   if (rc) {
     h->poisoned = true;
     return fail(KKM_ECUDA, "symmetric streaming kernel launch failed: %s", tc_gemm_error());
@@ -1112,6 +1143,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
     return KKM_OK;
   };
   int t = 0;
+  h->time_a2 = timing;
   for (t = 0; t < T; ++t) {
     if (timing) CKR(rec(ev));
     const double *S = nullptr;
@@ -1163,6 +1195,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
       break;
     }
   }
+  h->time_a2 = false;
   // J of the final labels (one more a2 + a3 pass, as the oracle's J_trace[iters])
   {
     const double *S = nullptr;
@@ -1195,7 +1228,14 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
       h->phase_ms[KKM_PH_ASSIGN] += c;
     }
     for (auto e : ev) cudaEventDestroy(e);
+    for (size_t i = 0; i + 1 < h->a2ev.size(); i += 2) {
+      float a = 0;
+      CK(cudaEventElapsedTime(&a, h->a2ev[i], h->a2ev[i + 1]));
+      h->phase_ms[KKM_PH_A2_KERNEL] += a;
+    }
   }
+  for (auto e : h->a2ev) cudaEventDestroy(e);
+  h->a2ev.clear();
   if (iters_run) *iters_run = t;
   if (J_trace) std::memcpy(J_trace, J.data(), (size_t)(t + 1) * 8);
   if (changed)

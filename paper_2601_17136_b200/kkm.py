@@ -19,7 +19,7 @@ PATH_AUTO, PATH_MATERIALIZE, PATH_STREAM = 0, 1, 2
 PREC_BF16X3, PREC_FP32_SIMT, PREC_FP16X3 = 0, 1, 2
 SYM_AUTO, SYM_OFF, SYM_ON = 0, 1, 2
 DBG_E, DBG_CNORM, DBG_SIZES, DBG_DIAG, DBG_DFULL, DBG_LABELS_PREV = range(6)
-PHASES = ("init_prep", "init_gemm", "spmm", "cnorm", "assign")
+PHASES = ("init_prep", "init_gemm", "spmm", "cnorm", "assign", "a2_kernel")
 
 
 class KKMError(RuntimeError):
