@@ -366,6 +366,26 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
 
 }  // namespace
 
+// CUDA events owned for one scope (destroyed on every exit path, errors included).
+struct EventList {
+  std::vector<cudaEvent_t> v;
+  EventList() = default;
+  EventList(const EventList &) = delete;
+  EventList &operator=(const EventList &) = delete;
+  ~EventList() { clear(); }
+  void clear() {
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
+    v.clear();
+  }
+  // creates and records one event; false if the runtime refused
+  bool record(cudaStream_t st) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return false;
+    v.push_back(e);
+    return cudaEventRecord(e, st) == cudaSuccess;
+  }
+};
+
 // Label-sorted copy of a point set (the B operand of the streaming kernel) and its sort.
 struct SortedSet {
   uint16_t *hi, *lo;
@@ -423,7 +443,7 @@ struct kkm_ctx {
   int64_t launches = 0;
   float phase_ms[KKM_NPHASES] = {0, 0, 0, 0, 0, 0};
   bool time_a2 = false;             // timing mode, inside the kkm_fit loop
-  std::vector<cudaEvent_t> a2ev;    // (start, end) pairs around the dominant a2 kernel
+  EventList a2ev;                   // (start, end) pairs around the dominant a2 kernel
   KappaParams kp;
   TcGemm tc;
 };
@@ -466,12 +486,7 @@ namespace {
 
 // Brackets the dominant a2 kernel launch(es) with CUDA events (timing mode, kkm_fit loop).
 void a2_mark(kkm_ctx *h) {
-  if (!h->time_a2) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) == cudaSuccess) {
-    cudaEventRecord(e, h->st);
-    h->a2ev.push_back(e);
-  }
+  if (h->time_a2) h->a2ev.record(h->st);
 }
 
 // Host or device pointer copy on the handle's stream.
@@ -1001,11 +1016,8 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         attr = true;
       }
     }
-    cudaEvent_t e0, e1, e2;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventCreate(&e2));
-    CK(cudaEventRecord(e0, h->st));
+    EventList evs;  // init phases: prep, GEMM
+    if (!evs.record(h->st)) return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
     // ---- X (Alg. 1 line 1: allgather P) into Xf [npad x ldf], zero padded
     CK(cudaMemsetAsync(h->Xf, 0, (size_t)P.npad * P.ldf * 4, h->st));
     if (P.nloc > 0)
@@ -1063,7 +1075,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     histogram_kernel<<<std::min<int64_t>(ceil_div(P.n, 256), 1024), 256, (size_t)P.k * 4, h->st>>>(
         h->lab[0], P.n, P.k, h->sizes[0]);
     CKL();
-    CK(cudaEventRecord(e1, h->st));
+    if (!evs.record(h->st)) return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
     // ---- a1: K tile [A set, B set] = kappa(X X^T), materialised once; with
     // symmetric storage (f1) the owned upper-triangle bands, one launch each
     if (P.ssym) {  // units, and the fixed-point scale 2^s with n * max|K| * 2^s < 2^61
@@ -1094,18 +1106,15 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     } else if (P.materialize) {
       CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));
     }
-    CK(cudaEventRecord(e2, h->st));
+    if (!evs.record(h->st)) return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
     CK(cudaStreamSynchronize(h->st));
     if (h->p.timing) {
       float a = 0, b = 0;
-      CK(cudaEventElapsedTime(&a, e0, e1));
-      CK(cudaEventElapsedTime(&b, e1, e2));
+      CK(cudaEventElapsedTime(&a, evs.v[0], evs.v[1]));
+      CK(cudaEventElapsedTime(&b, evs.v[1], evs.v[2]));
       h->phase_ms[KKM_PH_INIT_PREP] += a;
       h->phase_ms[KKM_PH_INIT_GEMM] += b;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
     return KKM_OK;
   }();
   if (rc == KKM_OK && P.pr > 1) {  // process-column communicator: ranks gi + gj * pr, key gi
@@ -1133,15 +1142,16 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned by an earlier CUDA/NCCL error");
   const Plan &P = h->P;
   const int T = h->p.max_iter;
-  std::vector<cudaEvent_t> ev;
+  EventList ev;  // 5 per iteration (timing mode)
   const bool timing = h->p.timing != 0;
-  auto rec = [&](std::vector<cudaEvent_t> &v) -> int {
-    cudaEvent_t e;
-    CK(cudaEventCreate(&e));
-    CK(cudaEventRecord(e, h->st));
-    v.push_back(e);
+  auto rec = [&](EventList &l) -> int {
+    if (!l.record(h->st)) {
+      h->poisoned = true;
+      return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
+    }
     return KKM_OK;
   };
+  h->a2ev.clear();
   int t = 0;
   h->time_a2 = timing;
   for (t = 0; t < T; ++t) {
@@ -1217,24 +1227,24 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (timing) {
-    for (size_t i = 0; i + 4 < ev.size(); i += 5) {  // the a2 phase includes the f3 S update
+    const std::vector<cudaEvent_t> &e5 = ev.v;
+    for (size_t i = 0; i + 4 < e5.size(); i += 5) {  // the a2 phase includes the f3 S update
       float a, b, c, d;
-      CK(cudaEventElapsedTime(&a, ev[i], ev[i + 1]));
-      CK(cudaEventElapsedTime(&b, ev[i + 1], ev[i + 2]));
-      CK(cudaEventElapsedTime(&c, ev[i + 2], ev[i + 3]));
-      CK(cudaEventElapsedTime(&d, ev[i + 3], ev[i + 4]));
+      CK(cudaEventElapsedTime(&a, e5[i], e5[i + 1]));
+      CK(cudaEventElapsedTime(&b, e5[i + 1], e5[i + 2]));
+      CK(cudaEventElapsedTime(&c, e5[i + 2], e5[i + 3]));
+      CK(cudaEventElapsedTime(&d, e5[i + 3], e5[i + 4]));
       h->phase_ms[KKM_PH_SPMM] += a + d;
       h->phase_ms[KKM_PH_CNORM] += b;
       h->phase_ms[KKM_PH_ASSIGN] += c;
     }
-    for (auto e : ev) cudaEventDestroy(e);
-    for (size_t i = 0; i + 1 < h->a2ev.size(); i += 2) {
+    const std::vector<cudaEvent_t> &a2 = h->a2ev.v;
+    for (size_t i = 0; i + 1 < a2.size(); i += 2) {
       float a = 0;
-      CK(cudaEventElapsedTime(&a, h->a2ev[i], h->a2ev[i + 1]));
+      CK(cudaEventElapsedTime(&a, a2[i], a2[i + 1]));
       h->phase_ms[KKM_PH_A2_KERNEL] += a;
     }
   }
-  for (auto e : h->a2ev) cudaEventDestroy(e);
   h->a2ev.clear();
   if (iters_run) *iters_run = t;
   if (J_trace) std::memcpy(J_trace, J.data(), (size_t)(t + 1) * 8);
