@@ -58,3 +58,56 @@ def test_lpt_balances_area():
     for I, r in enumerate(owner):
         area[r] += min(1024, 60000 - I * 1024) * (60000 - I * 1024)
     assert area.max() < 1.1 * area.min()
+
+
+def stream_units(n, tile, block, P):
+    """tc2_stream_sym units as make_plan builds them: (row tile, globally aligned column block
+    of <= `block` tiles, from the row tile's own tile on), spread largest first to the
+    least-loaded rank (stable order), each rank's list in row-major order."""
+    T = -(-n // tile)
+    allu = [(tm, max(tm, b * block), min(T, (b + 1) * block) - max(tm, b * block))
+            for tm in range(T) for b in range(tm // block, -(-T // block))]
+    order = sorted(range(len(allu)), key=lambda i: -allu[i][2])  # stable
+    load, owner = [0] * P, [0] * len(allu)
+    for i in order:
+        r = min(range(P), key=lambda q: (load[q], q))
+        load[r] += allu[i][2]
+        owner[i] = r
+    return [[u for i, u in enumerate(allu) if owner[i] == r] for r in range(P)]
+
+
+@pytest.mark.parametrize("n,tile,block,P", [(37, 8, 2, 1), (37, 8, 2, 3), (64, 8, 3, 2), (50, 4, 64, 4)])
+def test_symmetric_streaming_decomposition(n, tile, block, P):
+    """Upper-triangle tiles of the label-sorted K: row sums by the column segments on every
+    tile, column sums by the row segments off the diagonal tiles, summed in int64 fixed point
+    over the ranks == S from the full K (exactly the same integers for any P)."""
+    X = synth.blobs(n, 3, 4, seed=n + P)
+    lab = (np.arange(n) * 5 + 1) % 4
+    perm = np.argsort(lab, kind="stable")  # the label-sorted order
+    Ks = oracle.kernel_matrix(X, oracle.POLY, 0.5, 1.0, 2)[np.ix_(perm, perm)]
+    ls = lab[perm]
+    scale = 2.0 ** 30
+
+    def fx(v):
+        return np.rint(v * scale).astype(np.int64)
+
+    Sfix = np.zeros((n, 4), dtype=np.int64)
+    for units in stream_units(n, tile, block, P):
+        for tm, tn0, ntn in units:
+            r0, r1 = tm * tile, min(n, (tm + 1) * tile)
+            for tn in range(tn0, tn0 + ntn):
+                c0, c1 = tn * tile, min(n, (tn + 1) * tile)
+                blk = Ks[r0:r1, c0:c1]
+                for c in range(4):  # row part, by the column labels
+                    Sfix[r0:r1, c] += fx(blk[:, ls[c0:c1] == c].sum(axis=1))
+                if tn != tm:  # column part off the diagonal tile, by the row labels
+                    for c in range(4):
+                        Sfix[c0:c1, c] += fx(blk[ls[r0:r1] == c].sum(axis=0))
+    S = Sfix / scale
+    S_ref = np.stack([Ks[:, ls == c].sum(axis=1) for c in range(4)], axis=1)
+    assert np.allclose(S, S_ref, rtol=1e-7, atol=1e-6)
+    # every upper-triangle tile exactly once
+    T = -(-n // tile)
+    seen = sorted((tm, tn) for units in stream_units(n, tile, block, P) for tm, tn0, nt in units
+                  for tn in range(tn0, tn0 + nt))
+    assert seen == [(a, b) for a in range(T) for b in range(a, T)]
