@@ -39,7 +39,7 @@ def _handle(X, k, kind, gamma, coef0, degree, max_iter, precision, **kw):
                             precision=precision, **kw)
 
 
-def teacher_forced(X, k, kind, gamma=1.0, coef0=0.0, degree=1, iters=3, precision=0, init=None):
+def teacher_forced(X, k, kind, gamma=1.0, coef0=0.0, degree=1, iters=3, precision=0, init=None, check_J=True):
     """For each t: inject the oracle's cl_t, run one GPU iteration, compare everything."""
     ref = oracle.fit(X, k, kind, gamma, coef0, degree, max_iter=iters, init_labels=init,
                      keep_trace=True)
@@ -58,9 +58,11 @@ def teacher_forced(X, k, kind, gamma=1.0, coef0=0.0, degree=1, iters=3, precisio
                    Dfull=h.debug_read(kkm.DBG_DFULL), new_labels=new,
                    sizes=h.debug_read(kkm.DBG_SIZES), J=J[0])
         assert np.array_equal(h.debug_read(kkm.DBG_LABELS_PREV), cl)
+        if not check_J:
+            gpu.pop("J")
         mism += check_iteration(gpu, it, diag)
         assert ch[0] == int((new != cl).sum())
-        if np.array_equal(new, it["new_labels"]):  # final-labels J (J_trace[1])
+        if check_J and np.array_equal(new, it["new_labels"]):  # final-labels J (J_trace[1])
             Jn = oracle.objective(diag, new, k, oracle.cnorm(oracle.E_rows(K, new, k), new, k))
             assert abs(J[1] - Jn) <= j_tol(Jn, diag)
     h.destroy()
@@ -327,3 +329,23 @@ def test_full_size_objective_at_convergence(name, iters):
     Jref = hs.objective()
     hs.destroy()
     assert abs(J - Jref) <= 1e-5 * abs(Jref), (J, Jref)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+@pytest.mark.parametrize("d", [1, 3000])
+def test_extreme_feature_dims(precision, d):
+    """d = 1 (one partial 64-wide k-block) and d = 3000 (47 k-blocks, a 3008-wide fp32 pitch):
+    K, E, c, D, labels, sizes within the parity rules in every mode. J is checked except on the
+    tensor-core modes at d = 3000, where the accumulation bias (~d/16 MMA steps, DESIGN A9)
+    exceeds 1e-5 of J -- see test_large_d_objective_limit."""
+    X = synth.blobs(700, d, 4, seed=80 + d, sep=4.0)
+    cj = d <= 1024 or precision[0] == kkm.PREC_FP32_SIMT
+    teacher_forced(X, 4, oracle.GAUSSIAN, 0.5 / d, iters=2, precision=precision, check_J=cj)
+    teacher_forced(X, 4, oracle.POLY, 1.0 / d, 1.0, 2, iters=2, precision=precision, check_J=cj)
+
+
+@pytest.mark.xfail(strict=True, reason="fp16x3 tensor-core accumulation bias grows with d/16 MMA steps: "
+                   "at d = 3000 J is off by ~1.7e-5 relative (DESIGN A9); FP32_SIMT meets 1e-5")
+def test_large_d_objective_limit():
+    X = synth.blobs(700, 3000, 4, seed=3080, sep=4.0)
+    teacher_forced(X, 4, oracle.GAUSSIAN, 0.5 / 3000, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE))
