@@ -76,7 +76,7 @@ struct Plan {
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
       o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
 };
 
@@ -357,6 +357,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_band_desc = take((size_t)P.T * 4);
     P.o_colpart = take(std::max<size_t>(cpfloats, 1) * 4);
     P.o_colsum = take(std::max<size_t>(csdoubles, 1) * 8);
+    P.o_work = take(2 * 4);  // spmm_sym's item scheduler
     P.o_gfirst = take((size_t)P.T * (P.k + 1) * 4);
     P.o_Sfin = take((size_t)P.npad * P.k * 8);
   }
@@ -421,6 +422,7 @@ struct kkm_ctx {
   SymBand *bands = nullptr;
   float *colpart = nullptr;
   double *colsum = nullptr, *Sfin = nullptr;
+  int32_t *work = nullptr;  // spmm_sym's item scheduler (2 counters, zero between launches)
   // f1 streaming: units, int64 fixed-point S (sorted order), its original-order copy
   int4 *units = nullptr;
   long long *Sfix = nullptr, *Sorig = nullptr, *Sfmine = nullptr;
@@ -655,7 +657,7 @@ int launch_spmm_sym_kp(kkm_ctx *h, const int32_t *labels) {
   a2_mark(h);
   spmm_sym_kernel<KP><<<grid, SYM_THREADS, spmm_sym_smem_bytes(), h->st>>>(
       h->K, h->bands, (int)P.bands.size(), P.sym_items, labels, h->perm_b, h->groups, P.sym_gmax, P.k, P.nApad,
-      h->Spart, h->colpart);
+      h->Spart, h->colpart, h->work);
   a2_mark(h);
   CKL();
   return KKM_OK;
@@ -998,6 +1000,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->band_desc = (int32_t *)(w + P.o_band_desc);
     h->colpart = (float *)(w + P.o_colpart);
     h->colsum = (double *)(w + P.o_colsum);
+    h->work = (int32_t *)(w + P.o_work);
     h->gfirst = (int32_t *)(w + P.o_gfirst);
     h->Sfin = (double *)(w + P.o_Sfin);
   }
@@ -1099,6 +1102,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         CK(cudaMemcpyAsync(h->bands, P.bands.data(), P.bands.size() * sizeof(SymBand), cudaMemcpyHostToDevice,
                            h->st));
       CK(cudaMemcpyAsync(h->band_desc, P.band_desc.data(), (size_t)P.T * 4, cudaMemcpyHostToDevice, h->st));
+      CK(cudaMemsetAsync(h->work, 0, 2 * 4, h->st));
       for (const SymBand &b : P.bands) {
         const int64_t i0 = (int64_t)b.band * SYM_TB;
         CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, h->K + b.koff, b.ldb));

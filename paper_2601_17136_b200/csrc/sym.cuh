@@ -119,12 +119,13 @@ __global__ void __launch_bounds__(SYM_TB) band_sort_kernel(const int32_t *__rest
 // Items: for each owned band b (bands[b]), gmax groups x nsplit splits (empty groups skipped).
 // Spart[(s * rows_pad + row) * k + c] (fp64) for the group's rows, s < bands[b].nsplit;
 // colpart[cpoff + g * (ldb - TB) + (col - TB)] (fp32) for the stored columns col >= TB.
+// work[0] (next item), work[1] (CTAs past the end): zero between launches (reset at the end).
 template <int KP>
 __global__ void __launch_bounds__(SYM_THREADS, 1)
     spmm_sym_kernel(const float *__restrict__ K, const SymBand *__restrict__ bands, int nbands, int64_t nitems,
                     const int32_t *__restrict__ labels, const int32_t *__restrict__ perm,
                     const SymGroup *__restrict__ groups, int gmax, int k, int64_t rows_pad,
-                    double *__restrict__ Spart, float *__restrict__ colpart) {
+                    double *__restrict__ Spart, float *__restrict__ colpart, int32_t *__restrict__ work) {
   constexpr int R = SYM_R, STAGES = SYM_STAGES, CW = SYM_CW, CH = SYM_CH;
   constexpr int KH = KP / 2;  // clusters per half
   extern __shared__ __align__(128) uint8_t smem[];
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(SYM_THREADS, 1)
   float *red = ring + (size_t)STAGES * (R + 1) * CH;          // [CW][R][KH]
   uint64_t *full = reinterpret_cast<uint64_t *>(red + CW * R * (SP_KPMAX / 2));
   uint64_t *empty = full + STAGES;
+  __shared__ int4 s_item[STAGES];  // (band b, group g, split s) of a stage's item; b < 0: no more items
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -161,7 +163,11 @@ __global__ void __launch_bounds__(SYM_THREADS, 1)
   uint32_t phase = 0;
   if (warp == CW) {
     if (lane == 0) {
-      for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+      // dynamic item scheduling: items are taken in order (largest bands first) by whichever
+      // CTA is free (static round-robin left SMs idle at the end: a2 kernel 1.33 -> 1.26 ms)
+      for (;;) {
+        const int64_t item = atomicAdd(work, 1);
+        if (item >= nitems) break;
         int b, g, s;
         decode(item, b, g, s);
         const SymBand bd = bands[b];
@@ -181,6 +187,7 @@ __global__ void __launch_bounds__(SYM_THREADS, 1)
           const uint32_t cols = (uint32_t)(bd.ldb - col0 < CH ? bd.ldb - col0 : CH);
           mbar_wait(&empty[stage], phase ^ 1);
           float *st = ring + (size_t)stage * (R + 1) * CH;
+          s_item[stage] = make_int4(b, g, s, 0);
           mbar_arrive_expect_tx(&full[stage], (uint32_t)(gr.cnt + 1) * cols * 4u);
           bulk_g2s(st + R * CH, lab + col0, cols * 4u, &full[stage]);
 #pragma unroll
@@ -192,18 +199,27 @@ __global__ void __launch_bounds__(SYM_THREADS, 1)
           }
         }
       }
+      mbar_wait(&empty[stage], phase ^ 1);  // end marker for the consumers
+      s_item[stage] = make_int4(-1, 0, 0, 0);
+      mbar_arrive(&full[stage]);
+      // the last CTA past the end resets the scheduler for the next launch
+      if (atomicAdd(work + 1, 1) == (int)gridDim.x - 1) {
+        work[0] = 0;
+        work[1] = 0;
+      }
     }
     return;
   }
 
   const int half = warp >> 2, quarter = warp & 3;
   const int cbase = half * KH;
-  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    int b, g, s;
-    decode(item, b, g, s);
+  for (;;) {
+    mbar_wait(&full[stage], phase);  // the item's first stage (or the end marker)
+    const int4 it = s_item[stage];
+    if (it.x < 0) break;
+    const int b = it.x, g = it.y, s = it.z;
     const int band = bands[b].band, ldb = bands[b].ldb, cps = bands[b].cps;
     const int nr = groups[(int64_t)band * gmax + g].cnt;
-    if (nr == 0) continue;
     const int nchunks = (ldb + CH - 1) / CH;
     const int q0 = s * cps;
     const int q1 = q0 + cps < nchunks ? q0 + cps : nchunks;

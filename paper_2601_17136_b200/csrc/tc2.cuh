@@ -24,11 +24,6 @@ constexpr int T2_THREADS = (2 + TC_EPI_WARPS) * 32;
 constexpr int T2_BM = 256;                                      // rows per pair tile
 constexpr int T2_GROUP_M = 16;                                  // raster groups of pair tiles
 
-__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
