@@ -107,18 +107,26 @@ inline PFN_cuTensorMapEncodeTiled_v12000 &tc_encode_fn() {
   return f;
 }
 
-inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16, int64_t rows,
-                        int64_t dp) {
+// Resolves the driver's cuTensorMapEncodeTiled once; 0 on success.
+inline int tc_encode_ready() {
   PFN_cuTensorMapEncodeTiled_v12000 &encode = tc_encode_fn();
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) !=
             cudaSuccess ||
         q != cudaDriverEntryPointSuccess || !encode) {
+      encode = nullptr;
       tc_err_slot() = "cuTensorMapEncodeTiled unavailable";
       return 1;
     }
   }
+  return 0;
+}
+
+inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16, int64_t rows,
+                        int64_t dp) {
+  if (tc_encode_ready()) return 1;
+  PFN_cuTensorMapEncodeTiled_v12000 &encode = tc_encode_fn();
   cuuint64_t dims[2] = {(cuuint64_t)dp, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)dp * 2};
   cuuint32_t box[2] = {(cuuint32_t)TC_BK, 128u};
@@ -140,15 +148,17 @@ inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, boo
   return 0;
 }
 
-// fp32 [m x ncov] view of out (row pitch ldo floats, a multiple of 4) for the TMA stores.
-inline int tc_make_out_map(TcGemm &g, float *out, int64_t m, int64_t ncov, int64_t ldo) {
+// [m x ncov] view of out (row pitch ldo elements) for the TMA stores: fp32 boxes of 32 rows x 16
+// columns (ldo % 4 == 0), or with half_out fp16 boxes of 32 x 32 (ldo % 8 == 0); 64-byte swizzle.
+inline int tc_make_out_map(TcGemm &g, void *out, int64_t m, int64_t ncov, int64_t ldo, bool half_out = false) {
   cuuint64_t dims[2] = {(cuuint64_t)ncov, (cuuint64_t)m};
-  cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
-  cuuint32_t box[2] = {16u, 32u};
+  cuuint64_t strides[1] = {(cuuint64_t)ldo * (half_out ? 2 : 4)};
+  cuuint32_t box[2] = {half_out ? 32u : 16u, 32u};
   cuuint32_t es[2] = {1u, 1u};
-  CUresult r = tc_encode_fn()(&g.map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)out, dims, strides,
-                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tc_encode_fn()(&g.map_out, half_out ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                              2, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     tc_err_slot() = "cuTensorMapEncodeTiled (output) failed";
     return 1;

@@ -22,6 +22,7 @@
 #include "sort.cuh"
 #include "spmm.cuh"
 #include "stream.cuh"
+#include "spmm_tc.cuh"
 #include "sym.cuh"
 #include "tc2.cuh"
 #include "update.cuh"
@@ -71,12 +72,17 @@ struct Plan {
   std::vector<SymBand> bands;       // owned bands, ascending I
   std::vector<int32_t> band_desc;   // band -> index into bands, or -1
   bool ssym;                        // f1 on the streaming path (tc2_stream_sym_kernel)
+  // f4 fp16 K storage (spmm_tc.cuh): the f1 bands in fp16, a2 on the tensor cores
+  bool kh;
+  int ts_nsm;                       // max column splits of a band (Srow pitch)
+  std::vector<TsBand> tbands;       // owned bands (same order as bands)
+  std::vector<TsUnit> tunits;
   std::vector<int4> units;          // its work units on this rank
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_Srow, o_tcolpart, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
       o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
 };
 
@@ -95,8 +101,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (p->precision != KKM_PREC_BF16X3 && p->precision != KKM_PREC_FP32_SIMT &&
       p->precision != KKM_PREC_FP16X3)
     return fail(KKM_EINVAL, "unknown precision %d", p->precision);
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 2; ++i)
     if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
+  if (p->kstore != KKM_KSTORE_FP32 && p->kstore != KKM_KSTORE_FP16)
+    return fail(KKM_EINVAL, "unknown kstore %d", p->kstore);
   if (p->incremental != 0 && p->incremental != 1) return fail(KKM_EINVAL, "incremental must be 0 or 1");
   if (p->symmetric != KKM_SYM_AUTO && p->symmetric != KKM_SYM_OFF && p->symmetric != KKM_SYM_ON)
     return fail(KKM_EINVAL, "unknown symmetric mode %d", p->symmetric);
@@ -131,7 +139,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   // f1: symmetric band storage (1D, k <= 16). Bands go to ranks largest first, each to the
   // least-loaded rank (lowest rank on ties): deterministic, area-balanced.
   const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= SP_KPMAX;
-  const bool sym_ok = sym_elig && (p->symmetric == KKM_SYM_ON || n >= 8 * SYM_TB);
+  P.kh = p->kstore == KKM_KSTORE_FP16;
+  const bool sym_ok = sym_elig && (p->symmetric == KKM_SYM_ON || P.kh || n >= 8 * SYM_TB);
   double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
   P.T = (int)ceil_div(n, SYM_TB);
   P.sym_gmax = sym_gmax(P.k);
@@ -166,7 +175,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       P.band_desc[I] = (int32_t)P.bands.size();
       P.bands.push_back(b);
     }
-    kbytes = (double)koff * 4.0;
+    kbytes = (double)koff * (P.kh ? 2.0 : 4.0);
   }
   if (p->path == KKM_PATH_MATERIALIZE) {
     P.materialize = true;
@@ -181,6 +190,9 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     if (!P.tc)
       return fail(KKM_EUNSUP, "the streaming path needs a tensor-core precision (FP16X3 or BF16X3)");
   }
+  if (P.kh && !(P.materialize && sym_ok && P.tc))
+    return fail(KKM_EUNSUP, "fp16 K storage needs a tensor-core precision and the materialised f1 bands "
+                            "(1D, k <= 16, symmetric != OFF)");
   // v1 (one-hot FFMA2) is faster for k <= 16 (5.4 TB/s at k = 10); v2 (sorted groups, shuffle
   // bound at ~3.9 TB/s for any k) replaces v1's ceil(k/16) passes over K for 16 < k <= 64.
   P.spmm_v2 = P.k > SP_KPMAX && P.k <= SG_MAX_K;
@@ -247,10 +259,36 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       if (mine[i]) P.units.push_back(all[i]);
     P.nsplit = 1;
   }
+  P.tbands.clear();
+  P.tunits.clear();
+  P.ts_nsm = 0;
+  if (P.sym && P.kh) {  // f4: units = (band, 512-row slab, <= 16 chunks of 128 columns)
+    int64_t cpoff = 0;
+    for (size_t b = 0; b < P.bands.size(); ++b) {
+      const SymBand &sb = P.bands[b];
+      TsBand t;
+      t.koff = sb.koff;
+      t.cpoff = cpoff;
+      t.band = sb.band;
+      t.ldb = sb.ldb;
+      t.rows = (int32_t)std::min<int64_t>(SYM_TB, n - (int64_t)sb.band * SYM_TB);
+      const int nchunks = (int)ceil_div(t.ldb, TS_CH);
+      t.nsplit = (int)ceil_div(nchunks, TS_SPLIT_CHUNKS);
+      const int slabs = (int)ceil_div(t.rows, TS_SLAB_TILES * TS_ROWS);
+      cpoff += (int64_t)slabs * P.k * std::max(0, t.ldb - SYM_TB);
+      P.ts_nsm = std::max(P.ts_nsm, t.nsplit);
+      for (int sl = 0; sl < slabs; ++sl)
+        for (int sp = 0; sp < t.nsplit; ++sp)
+          P.tunits.push_back(TsUnit{(int32_t)b, sl, sp * TS_SPLIT_CHUNKS,
+                                    std::min(TS_SPLIT_CHUNKS, nchunks - sp * TS_SPLIT_CHUNKS)});
+      P.tbands.push_back(t);
+    }
+  }
   if (P.sym) {  // S partials over all rows (owned bands lie anywhere)
     P.nApad = P.npad;
     P.nsplit = 1;
     for (const SymBand &b : P.bands) P.nsplit = std::max(P.nsplit, (int)b.nsplit);
+    if (P.kh) P.nsplit = 1;  // (Spart unused: Srow instead)
     P.chunks_per_split = 0;
   } else {
     P.bands.clear();
@@ -293,7 +331,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       csdoubles += (size_t)P.k * std::max<int64_t>(0, b.ldb - SYM_TB);
     }
   }
-  P.o_K = P.materialize ? take(std::max<size_t>(kfloats, 1) * 4) : 0;
+  P.o_K = P.materialize ? take(std::max<size_t>(kfloats, 1) * (P.kh ? 2 : 4)) : 0;
   P.o_lab[0] = take((size_t)P.lablen * 4);
   P.o_lab[1] = take((size_t)P.lablen * 4);
   P.o_sizes[0] = take((size_t)P.k * 4);
@@ -355,11 +393,22 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_ngroups = take((size_t)P.T * 4);
     P.o_bands = take(std::max<size_t>(P.bands.size(), 1) * sizeof(SymBand));
     P.o_band_desc = take((size_t)P.T * 4);
-    P.o_colpart = take(std::max<size_t>(cpfloats, 1) * 4);
-    P.o_colsum = take(std::max<size_t>(csdoubles, 1) * 8);
+    P.o_colpart = take(P.kh ? 4 : std::max<size_t>(cpfloats, 1) * 4);
+    P.o_colsum = take(P.kh ? 8 : std::max<size_t>(csdoubles, 1) * 8);
     P.o_work = take(2 * 4);  // spmm_sym's item scheduler
     P.o_gfirst = take((size_t)P.T * (P.k + 1) * 4);
     P.o_Sfin = take((size_t)P.npad * P.k * 8);
+  }
+  if (P.sym && P.kh) {
+    size_t tcp = 0;
+    for (const TsBand &t : P.tbands)
+      tcp += (size_t)ceil_div(t.rows, TS_SLAB_TILES * TS_ROWS) * P.k * std::max(0, t.ldb - SYM_TB);
+    P.o_tmaps = take(std::max<size_t>(P.tbands.size(), 1) * sizeof(CUtensorMap));
+    P.o_tbands = take(std::max<size_t>(P.tbands.size(), 1) * sizeof(TsBand));
+    P.o_tunits = take(std::max<size_t>(P.tunits.size(), 1) * sizeof(TsUnit));
+    P.o_Srow = take((size_t)P.npad * P.ts_nsm * P.k * 4);
+    P.o_tcolpart = take(std::max<size_t>(tcp, 1) * 4);
+    P.o_fxmax = take(16);
   }
   P.total = off;
   return KKM_OK;
@@ -423,6 +472,12 @@ struct kkm_ctx {
   float *colpart = nullptr;
   double *colsum = nullptr, *Sfin = nullptr;
   int32_t *work = nullptr;  // spmm_sym's item scheduler (2 counters, zero between launches)
+  // f4 fp16 K storage
+  CUtensorMap *tmaps = nullptr;
+  TsBand *tbands = nullptr;
+  TsUnit *tunits = nullptr;
+  float *Srow = nullptr, *tcolpart = nullptr;
+  float kscale = 1.f;  // stored K = K * kscale (a power of two)
   // f1 streaming: units, int64 fixed-point S (sorted order), its original-order copy
   int4 *units = nullptr;
   long long *Sfix = nullptr, *Sorig = nullptr, *Sfmine = nullptr;
@@ -668,6 +723,32 @@ int launch_spmm_sym_kp(kkm_ctx *h, const int32_t *labels) {
 int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   const Plan &P = h->P;
   const int k = P.k;
+  if (P.kh) {  // f4: fp16 bands, a2 on the tensor cores (spmm_tc.cuh)
+    static bool attr_set = false;
+    if (!attr_set) {
+      CK(cudaFuncSetAttribute(spmm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM));
+      attr_set = true;
+    }
+    a2_mark(h);
+    if (!P.tunits.empty()) {
+      const int grid = (int)std::min<int64_t>((int64_t)P.tunits.size(), h->num_sms);
+      spmm_tc_kernel<<<grid, TS_THREADS, TS_SMEM, h->st>>>(h->tmaps, h->tbands, h->tunits, (int)P.tunits.size(),
+                                                           labels, P.n, k, P.npad, 1.0f / h->kscale, h->Srow,
+                                                           h->tcolpart, h->work);
+      CKL();
+    }
+    a2_mark(h);
+    ts_reduce_kernel<<<dim3((unsigned)ceil_div(P.npad, 256), (unsigned)k), 256, 0, h->st>>>(
+        h->Srow, h->tcolpart, h->tbands, h->band_desc, P.n, P.npad, k, h->Sfin);
+    CKL();
+    if (P.nranks == 1) {
+      *s_out = h->Sfin;
+      return KKM_OK;
+    }
+    CKN(ncclReduceScatter(h->Sfin, h->Smine, (size_t)P.B * k, ncclDouble, ncclSum, h->comm, h->st));
+    *s_out = h->Smine;
+    return KKM_OK;
+  }
   band_sort_kernel<<<P.T, SYM_TB, (size_t)(32 * k + 2 * (k + 1)) * 4, h->st>>>(
       labels, P.n, k, sym_rows(k), P.sym_gmax, h->perm_b, h->groups, h->ngroups, h->gfirst);
   CKL();
@@ -814,12 +895,14 @@ int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
   return KKM_OK;
 }
 
-int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, float *out, int64_t ldo) {
+// oscale > 0: out is fp16 and receives K * oscale (tensor-core precisions only)
+int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, void *out, int64_t ldo,
+                float oscale = 0.f) {
   const Plan &P = h->P;
   if (m <= 0 || ncov <= 0) return KKM_OK;
   if (P.tc) {
     int rc = tc2_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0,
-                             ncov, h->norms, h->kp, out, ldo, h->st, &h->launches);
+                             ncov, h->norms, h->kp, out, ldo, h->st, &h->launches, oscale);
     if (rc) {
       h->poisoned = true;
       return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
@@ -828,7 +911,7 @@ int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, flo
   }
   dim3 grid((unsigned)ceil_div(ncov, SG_BN), (unsigned)ceil_div(m, SG_BM));
   gemm_simt_kernel<<<grid, 256, 0, h->st>>>(h->Xf, P.ldf, P.n, P.d, i0, m, j0, ncov, h->norms,
-                                             h->kp, out, ldo);
+                                             h->kp, (float *)out, ldo);
   CKL();
   return KKM_OK;
 }
@@ -1001,6 +1084,14 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->colpart = (float *)(w + P.o_colpart);
     h->colsum = (double *)(w + P.o_colsum);
     h->work = (int32_t *)(w + P.o_work);
+    if (P.kh) {
+      h->tmaps = (CUtensorMap *)(w + P.o_tmaps);
+      h->tbands = (TsBand *)(w + P.o_tbands);
+      h->tunits = (TsUnit *)(w + P.o_tunits);
+      h->Srow = (float *)(w + P.o_Srow);
+      h->tcolpart = (float *)(w + P.o_tcolpart);
+      h->fxmax = (float *)(w + P.o_fxmax);
+    }
     h->gfirst = (int32_t *)(w + P.o_gfirst);
     h->Sfin = (double *)(w + P.o_Sfin);
   }
@@ -1103,9 +1194,38 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
                            h->st));
       CK(cudaMemcpyAsync(h->band_desc, P.band_desc.data(), (size_t)P.T * 4, cudaMemcpyHostToDevice, h->st));
       CK(cudaMemsetAsync(h->work, 0, 2 * 4, h->st));
+      if (P.kh) {  // f4: storage scale 2^e with |K| 2^e <= 60000 (|K_ij| <= max_i K_ii, bounded as for ssym)
+        max_norm_kernel<<<1, 1024, 0, h->st>>>(h->norms, P.n, h->fxmax);
+        CKL();
+        float mx = 0.f;
+        CK(cudaMemcpyAsync(&mx, h->fxmax, 4, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        double kmax = 1.0;
+        if (p->kind == KKM_KERNEL_LINEAR) kmax = (double)mx;
+        if (p->kind == KKM_KERNEL_POLY) kmax = std::pow(p->gamma * mx + std::fabs(p->coef0), (double)p->degree);
+        const int e = std::max(-100, std::min(100, (int)std::floor(std::log2(60000.0 / std::max(1e-30, kmax * 1.0001)))));
+        h->kscale = std::ldexp(1.0f, e);
+        std::vector<CUtensorMap> maps(P.tbands.size());
+        for (size_t b = 0; b < P.tbands.size(); ++b)
+          if (ts_encode_band(&maps[b], (const __half *)h->K + P.tbands[b].koff, P.tbands[b].rows, P.tbands[b].ldb))
+            return fail(KKM_ECUDA, "%s", tc_gemm_error());
+        if (!maps.empty()) {
+          CK(cudaMemcpyAsync(h->tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
+          CK(cudaMemcpyAsync(h->tbands, P.tbands.data(), P.tbands.size() * sizeof(TsBand), cudaMemcpyHostToDevice,
+                             h->st));
+        }
+        if (!P.tunits.empty())
+          CK(cudaMemcpyAsync(h->tunits, P.tunits.data(), P.tunits.size() * sizeof(TsUnit), cudaMemcpyHostToDevice,
+                             h->st));
+        CK(cudaStreamSynchronize(h->st));  // (host vectors go out of scope)
+      }
       for (const SymBand &b : P.bands) {
         const int64_t i0 = (int64_t)b.band * SYM_TB;
-        CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, h->K + b.koff, b.ldb));
+        if (P.kh)
+          CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, (__half *)h->K + b.koff, b.ldb,
+                          h->kscale));
+        else
+          CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, h->K + b.koff, b.ldb));
       }
     } else if (P.materialize) {
       CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));

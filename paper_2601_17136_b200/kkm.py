@@ -18,6 +18,7 @@ KERNEL_LINEAR, KERNEL_POLY, KERNEL_GAUSSIAN = 0, 1, 2
 PATH_AUTO, PATH_MATERIALIZE, PATH_STREAM = 0, 1, 2
 PREC_BF16X3, PREC_FP32_SIMT, PREC_FP16X3 = 0, 1, 2
 SYM_AUTO, SYM_OFF, SYM_ON = 0, 1, 2
+KSTORE_FP32, KSTORE_FP16 = 0, 1
 DBG_E, DBG_CNORM, DBG_SIZES, DBG_DIAG, DBG_DFULL, DBG_LABELS_PREV = range(6)
 PHASES = ("init_prep", "init_gemm", "spmm", "cnorm", "assign", "a2_kernel")
 
@@ -34,7 +35,8 @@ class KKMParams(ctypes.Structure):
                 ("stop_on_no_change", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("timing", ctypes.c_int32),
                 ("grid_rows", ctypes.c_int32), ("symmetric", ctypes.c_int32),
-                ("incremental", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("incremental", ctypes.c_int32), ("kstore", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 _lib = None
@@ -142,7 +144,8 @@ class KernelKMeans:
                  stop_on_no_change: bool = False, path: int = PATH_AUTO,
                  precision: int = PREC_FP16X3, timing: bool = False, init_labels=None,
                  rank: int = 0, nranks: int = 1, comm=None, stream=None, device=None,
-                 workspace=None, grid_rows: int = 1, symmetric: int = SYM_AUTO, incremental: bool = False):
+                 workspace=None, grid_rows: int = 1, symmetric: int = SYM_AUTO, incremental: bool = False,
+                 kstore: int = KSTORE_FP32):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
@@ -157,6 +160,7 @@ class KernelKMeans:
         p.grid_rows = grid_rows
         p.symmetric = symmetric
         p.incremental = int(incremental)
+        p.kstore = kstore
         self.params = p
         self.max_iter = max_iter
         nb = workspace_size(p, self.n, self.d, rank, nranks)

@@ -103,6 +103,26 @@ def test_workspace_size_and_errors():
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(q, 100, 4)
     q = kkm.default_params()
-    q.reserved[2] = 1
+    q.reserved[1] = 1
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(q, 100, 4)
+    # f4 fp16 K storage: half the band bytes, no fp32 column partials; only where it applies
+    q = kkm.default_params()
+    q.k = 10
+    q.kstore = kkm.KSTORE_FP16
+    nb_h = kkm.workspace_size(q, 60000, 784)
+    assert 0.45 * nb_sym1 < nb_h < 0.5 * nb_sym1
+    q.kstore = 2
+    with pytest.raises(kkm.KKMError, match="EINVAL"):
+        kkm.workspace_size(q, 100, 4)
+    for field, value in (("precision", kkm.PREC_FP32_SIMT), ("symmetric", kkm.SYM_OFF),
+                         ("path", kkm.PATH_STREAM), ("grid_rows", 2)):
+        q = kkm.default_params()
+        q.kstore = kkm.KSTORE_FP16
+        setattr(q, field, value)
+        with pytest.raises(kkm.KKMError, match="EUNSUP"):
+            kkm.workspace_size(q, 60000, 784, rank=0, nranks=2 if field == "grid_rows" else 1)
+    q = kkm.default_params()
+    q.kstore, q.k = kkm.KSTORE_FP16, 17
+    with pytest.raises(kkm.KKMError, match="EUNSUP"):
+        kkm.workspace_size(q, 60000, 784)

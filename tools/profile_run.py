@@ -18,6 +18,7 @@ ap.add_argument("--precision", default="fp16x3")
 ap.add_argument("--path", default="auto", choices=["auto", "mat", "stream"])
 ap.add_argument("--k", type=int, default=0, help="override the cluster count")
 ap.add_argument("--full-k", action="store_true", help="store full K rows (KKM_SYM_OFF) instead of the f1 bands")
+ap.add_argument("--kstore", default="fp32", choices=["fp32", "fp16"], help="f4: materialised K storage type")
 a = ap.parse_args()
 X, cfg = synth.make_config(a.config, n=a.n or None)
 prec = {"fp16x3": kkm.PREC_FP16X3, "bf16x3": kkm.PREC_BF16X3, "fp32": kkm.PREC_FP32_SIMT}[a.precision]
@@ -26,7 +27,8 @@ if a.k:
     cfg["k"] = a.k
 h = kkm.KernelKMeans(torch.from_numpy(X).cuda(), X.shape[0], cfg["k"], cfg["kind"], cfg["gamma"],
                      cfg["coef0"], cfg["degree"], max_iter=a.iters, precision=prec, timing=True, path=path,
-                     symmetric=kkm.SYM_OFF if a.full_k else kkm.SYM_AUTO)
+                     symmetric=kkm.SYM_OFF if a.full_k else kkm.SYM_AUTO,
+                     kstore=kkm.KSTORE_FP16 if a.kstore == "fp16" else kkm.KSTORE_FP32)
 it, J, ch = h.fit()
 torch.cuda.synchronize()
 ph = h.phase_ms()
@@ -43,14 +45,16 @@ if a.path == "stream":
     print(line)
 else:
     sym = not a.full_k and cfg["k"] <= 16
+    eb = 2 if a.kstore == "fp16" else 4
     if sym:  # f1 bands: ~n^2/2 useful flops and K bytes
         TB, kb = 1024, 0
         for I in range(-(-n // TB)):
-            kb += min(TB, n - I * TB) * (-(-(n - I * TB) // 32) * 32) * 4
-        flops = 2.0 * d * kb / 4
+            kb += min(TB, n - I * TB) * (-(-(n - I * TB) // 32) * 32) * eb
+        flops = 2.0 * d * kb / eb
     else:
         kb = n * (-(-n // 32) * 32) * 4
     print(f"a1 GEMM {ph['init_gemm']:.2f} ms -> useful {flops / (ph['init_gemm'] * 1e-3) / 1e12:.1f} TFLOP/s"
           f" ({'f1 bands' if sym else 'full K'})")
     per = ph["spmm"] / it
-    print(f"a2 SpMM k={cfg['k']} {per:.3f} ms/iter -> K bytes {kb / 1e9:.2f} GB: {kb / (per * 1e-3) / 1e9:.0f} GB/s")
+    print(f"a2 SpMM k={cfg['k']} {per:.3f} ms/iter -> K bytes {kb / 1e9:.2f} GB: {kb / (per * 1e-3) / 1e9:.0f} GB/s"
+          f" (a2 kernel {ph['a2_kernel'] / it:.3f} ms: {kb / (ph['a2_kernel'] / it * 1e-3) / 1e9:.0f} GB/s)")

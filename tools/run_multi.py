@@ -27,6 +27,8 @@ cases = [(name, n, iters, path, g, {}) for (name, n, iters) in [("har200k", 3001
 # 1D extras: f1 bands at a small n, incremental S (f3) and stop-on-no-change -- the latter two
 # branch on the (global) changed count, so every rank must take the same path
 cases += [("har200k", 3001, 6, kkm.PATH_MATERIALIZE, 1, dict(symmetric=kkm.SYM_ON)),
+          ("har200k", 3001, 6, kkm.PATH_MATERIALIZE, 1, dict(kstore=kkm.KSTORE_FP16)),
+          ("mnist60k", 2500, 5, kkm.PATH_MATERIALIZE, 1, dict(kstore=kkm.KSTORE_FP16)),
           ("mnist60k", 2500, 12, kkm.PATH_MATERIALIZE, 1, dict(incremental=True)),
           ("mnist60k", 2500, 12, kkm.PATH_STREAM, 1, dict(incremental=True)),
           ("rings", 1000, 60, kkm.PATH_MATERIALIZE, 1, dict(stop_on_no_change=True)),
