@@ -205,10 +205,12 @@ def run_ours(args):
                  "fp32": kkm.PREC_FP32_SIMT}[args.precision]
     kw = dict(kind=cfg["kind"], gamma=1.0, coef0=1.0, degree=2, max_iter=iters,
               precision=precision, rank=rank, nranks=world, comm=comm, timing=True,
-              symmetric=kkm.SYM_AUTO if args.symmetric == "auto" else kkm.SYM_OFF)
+              symmetric=kkm.SYM_AUTO if args.symmetric == "auto" else kkm.SYM_OFF,
+              kstore={"auto": kkm.KSTORE_AUTO, "fp32": kkm.KSTORE_FP32, "fp16x2": kkm.KSTORE_FP16X2}[args.kstore])
     p = kkm.default_params()
     p.kind, p.k, p.max_iter, p.precision = cfg["kind"], k, iters, precision
     p.symmetric = kw["symmetric"]
+    p.kstore = kw["kstore"]
     ws = torch.empty(kkm.workspace_size(p, n, d, rank, world), dtype=torch.uint8, device=dev)
     Xd = torch.from_numpy(X_local).to(dev)
     Xh = torch.from_numpy(X_local).pin_memory()
@@ -294,10 +296,11 @@ def run_ours(args):
     if kh_ok:
         p.kstore = kkm.KSTORE_FP16
         ws_kh = torch.empty(kkm.workspace_size(p, n, d, rank, world), dtype=torch.uint8, device=dev)
-        p.kstore = kkm.KSTORE_FP32
+        p.kstore = kw["kstore"]
+        kw_kh = dict(kw, kstore=kkm.KSTORE_FP16)
 
         def kh_run():
-            hk = kkm.KernelKMeans(Xd, n, k, workspace=ws_kh, stream=stream, kstore=kkm.KSTORE_FP16, **kw)
+            hk = kkm.KernelKMeans(Xd, n, k, workspace=ws_kh, stream=stream, **kw_kh)
             _, Jr, _ = hk.fit()
             phr = hk.phase_ms()
             hk.destroy()
@@ -330,6 +333,11 @@ def run_ours(args):
         nloc = min(B, n - 0)
         ldk = -(-n // 32) * 32
         sym = args.symmetric == "auto" and k <= 16
+        # the f1 bands as hi + lo fp16 planes with a2 on the tensor cores (KSTORE_AUTO's choice
+        # for a tensor-core precision), or fp32 bands with the one-hot FFMA2 kernel
+        tc_a2 = sym and args.kstore != "fp32" and precision != kkm.PREC_FP32_SIMT
+        a2_kernel = ("spmm_tc_kernel (a2 on the tensor cores over the f1 bands as hi + lo fp16 planes)" if tc_a2
+                     else "spmm_sym_kernel (a2 on the f1 fp32 bands)" if sym else "spmm_onehot_kernel (a2)")
         if sym:  # f1: the rank's upper-triangle bands (K read once; the column partials are
             # implementation traffic, visible in `traffic`) + S partials of all rows
             kfl = sym_band_share(n, world, 0)
@@ -348,7 +356,8 @@ def run_ours(args):
             with open(tp) as f:
                 caps = json.load(f).get("captures", [])
             for cap in caps:
-                if abs(cap.get("algorithmic_bytes", 0) - spmm_bytes) <= 0.01 * spmm_bytes:
+                if a2_kernel.startswith(cap.get("kernel", "").split("<")[0]) and \
+                        abs(cap.get("algorithmic_bytes", 0) - spmm_bytes) <= 0.01 * spmm_bytes:
                     traffic = cap.get("bytes_per_launch")
         tensor = precision in (kkm.PREC_BF16X3, kkm.PREC_FP16X3)
         # 3 dense 16-bit MMAs per useful product: useful-flop peak = measured bf16 dense / 3
@@ -362,16 +371,19 @@ def run_ours(args):
             "total_clustering_s": step_ms / 1e3,
             "config": {"workload": workload_desc(cfg, iters), "n": n, "d": d, "k": k,
                        "iterations": iters, "precision_a1": args.precision,
+                       "k_storage": ("f1 bands as hi + lo fp16 planes (hi = RN(K 2^e), lo = RN(K 2^e - hi): "
+                                     "~2^-22 relative, fp32-class; DESIGN A27)" if tc_a2 else
+                                     "fp32 f1 bands" if sym else "fp32 full K rows"),
                        "parallelism": f"1D row shards x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (14.4/N GB of K streamed per iteration)"},
-            "roofline": {"kernel": "spmm_sym_kernel (a2 on the f1 upper-triangle bands)" if sym
-                         else "spmm_onehot_kernel (a2)",
+            "roofline": {"kernel": a2_kernel,
                          "bound": "hbm", "achieved": a2k_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": a2k_gbs / peaks["hbm_gbs"], "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_launch": spmm_bytes, "launch_ms": a2k_ms,
                          "timing": "CUDA events around the kernel's launches on the handle's stream, "
                                    "inside the timed steps (kkm_phase_ms a2_kernel)"},
-            "roofline_a2_phase": {"what": ("band_sort + spmm_sym + sym_colsum + sym_reduce" if sym
+            "roofline_a2_phase": {"what": ("S memset + spmm_tc + fixed-point S to fp64" if tc_a2 else
+                                           "band_sort + spmm_sym + sym_colsum + sym_reduce" if sym
                                            else "a2 launches"), "achieved": spmm_gbs,
                                   "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": spmm_gbs / peaks["hbm_gbs"],
                                   "phase_ms": spmm_ms},
@@ -431,6 +443,9 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=1024)
     ap.add_argument("--symmetric", choices=["auto", "off"], default="auto",
                     help="auto: upper-triangle K bands (f1); off: full K rows")
+    ap.add_argument("--kstore", choices=["auto", "fp32", "fp16x2"], default="auto",
+                    help="f1 band storage: auto = hi + lo fp16 planes (fp32-class, a2 on the tensor cores) "
+                         "with a tensor-core precision; fp32 = fp32 bands (one-hot FFMA2 a2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

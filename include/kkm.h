@@ -74,8 +74,10 @@ extern "C" {
 #define KKM_SYM_AUTO 0
 #define KKM_SYM_OFF 1
 #define KKM_SYM_ON 2
-#define KKM_KSTORE_FP32 0
-#define KKM_KSTORE_FP16 1
+#define KKM_KSTORE_AUTO 0
+#define KKM_KSTORE_FP32 1
+#define KKM_KSTORE_FP16 2
+#define KKM_KSTORE_FP16X2 3
 
 /* ---- precision of the a1 contraction (reading A9) ----------------------- */
 #define KKM_PREC_BF16X3 0    /* tcgen05 kind::f16: hi*hi + hi*lo + lo*hi, bf16 split of x;
@@ -131,17 +133,23 @@ typedef struct kkm_params {
                               their old label (~4 m n d flops instead of a full pass;
                               exact up to rounding, S kept in fp64); otherwise a full
                               pass. 1D and a tensor-core precision only (KKM_EUNSUP). */
-  int32_t kstore;          /* f4, materialised K storage. KKM_KSTORE_FP32 (0, default):
-                              fp32 (the paper's precision). KKM_KSTORE_FP16 (1): the
-                              f1 upper-triangle bands stored in fp16, scaled by a power of
-                              two 2^e chosen from a bound on |K| (linear: max ||x||^2; poly:
-                              (gamma max ||x||^2 + |coef0|)^degree; Gaussian: 1) so that
-                              |K| 2^e <= 60000; a2 then runs on the tensor cores
-                              (spmm_tc.cuh) and reads half the bytes. Each stored value has
-                              a relative rounding error <= 2^-11 (DESIGN A27 states the
-                              resulting E / D / J bounds). Needs a tensor-core precision, a
-                              materialised 1D run with k <= 16 and symmetric != OFF (it
-                              implies the f1 bands for any n); else KKM_EUNSUP.           */
+  int32_t kstore;          /* f4, materialised K storage of the f1 bands.
+                              KKM_KSTORE_FP32 (1): fp32 (the paper's precision), a2 by
+                              the one-hot FFMA2 kernel (sym.cuh).
+                              KKM_KSTORE_FP16X2 (3): two fp16 planes hi = RN(K 2^e),
+                              lo = RN(K 2^e - hi), with 2^e the largest power of two such that
+                              a bound on |K| times 2^e is <= 60000 (linear: max ||x||^2; poly:
+                              (gamma max ||x||^2 + |coef0|)^degree; Gaussian: 1): 4 bytes per
+                              value like fp32, relative error <= ~2^-22 (fp32-class), and a2 on
+                              the tensor cores (spmm_tc.cuh) with S summed in int64 fixed point.
+                              KKM_KSTORE_FP16 (2): the hi plane only -- half the bytes, each
+                              value rounded to 2^-11 relative (DESIGN A27 bounds E / D / J).
+                              KKM_KSTORE_AUTO (0, default): FP16X2 whenever the run stores the
+                              f1 bands with a tensor-core precision (1D, k <= 16; see
+                              `symmetric`), else FP32.
+                              FP16 and FP16X2 need a tensor-core precision and a materialised
+                              1D run with k <= 16 and symmetric != OFF (they imply the f1 bands
+                              for any n); else KKM_EUNSUP.                                */
   int32_t reserved[2];     /* must be zero                                         */
 } kkm_params;
 

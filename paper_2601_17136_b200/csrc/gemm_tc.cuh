@@ -91,7 +91,7 @@ struct TcGemm {
   const void *hi = nullptr, *lo = nullptr;  // operands the tensor maps describe
   bool fp16 = false;
   CUtensorMap map_hi, map_lo;
-  CUtensorMap map_out;                        // re-encoded per launch (cheap, host only)
+  CUtensorMap map_out, map_out2;              // re-encoded per launch (cheap, host only)
   bool attr = false;
   int num_sms = 0;
 };

@@ -59,6 +59,7 @@ struct Plan {
   bool spmm_v2;                 // materialised a2 with label-sorted 32-column groups (k <= 64)
   int nsplit, chunks_per_split, nfin, nspmm_pass;
   int64_t rows_per_block;
+  size_t kelems;       // materialised K elements (per 16-bit plane)
   int64_t s_rows_pad;  // row pitch of the S (or S partials) finalize reads
   bool need_smine;     // a reduce-scatter delivers S of the own 1D block (Smine)
   // f3 incremental S: moved-point set of at most dmax points
@@ -74,6 +75,7 @@ struct Plan {
   bool ssym;                        // f1 on the streaming path (tc2_stream_sym_kernel)
   // f4 fp16 K storage (spmm_tc.cuh): the f1 bands in fp16, a2 on the tensor cores
   bool kh;
+  int kplanes;                      // 16-bit planes per K value: 1 (FP16) or 2 (FP16X2: hi + lo)
   int ts_nsm;                       // max column splits of a band (Srow pitch)
   std::vector<TsBand> tbands;       // owned bands (same order as bands)
   std::vector<TsUnit> tunits;
@@ -82,7 +84,7 @@ struct Plan {
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_Srow, o_tcolpart, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
       o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
 };
 
@@ -103,7 +105,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     return fail(KKM_EINVAL, "unknown precision %d", p->precision);
   for (int i = 0; i < 2; ++i)
     if (p->reserved[i]) return fail(KKM_EINVAL, "reserved params must be zero");
-  if (p->kstore != KKM_KSTORE_FP32 && p->kstore != KKM_KSTORE_FP16)
+  if (p->kstore < KKM_KSTORE_AUTO || p->kstore > KKM_KSTORE_FP16X2)
     return fail(KKM_EINVAL, "unknown kstore %d", p->kstore);
   if (p->incremental != 0 && p->incremental != 1) return fail(KKM_EINVAL, "incremental must be 0 or 1");
   if (p->symmetric != KKM_SYM_AUTO && p->symmetric != KKM_SYM_OFF && p->symmetric != KKM_SYM_ON)
@@ -139,7 +141,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   // f1: symmetric band storage (1D, k <= 16). Bands go to ranks largest first, each to the
   // least-loaded rank (lowest rank on ties): deterministic, area-balanced.
   const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= SP_KPMAX;
-  P.kh = p->kstore == KKM_KSTORE_FP16;
+  P.kh = p->kstore == KKM_KSTORE_FP16 || p->kstore == KKM_KSTORE_FP16X2;  // AUTO: decided below
+  P.kplanes = p->kstore == KKM_KSTORE_FP16 ? 1 : 2;
   const bool sym_ok = sym_elig && (p->symmetric == KKM_SYM_ON || P.kh || n >= 8 * SYM_TB);
   double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
   P.T = (int)ceil_div(n, SYM_TB);
@@ -175,7 +178,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       P.band_desc[I] = (int32_t)P.bands.size();
       P.bands.push_back(b);
     }
-    kbytes = (double)koff * (P.kh ? 2.0 : 4.0);
+    kbytes = (double)koff * (P.kh ? 2.0 * P.kplanes : 4.0);
   }
   if (p->path == KKM_PATH_MATERIALIZE) {
     P.materialize = true;
@@ -190,8 +193,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     if (!P.tc)
       return fail(KKM_EUNSUP, "the streaming path needs a tensor-core precision (FP16X3 or BF16X3)");
   }
+  // AUTO: the hi + lo fp16 planes (fp32-class, a2 on the tensor cores) whenever the bands are stored
+  if (p->kstore == KKM_KSTORE_AUTO && P.materialize && sym_ok && P.tc) P.kh = true;
   if (P.kh && !(P.materialize && sym_ok && P.tc))
-    return fail(KKM_EUNSUP, "fp16 K storage needs a tensor-core precision and the materialised f1 bands "
+    return fail(KKM_EUNSUP, "16-bit K storage needs a tensor-core precision and the materialised f1 bands "
                             "(1D, k <= 16, symmetric != OFF)");
   // v1 (one-hot FFMA2) is faster for k <= 16 (5.4 TB/s at k = 10); v2 (sorted groups, shuffle
   // bound at ~3.9 TB/s for any k) replaces v1's ceil(k/16) passes over K for 16 < k <= 64.
@@ -263,19 +268,16 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.tunits.clear();
   P.ts_nsm = 0;
   if (P.sym && P.kh) {  // f4: units = (band, 512-row slab, <= 16 chunks of 128 columns)
-    int64_t cpoff = 0;
     for (size_t b = 0; b < P.bands.size(); ++b) {
       const SymBand &sb = P.bands[b];
       TsBand t;
       t.koff = sb.koff;
-      t.cpoff = cpoff;
       t.band = sb.band;
       t.ldb = sb.ldb;
       t.rows = (int32_t)std::min<int64_t>(SYM_TB, n - (int64_t)sb.band * SYM_TB);
       const int nchunks = (int)ceil_div(t.ldb, TS_CH);
       t.nsplit = (int)ceil_div(nchunks, TS_SPLIT_CHUNKS);
       const int slabs = (int)ceil_div(t.rows, TS_SLAB_TILES * TS_ROWS);
-      cpoff += (int64_t)slabs * P.k * std::max(0, t.ldb - SYM_TB);
       P.ts_nsm = std::max(P.ts_nsm, t.nsplit);
       for (int sl = 0; sl < slabs; ++sl)
         for (int sp = 0; sp < t.nsplit; ++sp)
@@ -288,7 +290,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.nApad = P.npad;
     P.nsplit = 1;
     for (const SymBand &b : P.bands) P.nsplit = std::max(P.nsplit, (int)b.nsplit);
-    if (P.kh) P.nsplit = 1;  // (Spart unused: Srow instead)
+    if (P.kh) P.nsplit = 1;  // (Spart unused: spmm_tc sums S in int64 fixed point)
     P.chunks_per_split = 0;
   } else {
     P.bands.clear();
@@ -331,7 +333,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       csdoubles += (size_t)P.k * std::max<int64_t>(0, b.ldb - SYM_TB);
     }
   }
-  P.o_K = P.materialize ? take(std::max<size_t>(kfloats, 1) * (P.kh ? 2 : 4)) : 0;
+  P.o_K = P.materialize ? take(std::max<size_t>(kfloats, 1) * (P.kh ? 2 * P.kplanes : 4)) : 0;
+  P.kelems = kfloats;  // elements per plane
   P.o_lab[0] = take((size_t)P.lablen * 4);
   P.o_lab[1] = take((size_t)P.lablen * 4);
   P.o_sizes[0] = take((size_t)P.k * 4);
@@ -400,14 +403,12 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_Sfin = take((size_t)P.npad * P.k * 8);
   }
   if (P.sym && P.kh) {
-    size_t tcp = 0;
-    for (const TsBand &t : P.tbands)
-      tcp += (size_t)ceil_div(t.rows, TS_SLAB_TILES * TS_ROWS) * P.k * std::max(0, t.ldb - SYM_TB);
-    P.o_tmaps = take(std::max<size_t>(P.tbands.size(), 1) * sizeof(CUtensorMap));
+    P.o_tmaps = take(std::max<size_t>(P.tbands.size() * P.kplanes, 1) * sizeof(CUtensorMap));
     P.o_tbands = take(std::max<size_t>(P.tbands.size(), 1) * sizeof(TsBand));
     P.o_tunits = take(std::max<size_t>(P.tunits.size(), 1) * sizeof(TsUnit));
-    P.o_Srow = take((size_t)P.npad * P.ts_nsm * P.k * 4);
-    P.o_tcolpart = take(std::max<size_t>(tcp, 1) * 4);
+    P.o_tSfix = take((size_t)P.npad * P.k * 8);  // int64 fixed-point S, [label][row]
+    P.o_tSint = P.nranks > 1 ? take((size_t)P.npad * P.k * 8) : 0;
+    P.o_tSmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
     P.o_fxmax = take(16);
   }
   P.total = off;
@@ -476,8 +477,9 @@ struct kkm_ctx {
   CUtensorMap *tmaps = nullptr;
   TsBand *tbands = nullptr;
   TsUnit *tunits = nullptr;
-  float *Srow = nullptr, *tcolpart = nullptr;
+  long long *tSfix = nullptr, *tSint = nullptr, *tSmine = nullptr;
   float kscale = 1.f;  // stored K = K * kscale (a power of two)
+  double tfxm = 1.0, tfx_inv = 1.0;  // S fixed point: drained (scaled) sums x tfxm; back x tfx_inv
   // f1 streaming: units, int64 fixed-point S (sorted order), its original-order copy
   int4 *units = nullptr;
   long long *Sfix = nullptr, *Sorig = nullptr, *Sfmine = nullptr;
@@ -723,29 +725,35 @@ int launch_spmm_sym_kp(kkm_ctx *h, const int32_t *labels) {
 int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   const Plan &P = h->P;
   const int k = P.k;
-  if (P.kh) {  // f4: fp16 bands, a2 on the tensor cores (spmm_tc.cuh)
+  if (P.kh) {  // f4: 16-bit bands, a2 on the tensor cores (spmm_tc.cuh), S in int64 fixed point
     static bool attr_set = false;
     if (!attr_set) {
       CK(cudaFuncSetAttribute(spmm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM));
       attr_set = true;
     }
+    CK(cudaMemsetAsync(h->tSfix, 0, (size_t)P.npad * k * 8, h->st));
     a2_mark(h);
     if (!P.tunits.empty()) {
       const int grid = (int)std::min<int64_t>((int64_t)P.tunits.size(), h->num_sms);
       spmm_tc_kernel<<<grid, TS_THREADS, TS_SMEM, h->st>>>(h->tmaps, h->tbands, h->tunits, (int)P.tunits.size(),
-                                                           labels, P.n, k, P.npad, 1.0f / h->kscale, h->Srow,
-                                                           h->tcolpart, h->work);
+                                                           labels, P.n, k, P.npad, h->tfxm, h->tSfix, h->work,
+                                                           P.kplanes);
       CKL();
     }
     a2_mark(h);
-    ts_reduce_kernel<<<dim3((unsigned)ceil_div(P.npad, 256), (unsigned)k), 256, 0, h->st>>>(
-        h->Srow, h->tcolpart, h->tbands, h->band_desc, P.n, P.npad, k, h->Sfin);
-    CKL();
+    const unsigned gr = (unsigned)ceil_div(P.npad * k, 256);
     if (P.nranks == 1) {
+      ts_fix_out_kernel<<<gr, 256, 0, h->st>>>(h->tSfix, P.n, P.npad, k, h->tfx_inv, nullptr, h->Sfin);
+      CKL();
       *s_out = h->Sfin;
       return KKM_OK;
     }
-    CKN(ncclReduceScatter(h->Sfin, h->Smine, (size_t)P.B * k, ncclDouble, ncclSum, h->comm, h->st));
+    // exact: the int64 sums of the ranks' contributions, any order gives the same bits
+    ts_fix_out_kernel<<<gr, 256, 0, h->st>>>(h->tSfix, P.n, P.npad, k, 1.0, h->tSint, nullptr);
+    CKL();
+    CKN(ncclReduceScatter(h->tSint, h->tSmine, (size_t)P.B * k, ncclInt64, ncclSum, h->comm, h->st));
+    fx_to_double_kernel<<<(unsigned)ceil_div(P.B * k, 256), 256, 0, h->st>>>(h->tSmine, P.B * k, h->tfx_inv,
+                                                                           h->Smine);
     *s_out = h->Smine;
     return KKM_OK;
   }
@@ -897,12 +905,12 @@ int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
 
 // oscale > 0: out is fp16 and receives K * oscale (tensor-core precisions only)
 int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, void *out, int64_t ldo,
-                float oscale = 0.f) {
+                float oscale = 0.f, void *out_lo = nullptr) {
   const Plan &P = h->P;
   if (m <= 0 || ncov <= 0) return KKM_OK;
   if (P.tc) {
     int rc = tc2_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0,
-                             ncov, h->norms, h->kp, out, ldo, h->st, &h->launches, oscale);
+                             ncov, h->norms, h->kp, out, ldo, h->st, &h->launches, oscale, out_lo);
     if (rc) {
       h->poisoned = true;
       return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
@@ -1088,8 +1096,11 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
       h->tmaps = (CUtensorMap *)(w + P.o_tmaps);
       h->tbands = (TsBand *)(w + P.o_tbands);
       h->tunits = (TsUnit *)(w + P.o_tunits);
-      h->Srow = (float *)(w + P.o_Srow);
-      h->tcolpart = (float *)(w + P.o_tcolpart);
+      h->tSfix = (long long *)(w + P.o_tSfix);
+      if (P.nranks > 1) {
+        h->tSint = (long long *)(w + P.o_tSint);
+        h->tSmine = (long long *)(w + P.o_tSmine);
+      }
       h->fxmax = (float *)(w + P.o_fxmax);
     }
     h->gfirst = (int32_t *)(w + P.o_gfirst);
@@ -1205,10 +1216,16 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         if (p->kind == KKM_KERNEL_POLY) kmax = std::pow(p->gamma * mx + std::fabs(p->coef0), (double)p->degree);
         const int e = std::max(-100, std::min(100, (int)std::floor(std::log2(60000.0 / std::max(1e-30, kmax * 1.0001)))));
         h->kscale = std::ldexp(1.0f, e);
-        std::vector<CUtensorMap> maps(P.tbands.size());
+        // S as int64 fixed point 2^s with n max|K| 2^s < 2^61 (as the streaming f1 kernel)
+        const int sh = (int)std::floor(61.0 - std::log2(std::max(1e-300, (double)P.n * kmax * 1.0001)));
+        h->tfxm = std::ldexp(1.0, sh - e);
+        h->tfx_inv = std::ldexp(1.0, -sh);
+        std::vector<CUtensorMap> maps(P.tbands.size() * P.kplanes);
         for (size_t b = 0; b < P.tbands.size(); ++b)
-          if (ts_encode_band(&maps[b], (const __half *)h->K + P.tbands[b].koff, P.tbands[b].rows, P.tbands[b].ldb))
-            return fail(KKM_ECUDA, "%s", tc_gemm_error());
+          for (int pl = 0; pl < P.kplanes; ++pl)
+            if (ts_encode_band(&maps[b * P.kplanes + pl], (const __half *)h->K + pl * P.kelems + P.tbands[b].koff,
+                               P.tbands[b].rows, P.tbands[b].ldb))
+              return fail(KKM_ECUDA, "%s", tc_gemm_error());
         if (!maps.empty()) {
           CK(cudaMemcpyAsync(h->tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
           CK(cudaMemcpyAsync(h->tbands, P.tbands.data(), P.tbands.size() * sizeof(TsBand), cudaMemcpyHostToDevice,
@@ -1223,7 +1240,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         const int64_t i0 = (int64_t)b.band * SYM_TB;
         if (P.kh)
           CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, (__half *)h->K + b.koff, b.ldb,
-                          h->kscale));
+                          h->kscale, P.kplanes > 1 ? (__half *)h->K + P.kelems + b.koff : nullptr));
         else
           CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, h->K + b.koff, b.ldb));
       }

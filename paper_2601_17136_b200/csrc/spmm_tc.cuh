@@ -12,14 +12,17 @@
 // kernel is a pure HBM stream of half the bytes of the fp32 bands.
 //
 // Work unit = (owned band, 512-row slab = 4 row tiles, split of <= 16 chunks of 128 columns).
-// Per chunk: the 4 row tiles' row MMAs accumulate into D_row[tile] (over the unit's chunks), their
-// column MMAs into D_col (over the 4 tiles; skipped on the diagonal block K_II, which the row
-// part covers whole). D_col is drained per chunk to colpart[band][slab][c][column] and D_row at
-// the unit's end to Srow[split][c][row] (fp32, both multiplied by 2^-e, the storage scale);
-// ts_reduce_kernel sums them in fixed order (fp64), like sym_reduce.
+// Per chunk and row tile the row MMAs go to D_row[tile] and the column MMAs to D_col (skipped on
+// the diagonal block K_II, which the row part covers whole); an accumulator holds 2 chunks (row
+// sums) or 2 row tiles (column sums) and is then drained into fp64 registers: the column sums of
+// a chunk over the slab's tiles and the row sums over the unit's chunks are added to S of their
+// points as int64 fixed point (value x 2^-e x 2^s, `red.global.add.u64`): integer addition is
+// associative, so S is bitwise independent of the schedule and of the rank count (as the
+// streaming f1 kernel), and no partial arrays or reduction kernel are needed.
 //
-// Warp roles (192 threads): warp 0 = producer (lane 0: unit scheduler + TMA; all lanes build the
-// one-hot tiles), warp 1 = MMA issuer (lane 0) + TMEM owner, warps 2-5 = TMEM drains.
+// Warp roles (224 threads): warp 0 = producer (lane 0: unit scheduler + TMA; all lanes build the
+// one-hot tiles), warp 1 = row-sum MMA issuer (lane 0) + TMEM owner, warps 2-5 = TMEM drains,
+// warp 6 = column-sum MMA issuer (lane 0).
 #pragma once
 #include <cuda.h>
 
@@ -35,12 +38,14 @@ constexpr int TS_SPLIT_CHUNKS = 16;    // chunks per unit (2048 columns)
 constexpr int TS_STAGES = 5;
 constexpr uint32_t TS_TILE_BYTES = TS_ROWS * TS_CH * 2;  // 32 KB: 2 column halves x [128 rows x 128 B]
 constexpr uint32_t TS_OH_BYTES = 16 * 128 * 2;           // one-hot: 2 halves x [16 labels x 128 B]
-constexpr int TS_THREADS = 6 * 32;
-constexpr int TS_TMEM_COLS = 256;  // D_row 2 x 64 + D_col 2 x 16
+constexpr int TS_THREADS = 7 * 32;
+constexpr int TS_COL_WARP = 6;     // the column-sum MMA issuer
+constexpr int TS_DR_BUF = 3;       // D_row buffers (chunks in flight between the MMA and the drains)
+constexpr int TS_DC_BUF = 4;       // D_col buffers (tiles in flight)
+constexpr int TS_TMEM_COLS = 256;  // D_row 3 x (4 tiles x 16) + D_col 4 x 16
 
 struct TsBand {
-  int64_t koff;    // element offset of the band in the fp16 K buffer
-  int64_t cpoff;   // float offset of the band's column partials [slabs][k][ldb - TB]
+  int64_t koff;    // element offset of the band in the fp16 K buffer (per plane)
   int32_t band;    // band index I
   int32_t ldb;     // stored columns (row pitch, elements), ceil32(n - I TB)
   int32_t rows;    // stored rows, min(TB, n - I TB)
@@ -94,6 +99,9 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t 
   d |= (uint64_t)2 << 61;
   return d;
 }
+__device__ __forceinline__ void ts_red_add(long long *p, long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -120,7 +128,7 @@ struct TsSmem {
 };
 
 constexpr size_t TS_SMEM = 1024 + (size_t)TS_STAGES * TS_TILE_BYTES + 2 * TS_OH_BYTES +
-                           2 * TS_SLAB_TILES * TS_OH_BYTES + 256;
+                           2 * TS_SLAB_TILES * TS_OH_BYTES + 512;  // + barriers, units, TMEM slot
 
 __device__ __forceinline__ TsSmem ts_carve(uint8_t *raw) {
   const uint32_t a = smem_u32(raw);
@@ -140,36 +148,41 @@ __device__ __forceinline__ TsSmem ts_carve(uint8_t *raw) {
   s.bcolfull = s.browempty + 2;
   s.bcolempty = s.bcolfull + 2;
   s.dcolfull = s.bcolempty + 2;
-  s.dcolempty = s.dcolfull + 2;
-  s.drowfull = s.dcolempty + 2;
-  s.drowempty = s.drowfull + 2;
-  s.unit = reinterpret_cast<TsUnit *>(s.drowempty + 2);
+  s.dcolempty = s.dcolfull + TS_DC_BUF;
+  s.drowfull = s.dcolempty + TS_DC_BUF;
+  s.drowempty = s.drowfull + TS_DR_BUF;
+  s.unit = reinterpret_cast<TsUnit *>(s.drowempty + TS_DR_BUF);
   s.tmem_slot = reinterpret_cast<uint32_t *>(s.unit + 2);
   return s;
 }
 
-// maps[b]: fp16 [rows x ldb] view of owned band b, box {64 columns, 128 rows}, 128-byte swizzle
-// (global memory, 64-B aligned). work[0], work[1]: zero between launches (reset at the end).
+// maps[b * planes + pl]: fp16 [rows x ldb] view of plane pl (hi, lo) of owned band b, box {64
+// columns, 128 rows}, 128-byte swizzle (global memory, 64-B aligned); both planes of a tile
+// accumulate into the same TMEM sums. work[0], work[1]: zero between launches (reset at the end).
 __global__ void __launch_bounds__(TS_THREADS, 1)
     spmm_tc_kernel(const CUtensorMap *__restrict__ maps, const TsBand *__restrict__ bands,
                    const TsUnit *__restrict__ units, int nunits, const int32_t *__restrict__ labels, int64_t n,
-                   int k, int64_t rows_pad, float unscale, float *__restrict__ Srow, float *__restrict__ colpart,
-                   int32_t *__restrict__ work) {
+                   int k, int64_t rows_pad, double fxm, long long *__restrict__ Sfix,
+                   int32_t *__restrict__ work, int planes) {
   extern __shared__ uint8_t smem_raw[];
   const TsSmem s = ts_carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < TS_STAGES; ++i) {
       mbar_init(&s.full[i], 1);
-      mbar_init(&s.empty[i], 1);
+      mbar_init(&s.empty[i], 2);  // both MMA issuers commit
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s.browfull[i], 1);
       mbar_init(&s.browempty[i], 1);
       mbar_init(&s.bcolfull[i], 1);
-      mbar_init(&s.bcolempty[i], 1 + 4);  // the MMA commit + the 4 drain warps
+      mbar_init(&s.bcolempty[i], 2 + 4);  // the 2 MMA issuers' commits + the 4 drain warps
+    }
+    for (int i = 0; i < TS_DC_BUF; ++i) {
       mbar_init(&s.dcolfull[i], 1);
       mbar_init(&s.dcolempty[i], 4);
+    }
+    for (int i = 0; i < TS_DR_BUF; ++i) {
       mbar_init(&s.drowfull[i], 1);
       mbar_init(&s.drowempty[i], 4);
     }
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         s.unit[ub] = u;
         mbar_arrive(&s.bcolfull[ub]);
       }
-      const CUtensorMap *map = maps + u.b;
+      const CUtensorMap *map = maps + (int64_t)u.b * planes;
       for (int qi = 0; qi < u.nq; ++qi, ++chunk_it) {
         const int q = u.q0 + qi;
         const int rb = (int)(chunk_it & 1);
@@ -245,27 +258,35 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&s.browfull[rb]);
-          for (int t = 0; t < ntiles; ++t) {
-            mbar_wait(&s.empty[stage], sphase ^ 1u);
-            uint8_t *st = s.stages + stage * TS_TILE_BYTES;
-            mbar_arrive_expect_tx(&s.full[stage], TS_TILE_BYTES);
-            const int row = r0 + t * TS_ROWS;
-            ts_tma_load(st, map, q * TS_CH, row, &s.full[stage]);
-            ts_tma_load(st + TS_TILE_BYTES / 2, map, q * TS_CH + 64, row, &s.full[stage]);
-            if (++stage == TS_STAGES) {
-              stage = 0;
-              sphase ^= 1u;
+          for (int t = 0; t < ntiles; ++t)
+            for (int pl = 0; pl < planes; ++pl) {
+              mbar_wait(&s.empty[stage], sphase ^ 1u);
+              uint8_t *st = s.stages + stage * TS_TILE_BYTES;
+              mbar_arrive_expect_tx(&s.full[stage], TS_TILE_BYTES);
+              const int row = r0 + t * TS_ROWS;
+              ts_tma_load(st, map + pl, q * TS_CH, row, &s.full[stage]);
+              ts_tma_load(st + TS_TILE_BYTES / 2, map + pl, q * TS_CH + 64, row, &s.full[stage]);
+              if (++stage == TS_STAGES) {
+                stage = 0;
+                sphase ^= 1u;
+              }
             }
-          }
         }
         __syncwarp();
       }
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer
+  } else if (warp == 1 || warp == TS_COL_WARP) {  // ---------------- MMA issuers
+    // warp 1 issues the row-sum MMAs, warp 6 the column-sum MMAs (one thread each: the issue
+    // rate of a single thread limited the kernel). A TMEM accumulator sums at most 2 chunks (row
+    // sums) or 2 row tiles (column sums), i.e. <= 16 k-steps x planes MMAs, before it is
+    // drained: the tensor core rounds every accumulation to the running fp32 sum, and over a
+    // whole 2048-column unit the one-signed part of that error reached ~3e-6 of S (J 1.1e-5 off
+    // at HAR); the drains add in fp64 instead (DESIGN A9, §5.5b).
+    const bool rowp = warp == 1;
     if (lane == 0) {
       int stage = 0;
       uint32_t sphase = 0;
-      int64_t chunk_it = 0, dcol_it = 0;
+      int64_t chunk_it = 0, dcol_it = 0, drow_it = 0;
       constexpr uint32_t IROW = ts_idesc(false), ICOL = ts_idesc(true);
       for (int64_t uit = 0;; ++uit) {
         const int ub = (int)(uit & 1);
@@ -276,61 +297,76 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         const TsBand bd = bands[u.b];
         const int r0 = u.slab * TS_SLAB_TILES * TS_ROWS;
         const int ntiles = min(TS_SLAB_TILES, (bd.rows - r0 + TS_ROWS - 1) / TS_ROWS);
-        mbar_wait(&s.drowempty[ub], uph ^ 1u);
-        tc_fence_after();
-        const uint32_t drow = tmem + (uint32_t)ub * 64u;
         const uint32_t bcol = smem_u32(s.bcol + ub * TS_SLAB_TILES * TS_OH_BYTES);
         for (int qi = 0; qi < u.nq; ++qi, ++chunk_it) {
           const int q = u.q0 + qi;
           const bool off = q * TS_CH >= TS_TB;  // the column part skips the diagonal block
           const int rb = (int)(chunk_it & 1);
-          mbar_wait(&s.browfull[rb], (uint32_t)(chunk_it >> 1) & 1u);
-          const int dc = (int)(dcol_it & 1);
-          if (off) mbar_wait(&s.dcolempty[dc], ((uint32_t)(dcol_it >> 1) & 1u) ^ 1u);
-          tc_fence_after();
-          const uint32_t brow = smem_u32(s.brow + rb * TS_OH_BYTES);
-          const uint32_t dcol = tmem + 128u + (uint32_t)dc * 16u;
-          for (int t = 0; t < ntiles; ++t) {
-            mbar_wait(&s.full[stage], sphase);
+          const int db = (int)(drow_it % TS_DR_BUF);
+          const bool rfirst = (qi & 1) == 0, rlast = (qi & 1) == 1 || qi == u.nq - 1;
+          if (rowp) {
+            mbar_wait(&s.browfull[rb], (uint32_t)(chunk_it >> 1) & 1u);
+            if (rfirst) mbar_wait(&s.drowempty[db], ((uint32_t)(drow_it / TS_DR_BUF) & 1u) ^ 1u);
             tc_fence_after();
-            const uint32_t a = smem_u32(s.stages + stage * TS_TILE_BYTES);
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {  // row sums: K-major, k-steps over the 128 columns
-              const uint32_t ko = (uint32_t)(ks >> 2) * (TS_TILE_BYTES / 2) + (uint32_t)(ks & 3) * 32u;
-              const uint32_t bo = (uint32_t)(ks >> 2) * 2048u + (uint32_t)(ks & 3) * 32u;
-              ts_mma(drow + (uint32_t)t * 16u, umma_desc_sw128(a + ko), umma_desc_sw128(brow + bo), IROW,
-                     (qi > 0 || ks > 0) ? 1u : 0u);
+          }
+          const uint64_t brd = umma_desc_sw128(smem_u32(s.brow + rb * TS_OH_BYTES));
+          const uint32_t drow = tmem + (uint32_t)db * 64u;
+          for (int t = 0; t < ntiles; ++t) {
+            const int dc = (int)(dcol_it % TS_DC_BUF);
+            const bool cfirst = (t & 1) == 0, clast = (t & 1) == 1 || t == ntiles - 1;
+            const bool colp = !rowp && off;
+            if (colp && cfirst) {
+              mbar_wait(&s.dcolempty[dc], ((uint32_t)(dcol_it / TS_DC_BUF) & 1u) ^ 1u);
+              tc_fence_after();
             }
-            if (off) {
-              const uint32_t bc = bcol + (uint32_t)t * TS_OH_BYTES;
+            const uint32_t dcol = tmem + (uint32_t)(TS_DR_BUF * 64) + (uint32_t)dc * 16u;
+            const uint64_t bcd = umma_desc_sw128(bcol + (uint32_t)t * TS_OH_BYTES);
+            for (int pl = 0; pl < planes; ++pl) {
+              mbar_wait(&s.full[stage], sphase);
+              tc_fence_after();
+              // descriptors: one per operand, the k-steps add their (address >> 4) offsets
+              const uint32_t a = smem_u32(s.stages + stage * TS_TILE_BYTES);
+              if (rowp) {
+                const uint64_t ad = umma_desc_sw128(a);
+                const uint32_t acc0 = (!rfirst || pl > 0) ? 1u : 0u;
 #pragma unroll
-              for (int ks = 0; ks < 8; ++ks) {  // column sums: A = K^T (MN-major), k-steps over the rows
-                const uint32_t bo = (uint32_t)(ks >> 2) * 2048u + (uint32_t)(ks & 3) * 32u;
-                ts_mma(dcol, umma_desc_sw128_mn(a + (uint32_t)ks * 2048u, TS_TILE_BYTES / 2),
-                       umma_desc_sw128(bc + bo), ICOL, (t > 0 || ks > 0) ? 1u : 0u);
+                for (int ks = 0; ks < 8; ++ks) {  // row sums: K-major, k-steps over the 128 columns
+                  const uint32_t ko = ((uint32_t)(ks >> 2) * (TS_TILE_BYTES / 2) + (uint32_t)(ks & 3) * 32u) >> 4;
+                  const uint32_t bo = ((uint32_t)(ks >> 2) * 2048u + (uint32_t)(ks & 3) * 32u) >> 4;
+                  ts_mma(drow + (uint32_t)t * 16u, ad + ko, brd + bo, IROW, ks > 0 ? 1u : acc0);
+                }
+              } else if (colp) {
+                const uint64_t amn = umma_desc_sw128_mn(a, TS_TILE_BYTES / 2);
+                const uint32_t acc0 = (!cfirst || pl > 0) ? 1u : 0u;
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {  // column sums: A = K^T (MN-major), k-steps over the rows
+                  const uint32_t bo = ((uint32_t)(ks >> 2) * 2048u + (uint32_t)(ks & 3) * 32u) >> 4;
+                  ts_mma(dcol, amn + (uint32_t)ks * (2048u >> 4), bcd + bo, ICOL, ks > 0 ? 1u : acc0);
+                }
+              }
+              ts_commit(&s.empty[stage]);  // (arrives at once when this thread issued no MMA)
+              if (++stage == TS_STAGES) {
+                stage = 0;
+                sphase ^= 1u;
               }
             }
-            ts_commit(&s.empty[stage]);
-            if (++stage == TS_STAGES) {
-              stage = 0;
-              sphase ^= 1u;
-            }
+            if (colp && clast) ts_commit(&s.dcolfull[dc]);
+            if (off && clast) ++dcol_it;
           }
-          ts_commit(&s.browempty[rb]);
-          if (off) {
-            ts_commit(&s.dcolfull[dc]);
-            ++dcol_it;
+          if (rowp) {
+            ts_commit(&s.browempty[rb]);
+            if (rlast) ts_commit(&s.drowfull[db]);
           }
+          if (rlast) ++drow_it;
         }
-        ts_commit(&s.drowfull[ub]);
         ts_commit(&s.bcolempty[ub]);
       }
     }
     __syncwarp();
-  } else {  // ---------------- drains (warps 2-5: TMEM lane quarters)
+  } else if (warp < TS_COL_WARP) {  // ---------------- drains (warps 2-5: TMEM lane quarters), fp64 sums
     const int quarter = warp & 3;
     const uint32_t lq = (uint32_t)(quarter * 32) << 16;
-    int64_t dcol_it = 0;
+    int64_t dcol_it = 0, drow_it = 0;
     for (int64_t uit = 0;; ++uit) {
       const int ub = (int)(uit & 1);
       const uint32_t uph = (uint32_t)(uit >> 1) & 1u;
@@ -342,46 +378,66 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       const int r0 = u.slab * TS_SLAB_TILES * TS_ROWS;
       const int ntiles = min(TS_SLAB_TILES, (bd.rows - r0 + TS_ROWS - 1) / TS_ROWS);
       const int64_t w = (int64_t)bd.ldb - TS_TB;
+      double racc[TS_SLAB_TILES][16];
+#pragma unroll
+      for (int t = 0; t < TS_SLAB_TILES; ++t)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) racc[t][c] = 0.0;
       for (int qi = 0; qi < u.nq; ++qi) {
         const int q = u.q0 + qi;
-        if (q * TS_CH < TS_TB) continue;
-        const int dc = (int)(dcol_it & 1);
-        mbar_wait(&s.dcolfull[dc], (uint32_t)(dcol_it >> 1) & 1u);
-        ++dcol_it;
-        tc_fence_after();
-        float v[16];
-        tmem_ld16(tmem + 128u + (uint32_t)dc * 16u + lq, v);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s.dcolempty[dc]);
-        const int64_t jc = (int64_t)q * TS_CH + quarter * 32 + lane - TS_TB;  // off-diagonal column
-        if (jc < w) {
-          float *cp = colpart + bd.cpoff + (int64_t)u.slab * k * w + jc;
+        if (q * TS_CH >= TS_TB) {  // the column sums of the chunk over the slab's tiles (pairs)
+          double cacc[16];
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c < k) cp[(int64_t)c * w] = v[c] * unscale;
+          for (int c = 0; c < 16; ++c) cacc[c] = 0.0;
+          for (int t = 0; t < ntiles; t += 2, ++dcol_it) {
+            const int dc = (int)(dcol_it % TS_DC_BUF);
+            mbar_wait(&s.dcolfull[dc], (uint32_t)(dcol_it / TS_DC_BUF) & 1u);
+            tc_fence_after();
+            float v[16];
+            tmem_ld16(tmem + (uint32_t)(TS_DR_BUF * 64) + (uint32_t)dc * 16u + lq, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.dcolempty[dc]);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) cacc[c] += (double)v[c];
+          }
+          const int64_t jc = (int64_t)q * TS_CH + quarter * 32 + lane - TS_TB;  // off-diagonal column
+          if (jc < w) {  // the point g0 + TB + jc of a later band: its column part
+            long long *o = Sfix + g0 + TS_TB + jc;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c < k) ts_red_add(o + (int64_t)c * rows_pad, __double2ll_rn(cacc[c] * fxm));
+          }
+        }
+        if ((qi & 1) == 1 || qi == u.nq - 1) {  // the row sums of a chunk pair
+          const int db = (int)(drow_it % TS_DR_BUF);
+          mbar_wait(&s.drowfull[db], (uint32_t)(drow_it / TS_DR_BUF) & 1u);
+          ++drow_it;
+          tc_fence_after();
+#pragma unroll
+          for (int t = 0; t < TS_SLAB_TILES; ++t)
+            if (t < ntiles) {
+              float v[16];
+              tmem_ld16(tmem + (uint32_t)db * 64u + (uint32_t)t * 16u + lq, v);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) racc[t][c] += (double)v[c];
+            }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s.drowempty[db]);
         }
       }
-      mbar_wait(&s.drowfull[ub], uph);
-      tc_fence_after();
-      const int p = u.q0 / TS_SPLIT_CHUNKS;
-      for (int t = 0; t < ntiles; ++t) {
-        float v[16];
-        tmem_ld16(tmem + (uint32_t)ub * 64u + (uint32_t)t * 16u + lq, v);
+#pragma unroll
+      for (int t = 0; t < TS_SLAB_TILES; ++t) {
         const int64_t row = g0 + r0 + t * TS_ROWS + quarter * 32 + lane;
-        if (row < n) {  // Srow[p][c][row]: coalesced here and in ts_reduce_kernel
-          float *o = Srow + (int64_t)p * k * rows_pad + row;
+        if (t < ntiles && row < n) {  // the row part
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c < k) o[(int64_t)c * rows_pad] = v[c] * unscale;
+            if (c < k) ts_red_add(Sfix + (int64_t)c * rows_pad + row, __double2ll_rn(racc[t][c] * fxm));
         }
       }
-      tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s.drowempty[ub]);
-        mbar_arrive(&s.bcolempty[ub]);
-      }
+      if (lane == 0) mbar_arrive(&s.bcolempty[ub]);
     }
   }
   tc_fence_before();
@@ -392,32 +448,17 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   }
 }
 
-// One thread per (row i < rows_pad, label c = blockIdx.y); rows >= n get zeros. S[i][c] (fp64) =
-// this rank's contributions to S(i, c): the row partials of its own band (splits in order) + the
-// column partials (slabs in order) of the owned bands I' < band(i), in order.
-__global__ void ts_reduce_kernel(const float *__restrict__ Srow, const float *__restrict__ colpart,
-                                 const TsBand *__restrict__ bands, const int32_t *__restrict__ band_desc, int64_t n,
-                                 int64_t rows_pad, int k, double *__restrict__ S) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = blockIdx.y;
-  if (i >= rows_pad) return;
-  double acc = 0.0;
-  if (i < n) {
-    const int I = (int)(i / TS_TB);
-    const int bi = band_desc[I];
-    if (bi >= 0)
-      for (int p = 0; p < bands[bi].nsplit; ++p) acc += (double)Srow[((int64_t)p * k + c) * rows_pad + i];
-    for (int Ip = 0; Ip < I; ++Ip) {
-      const int bp = band_desc[Ip];
-      if (bp < 0) continue;
-      const TsBand bd = bands[bp];
-      const int64_t w = (int64_t)bd.ldb - TS_TB;
-      const int64_t jc = i - (int64_t)Ip * TS_TB - TS_TB;
-      const int slabs = (bd.rows + TS_SLAB_TILES * TS_ROWS - 1) / (TS_SLAB_TILES * TS_ROWS);
-      for (int sl = 0; sl < slabs; ++sl) acc += (double)colpart[bd.cpoff + ((int64_t)sl * k + c) * w + jc];
-    }
-  }
-  S[i * k + c] = acc;
+// Sfix[c][row] (int64 fixed point, label-major) -> Sout[row][c]: int64 (Sint, for an exact
+// ReduceScatter over ranks) or fp64 times inv (Sd); rows >= n give 0.
+__global__ void ts_fix_out_kernel(const long long *__restrict__ Sfix, int64_t n, int64_t rows_pad, int k,
+                                  double inv, long long *__restrict__ Sint, double *__restrict__ Sd) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows_pad * k) return;
+  const int64_t i = t / k;
+  const int c = (int)(t % k);
+  const long long v = i < n ? Sfix[(int64_t)c * rows_pad + i] : 0ll;
+  if (Sint) Sint[t] = v;
+  if (Sd) Sd[t] = (double)v * inv;
 }
 
 // ---------------------------------------------------------------- host side

@@ -331,10 +331,12 @@ constexpr size_t T2_GEMM_SMEM = (size_t)T2_STAGES * T2_STAGE_BYTES + T2_GEMM_EXT
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
-                    const __grid_constant__ CUtensorMap tm_out, uint32_t idesc, int nkb, int64_t n,
+                    const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_out2,
+                    uint32_t idesc, int nkb, int64_t n,
                     int64_t i0, int64_t m, int64_t j0, int64_t ncov, const float *__restrict__ norms,
-                    const float *__restrict__ rscale, KappaParams kp, T2GemmSched sc, float oscale) {
-  // oscale == 0: fp32 output; > 0: fp16 output of K * oscale (f4 low-precision storage)
+                    const float *__restrict__ rscale, KappaParams kp, T2GemmSched sc, float oscale, int planes) {
+  // oscale == 0: fp32 output; > 0: fp16 output of K' = K * oscale (f4 K storage): planes == 1
+  // hi = RN(K') only, planes == 2 also lo = RN(K' - hi) through tm_out2 (hi + lo = K' to ~2^-22)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *extra;
   const T2Smem s = t2_carve(smem_raw, (uint32_t)T2_GEMM_EXTRA, &extra);
@@ -390,25 +392,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
           for (int q = 0; q < 32; ++q)
             if (!row_ok || jb + q >= n) v[q] = 0.f;
         }
-        if (oscale > 0.f) {  // one 32 x 32 fp16 box per chunk (64-byte rows, same swizzle)
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          __syncwarp();
+        if (oscale > 0.f) {  // 32 x 32 fp16 boxes per chunk and plane (64-byte rows, same swizzle)
 #pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            uint32_t hw[4];
+          for (int q = 0; q < 32; ++q) v[q] *= oscale;
+          for (int pl = 0; pl < planes; ++pl) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const __half2 h2 = __floats2half2_rn(v[8 * u4 + 2 * e] * oscale, v[8 * u4 + 2 * e + 1] * oscale);
-              hw[e] = *reinterpret_cast<const uint32_t *>(&h2);
+            for (int u4 = 0; u4 < 4; ++u4) {
+              uint32_t hw[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int q = 8 * u4 + 2 * e;
+                const __half2 h2 = __floats2half2_rn(v[q], v[q + 1]);
+                hw[e] = *reinterpret_cast<const uint32_t *>(&h2);
+                if (pl == 0 && planes > 1) {  // the residual for the lo plane (exact in fp32)
+                  const float2 f = __half22float2(h2);
+                  v[q] -= f.x;
+                  v[q + 1] -= f.y;
+                }
+              }
+              *reinterpret_cast<uint4 *>(stg + lane * 64 + ((u4 ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(hw[0], hw[1], hw[2], hw[3]);
             }
-            *reinterpret_cast<uint4 *>(stg + lane * 64 + ((u4 ^ ((lane >> 1) & 3)) << 4)) =
-                make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tm_out, (int)(jb - j0), (int)(ibase - i0), stg, evict);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(pl ? &tm_out2 : &tm_out, (int)(jb - j0), (int)(ibase - i0), stg, evict);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
           }
           continue;
         }
@@ -772,15 +784,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
 inline int tc2_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16,
                            const float *rscale, int64_t rows, int64_t dp, int64_t n, int64_t i0, int64_t m,
                            int64_t j0, int64_t ncov, const float *norms, const KappaParams &kp, void *out,
-                           int64_t ldo, cudaStream_t st, int64_t *launches, float oscale = 0.f) {
-  // oscale > 0: out is fp16 and receives K * oscale
+                           int64_t ldo, cudaStream_t st, int64_t *launches, float oscale = 0.f,
+                           void *out_lo = nullptr) {
+  // oscale > 0: out is fp16 and receives hi = RN(K * oscale); with out_lo also lo = RN(K * oscale - hi)
   if (g.hi != Xhi || g.lo != Xlo || g.fp16 != fp16)
     if (tc_make_maps(g, Xhi, Xlo, fp16, rows, dp)) return 1;
   if ((ldo & (oscale > 0.f ? 7 : 3)) || (reinterpret_cast<uintptr_t>(out) & 15)) {
     tc_err_slot() = "tcgen05 GEMM output needs 16-byte alignment and 16-byte aligned rows";
     return 1;
   }
+  if (out_lo) {
+    if (tc_make_out_map(g, out_lo, m, ncov, ldo, true)) return 1;
+    g.map_out2 = g.map_out;
+  }
   if (tc_make_out_map(g, out, m, ncov, ldo, oscale > 0.f)) return 1;
+  if (!out_lo) g.map_out2 = g.map_out;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(tc2_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T2_GEMM_SMEM) !=
@@ -803,8 +821,8 @@ inline int tc2_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, 
   sc.j0 = j0;
   const int64_t clusters = sc.nitems < g.num_sms / 2 ? sc.nitems : g.num_sms / 2;
   tc2_gemm_kernel<<<(unsigned)(2 * clusters), T2_THREADS, T2_GEMM_SMEM, st>>>(
-      g.map_hi, g.map_lo, g.map_out, t2_idesc(fp16), (int)(dp / TC_BK), n, i0, m, j0, ncov, norms,
-      fp16 ? rscale : nullptr, kp, sc, oscale);
+      g.map_hi, g.map_lo, g.map_out, g.map_out2, t2_idesc(fp16), (int)(dp / TC_BK), n, i0, m, j0, ncov, norms,
+      fp16 ? rscale : nullptr, kp, sc, oscale, out_lo ? 2 : 1);
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -18,7 +18,7 @@ KERNEL_LINEAR, KERNEL_POLY, KERNEL_GAUSSIAN = 0, 1, 2
 PATH_AUTO, PATH_MATERIALIZE, PATH_STREAM = 0, 1, 2
 PREC_BF16X3, PREC_FP32_SIMT, PREC_FP16X3 = 0, 1, 2
 SYM_AUTO, SYM_OFF, SYM_ON = 0, 1, 2
-KSTORE_FP32, KSTORE_FP16 = 0, 1
+KSTORE_AUTO, KSTORE_FP32, KSTORE_FP16, KSTORE_FP16X2 = 0, 1, 2, 3
 DBG_E, DBG_CNORM, DBG_SIZES, DBG_DIAG, DBG_DFULL, DBG_LABELS_PREV = range(6)
 PHASES = ("init_prep", "init_gemm", "spmm", "cnorm", "assign", "a2_kernel")
 
@@ -145,7 +145,7 @@ class KernelKMeans:
                  precision: int = PREC_FP16X3, timing: bool = False, init_labels=None,
                  rank: int = 0, nranks: int = 1, comm=None, stream=None, device=None,
                  workspace=None, grid_rows: int = 1, symmetric: int = SYM_AUTO, incremental: bool = False,
-                 kstore: int = KSTORE_FP32):
+                 kstore: int = KSTORE_AUTO):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device

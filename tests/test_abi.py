@@ -87,9 +87,10 @@ def test_workspace_size_and_errors():
     q.symmetric = kkm.SYM_OFF
     nb_1d = kkm.workspace_size(q, 60000, 784, rank=1, nranks=4)
     assert abs(nb_15 - nb_1d) < 0.05 * nb_1d  # same K-tile size, n^2 / P
-    # f1: the symmetric bands hold ~n^2/2 floats (+ 1/R of them as column partials), spread
-    # over the ranks by area
+    # f1: the symmetric bands hold ~n^2/2 floats (+ 1/R of them as column partials with fp32
+    # storage), spread over the ranks by area
     q.symmetric = kkm.SYM_AUTO
+    q.kstore = kkm.KSTORE_FP32
     kfull = 60000 * 60000 * 4
     nb_sym1 = kkm.workspace_size(q, 60000, 784)
     q.symmetric = kkm.SYM_OFF
@@ -112,7 +113,15 @@ def test_workspace_size_and_errors():
     q.kstore = kkm.KSTORE_FP16
     nb_h = kkm.workspace_size(q, 60000, 784)
     assert 0.45 * nb_sym1 < nb_h < 0.5 * nb_sym1
-    q.kstore = 2
+    q.kstore = kkm.KSTORE_FP16X2  # hi + lo planes: the fp32 band bytes, still no fp32 column partials
+    nb_h2 = kkm.workspace_size(q, 60000, 784)
+    assert 0.85 * nb_sym1 < nb_h2 < 0.95 * nb_sym1
+    q.kstore = kkm.KSTORE_AUTO  # = FP16X2 where the bands are stored with a tensor-core precision
+    assert kkm.workspace_size(q, 60000, 784) == nb_h2
+    q.precision = kkm.PREC_FP32_SIMT  # ... else fp32
+    assert kkm.workspace_size(q, 60000, 784) > nb_h2
+    q.precision = kkm.PREC_FP16X3
+    q.kstore = 4
     with pytest.raises(kkm.KKMError, match="EINVAL"):
         kkm.workspace_size(q, 100, 4)
     for field, value in (("precision", kkm.PREC_FP32_SIMT), ("symmetric", kkm.SYM_OFF),

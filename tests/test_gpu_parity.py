@@ -23,16 +23,23 @@ import paper_2601_17136_b200 as kkm  # noqa: E402
 # f1 (symmetric K): materialised runs store upper-triangle bands from n >= 8192 on (AUTO), so
 # "fp16x3-sym" forces them at the test sizes; streaming runs use the upper-triangle kernel by
 # default ("fp16x3-stream"), "fp16x3-stream-full" keeps the full streaming kernel covered.
+# "fp16x3-kx2": the f1 bands stored as two fp16 planes (kstore FP16X2, fp32-class: hi + lo to
+# ~2^-22) with a2 on the tensor cores (spmm_tc.cuh), held to the same 1e-4 / 1e-5 rules.
 PRECISIONS = [(kkm.PREC_FP32_SIMT, kkm.PATH_MATERIALIZE), (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE),
-              (kkm.PREC_FP16X3, kkm.PATH_STREAM), (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON),
-              (kkm.PREC_FP16X3, kkm.PATH_STREAM, kkm.SYM_OFF)]
-PREC_IDS = ["fp32", "fp16x3", "fp16x3-stream", "fp16x3-sym", "fp16x3-stream-full"]
+              (kkm.PREC_FP16X3, kkm.PATH_STREAM), (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP32),
+              (kkm.PREC_FP16X3, kkm.PATH_STREAM, kkm.SYM_OFF),
+              (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP16X2)]
+PREC_IDS = ["fp32", "fp16x3", "fp16x3-stream", "fp16x3-sym", "fp16x3-stream-full", "fp16x3-kx2"]
 
 
 def _handle(X, k, kind, gamma, coef0, degree, max_iter, precision, **kw):
     if isinstance(precision, tuple):
-        if len(precision) == 3:
+        if len(precision) >= 3:
             kw["symmetric"] = precision[2]
+        if len(precision) == 4:
+            if k > 16 and precision[3] != kkm.KSTORE_FP32:
+                pytest.skip("16-bit K storage needs k <= 16")
+            kw["kstore"] = precision[3]
         precision, kw["path"] = precision[:2]
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
     return kkm.KernelKMeans(Xd, X.shape[0], k, kind, gamma, coef0, degree, max_iter=max_iter,
@@ -171,7 +178,8 @@ def test_host_buffers_e2e(precision):
     Xh = torch.from_numpy(X).pin_memory()
     h = kkm.KernelKMeans(Xh, 1000, 4, kkm.KERNEL_GAUSSIAN, 0.01, 0.0, 1, max_iter=5,
                          precision=precision[0], path=precision[1],
-                         symmetric=precision[2] if len(precision) > 2 else kkm.SYM_AUTO)
+                         symmetric=precision[2] if len(precision) > 2 else kkm.SYM_AUTO,
+                         kstore=precision[3] if len(precision) > 3 else kkm.KSTORE_AUTO)
     h.fit()
     out = torch.empty(1000, dtype=torch.int32).pin_memory()
     h.assign(out)
@@ -192,7 +200,8 @@ def test_stream_equals_materialised():
     assert np.allclose(Ja, Jb, rtol=1e-6, atol=0)
     assert np.allclose(a.debug_read(kkm.DBG_E), b.debug_read(kkm.DBG_E), rtol=1e-5, atol=1e-3)
     # f1: upper-triangle storage / upper-triangle streaming against the full K (a)
-    for mode in ((kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON),
+    for mode in ((kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP32),
+                 (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP16X2),
                  (kkm.PREC_FP16X3, kkm.PATH_STREAM, kkm.SYM_OFF)):
         c = _handle(X, 10, *args, 12, mode)
         ic, Jc, cc = c.fit()
@@ -208,7 +217,8 @@ def test_symmetric_bands(k, kind):
     k = 3, 11, 16; teacher-forced against the oracle."""
     X = synth.blobs(4133, 6, k, seed=60 + k, sep=2.5)
     gamma = 0.05 if kind == oracle.GAUSSIAN else 1.0
-    teacher_forced(X, k, kind, gamma, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON))
+    for ks in (kkm.KSTORE_FP32, kkm.KSTORE_FP16X2):  # fp32 bands (sym.cuh), hi + lo planes (spmm_tc.cuh)
+        teacher_forced(X, k, kind, gamma, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, ks))
     teacher_forced(X, k, kind, gamma, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_STREAM))
 
 
@@ -285,8 +295,9 @@ def test_bf16x3_rings_limit():
 
 
 @pytest.mark.parametrize("mode", [(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE), (kkm.PREC_FP16X3, kkm.PATH_STREAM),
-                                  (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON)],
-                         ids=["mat", "stream", "sym"])
+                                  (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP32),
+                                  (kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP16X2)],
+                         ids=["mat", "stream", "sym", "sym-kx2"])
 @pytest.mark.parametrize("name,n,k", [("mnist60k", 3000, 10), ("har200k", 2500, 6), ("mnist60k", 2000, 21)])
 def test_incremental_matches_full(mode, name, n, k):
     """f3: S maintained by the moved points (kkm_params.incremental) gives the same label trace
