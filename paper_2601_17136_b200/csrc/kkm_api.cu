@@ -142,6 +142,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   // least-loaded rank (lowest rank on ties): deterministic, area-balanced.
   const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= SP_KPMAX;
   P.kh = p->kstore == KKM_KSTORE_FP16 || p->kstore == KKM_KSTORE_FP16X2;  // AUTO: decided below
+  const bool kh_pitch = P.kh || (p->kstore == KKM_KSTORE_AUTO && P.tc);  // the bands if stored are 16-bit
   P.kplanes = p->kstore == KKM_KSTORE_FP16 ? 1 : 2;
   const bool sym_ok = sym_elig && (p->symmetric == KKM_SYM_ON || P.kh || n >= 8 * SYM_TB);
   double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
@@ -155,7 +156,9 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     int64_t koff = 0, cpoff = 0, csoff = 0;
     for (int I = 0; I < P.T; ++I) {
       const int64_t rows = std::min<int64_t>(SYM_TB, n - (int64_t)I * SYM_TB);
-      const int64_t ldb = round_up(n - (int64_t)I * SYM_TB, 32);
+      // 16-bit planes (spmm_tc): rows padded to 128 elements = 256 B, so each 128-column chunk
+      // of a row is one 256-B aligned L2 promotion unit (no re-fetch of a neighbour's bytes)
+      const int64_t ldb = round_up(n - (int64_t)I * SYM_TB, kh_pitch ? 128 : 32);
       int owner = 0;
       for (int r = 1; r < nranks; ++r)
         if (load[r] < load[owner]) owner = r;

@@ -30,6 +30,9 @@
 
 namespace kkm {
 
+#ifndef KKM_TS_PROMO
+#define KKM_TS_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 constexpr int TS_TB = 1024;            // band height (rows) = SYM_TB
 constexpr int TS_ROWS = 128;           // row tile
 constexpr int TS_CH = 128;             // chunk columns
@@ -47,7 +50,7 @@ constexpr int TS_TMEM_COLS = 256;  // D_row 3 x (4 tiles x 16) + D_col 4 x 16
 struct TsBand {
   int64_t koff;    // element offset of the band in the fp16 K buffer (per plane)
   int32_t band;    // band index I
-  int32_t ldb;     // stored columns (row pitch, elements), ceil32(n - I TB)
+  int32_t ldb;     // stored columns (row pitch, elements), ceil128(n - I TB)
   int32_t rows;    // stored rows, min(TB, n - I TB)
   int32_t nsplit;  // column splits
 };
@@ -471,7 +474,7 @@ inline int ts_encode_band(CUtensorMap *m, const void *ptr, int64_t rows, int64_t
   cuuint32_t es[2] = {1u, 1u};
   CUresult r = tc_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void *)ptr, dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              (CUtensorMapL2promotion)KKM_TS_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     tc_err_slot() = "cuTensorMapEncodeTiled (fp16 band) failed";
     return 1;

@@ -18,7 +18,8 @@ ap.add_argument("--precision", default="fp16x3")
 ap.add_argument("--path", default="auto", choices=["auto", "mat", "stream"])
 ap.add_argument("--k", type=int, default=0, help="override the cluster count")
 ap.add_argument("--full-k", action="store_true", help="store full K rows (KKM_SYM_OFF) instead of the f1 bands")
-ap.add_argument("--kstore", default="fp32", choices=["fp32", "fp16", "fp16x2"], help="f4: materialised K storage type")
+ap.add_argument("--kstore", default="auto", choices=["auto", "fp32", "fp16", "fp16x2"],
+                help="materialised band storage (auto: hi + lo fp16 planes with a tensor-core precision)")
 a = ap.parse_args()
 X, cfg = synth.make_config(a.config, n=a.n or None)
 prec = {"fp16x3": kkm.PREC_FP16X3, "bf16x3": kkm.PREC_BF16X3, "fp32": kkm.PREC_FP32_SIMT}[a.precision]
@@ -28,7 +29,8 @@ if a.k:
 h = kkm.KernelKMeans(torch.from_numpy(X).cuda(), X.shape[0], cfg["k"], cfg["kind"], cfg["gamma"],
                      cfg["coef0"], cfg["degree"], max_iter=a.iters, precision=prec, timing=True, path=path,
                      symmetric=kkm.SYM_OFF if a.full_k else kkm.SYM_AUTO,
-                     kstore={"fp32": kkm.KSTORE_FP32, "fp16": kkm.KSTORE_FP16, "fp16x2": kkm.KSTORE_FP16X2}[a.kstore])
+                     kstore={"auto": kkm.KSTORE_AUTO, "fp32": kkm.KSTORE_FP32, "fp16": kkm.KSTORE_FP16,
+                             "fp16x2": kkm.KSTORE_FP16X2}[a.kstore])
 it, J, ch = h.fit()
 torch.cuda.synchronize()
 ph = h.phase_ms()
