@@ -96,7 +96,8 @@ for name in a.configs.split(","):
         loop_ms = (spmm_ms + cn_ms + as_ms) / it
         out = {"config": name, "n": n, "d": d, "k": cfg["k"], "n_gpus": world,
                "grid": f"{a.grid_rows}x{world // a.grid_rows}", "iterations": it,
-               "path": (("materialised (f1 bands)" if sym else "materialised") if mat else
+               "path": (("materialised (f1 bands, hi + lo fp16 planes, a2 on tensor cores)" if sym else "materialised")
+                        if mat else
                         ("streaming (f1 upper triangle)" if cfg["k"] <= 16 and a.grid_rows <= 1
                          else "streaming")),
                "sec_per_iter": loop_ms / 1e3, "total_clustering_s": (init_ms + fit_ms) / 1e3,
