@@ -65,6 +65,12 @@ struct Plan {
   // f3 incremental S: moved-point set of at most dmax points
   bool inc;
   bool fused;  // a3 + a4 as one single-CTA kernel (one rank, small n, k <= 16)
+  // replicated a3/a4 (1D f1 paths on several ranks): S of ALL points is allreduced (it is summed
+  // over the ranks' bands anyway) and every rank runs a3/a4 on all n points -- identical inputs,
+  // deterministic kernels, identical labels -- so no c-partial allgather, labels allgather or
+  // sizes / changed allreduce remain: one collective per iteration instead of three
+  bool repl;
+  int64_t a_row0, a_n, a_B;  // the a3/a4 rows: [a_row0, a_row0 + a_n), buffers of a_B rows
   int64_t dmax, dpad;
   // f1 symmetric storage (sym.cuh): bands of SYM_TB rows, the rank's share spread by area
   bool sym;
@@ -166,6 +172,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       if (owner != rank) continue;
       SymBand b;
       b.band = I;
+      b.row0 = 0;
+      b.rows = (int32_t)rows;
       b.ldb = (int32_t)ldb;
       b.koff = koff;
       b.cpoff = cpoff;
@@ -270,14 +278,42 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.tbands.clear();
   P.tunits.clear();
   P.ts_nsm = 0;
-  if (P.sym && P.kh) {  // f4: units = (band, 512-row slab, <= 16 chunks of 128 columns)
+  if (P.sym && P.kh && nranks > 1) {
+    // 16-bit bands on several ranks: spread 512-row pieces of the bands by area (finer than whole
+    // bands, so the ranks' a2 work is balanced to ~1 % instead of ~10 %)
+    P.bands.clear();
+    P.band_desc.assign(P.T, -1);  // (used by the fp32 band path only)
+    std::vector<double> load(nranks, 0.0);
+    int64_t koff = 0;
+    constexpr int PIECE = TS_SLAB_TILES * TS_ROWS;
+    for (int I = 0; I < P.T; ++I)
+      for (int r0 = 0; r0 < SYM_TB && (int64_t)I * SYM_TB + r0 < n; r0 += PIECE) {
+        const int64_t rows = std::min<int64_t>(PIECE, n - (int64_t)I * SYM_TB - r0);
+        const int64_t ldb = round_up(n - (int64_t)I * SYM_TB, 128);
+        int owner = 0;
+        for (int r = 1; r < nranks; ++r)
+          if (load[r] < load[owner]) owner = r;
+        load[owner] += (double)rows * (double)ldb;
+        if (owner != rank) continue;
+        SymBand b{};
+        b.band = I;
+        b.row0 = r0;
+        b.rows = (int32_t)rows;
+        b.ldb = (int32_t)ldb;
+        b.koff = koff;
+        koff += rows * ldb;
+        P.bands.push_back(b);
+      }
+  }
+  if (P.sym && P.kh) {  // f4: units = (piece, 512-row slab, <= 16 chunks of 128 columns)
     for (size_t b = 0; b < P.bands.size(); ++b) {
       const SymBand &sb = P.bands[b];
       TsBand t;
       t.koff = sb.koff;
       t.band = sb.band;
+      t.row0 = sb.row0;
       t.ldb = sb.ldb;
-      t.rows = (int32_t)std::min<int64_t>(SYM_TB, n - (int64_t)sb.band * SYM_TB);
+      t.rows = sb.rows;
       const int nchunks = (int)ceil_div(t.ldb, TS_CH);
       t.nsplit = (int)ceil_div(nchunks, TS_SPLIT_CHUNKS);
       const int slabs = (int)ceil_div(t.rows, TS_SLAB_TILES * TS_ROWS);
@@ -302,15 +338,20 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (P.ssym) P.nApad = P.npad;
   P.s_rows_pad = (P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1)) ? P.B : P.nApad;  // == need_smine
   P.inc = p->incremental == 1;
-  P.fused = nranks == 1 && n <= FUSED_MAX_ROWS && P.k <= 16;
+  P.repl = nranks > 1 && P.pr == 1 && (P.sym || P.ssym) && !P.inc;
+  P.a_row0 = P.repl ? 0 : P.row0;
+  P.a_n = P.repl ? n : P.nloc;
+  P.a_B = P.repl ? P.npad : P.B;
+  if (P.repl) P.s_rows_pad = P.npad;
+  P.fused = (nranks == 1 || P.repl) && n <= FUSED_MAX_ROWS && P.k <= 16;
   if (P.inc && (P.pr > 1 || !P.tc))
     return fail(KKM_EUNSUP, "incremental S needs the 1D algorithm and a tensor-core precision");
   P.dmax = std::max<int64_t>(1, n / 16);
   P.dpad = round_up(P.dmax, 256);
   P.sort_blocks = (int)ceil_div(std::max<int64_t>(P.nB, 1), SORT_BLOCK);
   P.nspmm_pass = (int)ceil_div(P.k, SP_KPMAX);
-  P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.nloc, 1), FIN_THREADS));
-  P.rows_per_block = ceil_div(std::max<int64_t>(P.nloc, 1), P.nfin);
+  P.nfin = (int)std::min<int64_t>(1024, ceil_div(std::max<int64_t>(P.a_n, 1), FIN_THREADS));
+  P.rows_per_block = ceil_div(std::max<int64_t>(P.a_n, 1), P.nfin);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -325,13 +366,13 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.o_Xlo = P.tc ? take((size_t)P.npad * P.dp * 2) : 0;
   P.o_rscale = take((size_t)P.npad * 4);
   P.o_norms = take((size_t)P.npad * 4);
-  P.o_diag = take((size_t)P.B * 8);
+  P.o_diag = take((size_t)P.a_B * 8);
   size_t kfloats = (size_t)P.nApad * P.ldk;
   size_t cpfloats = 0, csdoubles = 0;
   if (P.sym) {
     kfloats = 0;
     for (const SymBand &b : P.bands) {
-      kfloats += (size_t)std::min<int64_t>(SYM_TB, n - (int64_t)b.band * SYM_TB) * b.ldb;
+      kfloats += (size_t)b.rows * b.ldb;
       cpfloats += (size_t)P.sym_gmax * std::max<int64_t>(0, b.ldb - SYM_TB);
       csdoubles += (size_t)P.k * std::max<int64_t>(0, b.ldb - SYM_TB);
     }
@@ -343,15 +384,15 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.o_sizes[0] = take((size_t)P.k * 4);
   P.o_sizes[1] = take((size_t)P.k * 4);
   P.o_Spart = take((size_t)P.nsplit * P.nApad * P.k * 8);
-  P.o_E = take((size_t)P.B * P.k * 8);
+  P.o_E = take((size_t)P.a_B * P.k * 8);
   P.o_blockpart = take((size_t)P.nfin * k1 * 8);
   P.o_rankpart = take((size_t)nranks * k1 * 8);
   P.o_cnorm = take((size_t)P.k * 8);
   P.o_J = take((size_t)(P.max_iter + 2) * 8);
   P.o_changed = take((size_t)(P.max_iter + 2) * 8);
-  P.o_Dfull = take((size_t)P.B * P.k * 8);
+  P.o_Dfull = take((size_t)P.a_B * P.k * 8);
   P.o_bad = take(16);
-  P.o_E2 = take((size_t)P.B * P.k * 8);
+  P.o_E2 = take((size_t)P.a_B * P.k * 8);
   P.o_cnorm2 = take((size_t)P.k * 8);
   if (!P.materialize) {
     P.o_Shi = take((size_t)P.npad * P.dp * 2);
@@ -369,7 +410,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_labB = take((size_t)P.ldk * 4);
     P.o_Scol = take((size_t)P.nApad * P.k * 8);
   }
-  P.need_smine = P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1);  // S of the own block after a reduce-scatter
+  P.need_smine = P.pr > 1 || ((P.sym || P.ssym) && P.nranks > 1 && !P.repl);  // S of the own block after a reduce-scatter
   if (P.need_smine) P.o_Smine = take((size_t)P.B * P.k * 8);
   if (P.ssym) {
     P.o_units = take(std::max<size_t>(P.units.size(), 1) * sizeof(int4));
@@ -745,7 +786,9 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
     }
     a2_mark(h);
     const unsigned gr = (unsigned)ceil_div(P.npad * k, 256);
-    if (P.nranks == 1) {
+    if (P.repl)  // S of all points on every rank (exact int64 sum)
+      CKN(ncclAllReduce(h->tSfix, h->tSfix, (size_t)P.npad * k, ncclInt64, ncclSum, h->comm, h->st));
+    if (P.nranks == 1 || P.repl) {
       ts_fix_out_kernel<<<gr, 256, 0, h->st>>>(h->tSfix, P.n, P.npad, k, h->tfx_inv, nullptr, h->Sfin);
       CKL();
       *s_out = h->Sfin;
@@ -786,7 +829,8 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   sym_reduce_kernel<<<dim3((unsigned)ceil_div(P.npad, 256), (unsigned)k), 256, 0, h->st>>>(
       h->Spart, h->colsum, h->bands, h->band_desc, P.n, P.npad, k, h->Sfin);
   CKL();
-  if (P.nranks == 1) {
+  if (P.repl) CKN(ncclAllReduce(h->Sfin, h->Sfin, (size_t)P.npad * k, ncclDouble, ncclSum, h->comm, h->st));
+  if (P.nranks == 1 || P.repl) {
     *s_out = h->Sfin;
     return KKM_OK;
   }
@@ -815,7 +859,9 @@ int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   }
   const unsigned g = (unsigned)ceil_div(P.npad * k, 256);
   double *Sd = h->Spart;  // P.nsplit = 1: [npad][k] fp64
-  if (P.nranks == 1) {
+  if (P.repl)  // the sorted order is the same on every rank (same labels, stable sort): sum in place
+    CKN(ncclAllReduce(h->Sfix, h->Sfix, (size_t)P.npad * k, ncclInt64, ncclSum, h->comm, h->st));
+  if (P.nranks == 1 || P.repl) {
     fx_unpermute_kernel<<<g, 256, 0, h->st>>>(h->Sfix, h->pos, P.n, P.npad, k, h->fx_inv, nullptr, Sd);
     CKL();
     *s_out = Sd;
@@ -866,20 +912,21 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
   const int32_t *labels = h->lab[h->cur];
   const int32_t *sizes = h->sizes[h->cur];
   const int k1 = P.k + 1;
-  if (P.nloc > 0) {
+  const int nr = P.repl ? 1 : P.nranks, r = P.repl ? 0 : P.rank;  // replicated a3: one "rank"
+  if (P.a_n > 0) {
     int fth = FIN_THREADS;  // power of two with (k+1) * fth doubles <= 48 KB
     while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
-        S, nsplit, P.nloc, rows_pad, P.k, sizes, labels + P.row0, h->diag, P.rows_per_block,
+        S, nsplit, P.a_n, rows_pad, P.k, sizes, labels + P.a_row0, h->diag, P.rows_per_block,
         E_out, h->blockpart);
     CKL();
   }
-  cnorm_local_kernel<<<1, 32 * std::min(32, k1), 0, h->st>>>(h->blockpart, P.nloc > 0 ? P.nfin : 0, P.k,
-                                           h->rankpart + (int64_t)P.rank * k1);
+  cnorm_local_kernel<<<1, 32 * std::min(32, k1), 0, h->st>>>(h->blockpart, P.a_n > 0 ? P.nfin : 0, P.k,
+                                           h->rankpart + (int64_t)r * k1);
   CKL();
-  if (P.nranks > 1)
-    CKN(ncclAllGather(h->rankpart + (int64_t)P.rank * k1, h->rankpart, k1, ncclDouble, h->comm, h->st));
-  cnorm_final_kernel<<<1, 128, 0, h->st>>>(h->rankpart, P.nranks, P.k, sizes, cnorm_out, J_out,
+  if (nr > 1)
+    CKN(ncclAllGather(h->rankpart + (int64_t)r * k1, h->rankpart, k1, ncclDouble, h->comm, h->st));
+  cnorm_final_kernel<<<1, 128, 0, h->st>>>(h->rankpart, nr, P.k, sizes, cnorm_out, J_out,
                                            sizes_next, changed_out);
   CKL();
   return KKM_OK;
@@ -889,14 +936,14 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
 int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
   const Plan &P = h->P;
   const int nx = h->cur ^ 1;
-  if (P.nloc > 0) {
+  if (P.a_n > 0) {
     const int th = 256;
-    assign_kernel<<<(unsigned)ceil_div(P.nloc, th), th, (size_t)P.k * 4, h->st>>>(
-        h->E, P.nloc, P.k, h->cnorm, h->diag, h->lab[h->cur] + P.row0, h->lab[nx] + P.row0,
+    assign_kernel<<<(unsigned)ceil_div(P.a_n, th), th, (size_t)P.k * 4, h->st>>>(
+        h->E, P.a_n, P.k, h->cnorm, h->diag, h->lab[h->cur] + P.a_row0, h->lab[nx] + P.a_row0,
         h->sizes[nx], changed_out, h->Dfull);
     CKL();
   }
-  if (P.nranks > 1) {  // the changed count is global too: every rank takes the same control path
+  if (P.nranks > 1 && !P.repl) {  // the changed count is global too: every rank takes the same control path
     CKN(ncclGroupStart());
     CKN(ncclAllGather(h->lab[nx] + P.row0, h->lab[nx], P.B, ncclInt32, h->comm, h->st));
     CKN(ncclAllReduce(h->sizes[nx], h->sizes[nx], P.k, ncclInt32, ncclSum, h->comm, h->st));
@@ -1154,9 +1201,9 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
           h->Xf, P.ldf, P.n, P.npad, P.d, h->norms, h->Xhi, h->Xlo, P.dp,
           P.tc ? (P.fp16 ? 2 : 1) : 0, h->rscale);
       CKL();
-      if (P.nloc > 0) {
-        diag_kernel<<<(unsigned)ceil_div(P.nloc, wpb), wpb * 32, 0, h->st>>>(
-            h->Xf, P.ldf, P.d, P.row0, P.nloc, p->kind, p->gamma, p->coef0, p->degree, h->diag);
+      if (P.a_n > 0) {
+        diag_kernel<<<(unsigned)ceil_div(P.a_n, wpb), wpb * 32, 0, h->st>>>(
+            h->Xf, P.ldf, P.d, P.a_row0, P.a_n, p->kind, p->gamma, p->coef0, p->degree, h->diag);
         CKL();
       }
     }
@@ -1240,12 +1287,12 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         CK(cudaStreamSynchronize(h->st));  // (host vectors go out of scope)
       }
       for (const SymBand &b : P.bands) {
-        const int64_t i0 = (int64_t)b.band * SYM_TB;
+        const int64_t j0 = (int64_t)b.band * SYM_TB, i0 = j0 + b.row0;  // rows of the piece, columns >= band start
         if (P.kh)
-          CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, (__half *)h->K + b.koff, b.ldb,
-                          h->kscale, P.kplanes > 1 ? (__half *)h->K + P.kelems + b.koff : nullptr));
+          CKR(launch_gemm(h, i0, b.rows, j0, b.ldb, (__half *)h->K + b.koff, b.ldb, h->kscale,
+                          P.kplanes > 1 ? (__half *)h->K + P.kelems + b.koff : nullptr));
         else
-          CKR(launch_gemm(h, i0, std::min<int64_t>(SYM_TB, P.n - i0), i0, b.ldb, h->K + b.koff, b.ldb));
+          CKR(launch_gemm(h, i0, b.rows, j0, b.ldb, h->K + b.koff, b.ldb));
       }
     } else if (P.materialize) {
       CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));
@@ -1630,13 +1677,15 @@ int kkm_debug_read(kkm_handle h, int32_t what, void *dst) {
   const Plan &P = h->P;
   const int prev = h->cur ^ 1;  // buffers of the labels entering the last iteration
   switch (what) {
-    case KKM_DBG_E: CKR(copy_any(h, dst, h->E, (size_t)P.nloc * P.k * 8)); break;
+    case KKM_DBG_E: CKR(copy_any(h, dst, h->E + (P.row0 - P.a_row0) * P.k, (size_t)P.nloc * P.k * 8)); break;
     case KKM_DBG_CNORM: CKR(copy_any(h, dst, h->cnorm, (size_t)P.k * 8)); break;
     case KKM_DBG_SIZES:
       CKR(copy_any(h, dst, h->sizes[h->have_last ? prev : h->cur], (size_t)P.k * 4));
       break;
-    case KKM_DBG_DIAG: CKR(copy_any(h, dst, h->diag, (size_t)P.nloc * 8)); break;
-    case KKM_DBG_DFULL: CKR(copy_any(h, dst, h->Dfull, (size_t)P.nloc * P.k * 8)); break;
+    case KKM_DBG_DIAG: CKR(copy_any(h, dst, h->diag + (P.row0 - P.a_row0), (size_t)P.nloc * 8)); break;
+    case KKM_DBG_DFULL:
+      CKR(copy_any(h, dst, h->Dfull + (P.row0 - P.a_row0) * P.k, (size_t)P.nloc * P.k * 8));
+      break;
     case KKM_DBG_LABELS_PREV:
       CKR(copy_any(h, dst, h->lab[h->have_last ? prev : h->cur], (size_t)P.n * 4));
       break;

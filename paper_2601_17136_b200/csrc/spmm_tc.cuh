@@ -11,7 +11,7 @@
 // the labels. Accumulators live in TMEM (fp32); no per-element instruction touches K, so the
 // kernel is a pure HBM stream of half the bytes of the fp32 bands.
 //
-// Work unit = (owned band, 512-row slab = 4 row tiles, split of <= 16 chunks of 128 columns).
+// Work unit = (owned band piece, 512-row slab = 4 row tiles, split of <= 8 chunks of 128 columns).
 // Per chunk and row tile the row MMAs go to D_row[tile] and the column MMAs to D_col (skipped on
 // the diagonal block K_II, which the row part covers whole); an accumulator holds 2 chunks (row
 // sums) or 2 row tiles (column sums) and is then drained into fp64 registers: the column sums of
@@ -37,7 +37,10 @@ constexpr int TS_TB = 1024;            // band height (rows) = SYM_TB
 constexpr int TS_ROWS = 128;           // row tile
 constexpr int TS_CH = 128;             // chunk columns
 constexpr int TS_SLAB_TILES = 4;       // row tiles per unit (512 rows)
-constexpr int TS_SPLIT_CHUNKS = 16;    // chunks per unit (2048 columns)
+#ifndef KKM_TS_SPLIT
+#define KKM_TS_SPLIT 8
+#endif
+constexpr int TS_SPLIT_CHUNKS = KKM_TS_SPLIT;  // chunks per unit (1024 columns: 4 MB units of the two planes were too coarse for 4 GPUs)
 constexpr int TS_STAGES = 5;
 constexpr uint32_t TS_TILE_BYTES = TS_ROWS * TS_CH * 2;  // 32 KB: 2 column halves x [128 rows x 128 B]
 constexpr uint32_t TS_OH_BYTES = 16 * 128 * 2;           // one-hot: 2 halves x [16 labels x 128 B]
@@ -47,11 +50,12 @@ constexpr int TS_DR_BUF = 3;       // D_row buffers (chunks in flight between th
 constexpr int TS_DC_BUF = 4;       // D_col buffers (tiles in flight)
 constexpr int TS_TMEM_COLS = 256;  // D_row 3 x (4 tiles x 16) + D_col 4 x 16
 
-struct TsBand {
-  int64_t koff;    // element offset of the band in the fp16 K buffer (per plane)
+struct TsBand {    // a stored piece of band I: rows [I TB + row0, + rows) x columns [I TB, + ldb)
+  int64_t koff;    // element offset of the piece in the fp16 K buffer (per plane)
   int32_t band;    // band index I
+  int32_t row0;    // first row of the piece within the band (0 or 512)
   int32_t ldb;     // stored columns (row pitch, elements), ceil128(n - I TB)
-  int32_t rows;    // stored rows, min(TB, n - I TB)
+  int32_t rows;    // stored rows (<= 512 when the rank holds 512-row pieces)
   int32_t nsplit;  // column splits
 };
 struct TsUnit {
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       const int ntiles = min(TS_SLAB_TILES, (bd.rows - r0 + TS_ROWS - 1) / TS_ROWS);
       // row-label one-hots of the unit's tiles
       for (int t = 0; t < ntiles; ++t) {
-        const int64_t r = g0 + r0 + t * TS_ROWS + 4 * lane;
+        const int64_t r = g0 + bd.row0 + r0 + t * TS_ROWS + 4 * lane;
         int4 l4;
         l4.x = r < n ? labels[r] : -1;
         l4.y = r + 1 < n ? labels[r + 1] : -1;
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       }
 #pragma unroll
       for (int t = 0; t < TS_SLAB_TILES; ++t) {
-        const int64_t row = g0 + r0 + t * TS_ROWS + quarter * 32 + lane;
+        const int64_t row = g0 + bd.row0 + r0 + t * TS_ROWS + quarter * 32 + lane;
         if (t < ntiles && row < n) {  // the row part
 #pragma unroll
           for (int c = 0; c < 16; ++c)

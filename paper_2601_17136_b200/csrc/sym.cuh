@@ -37,6 +37,8 @@ struct SymBand {
   int32_t ldb;     // stored columns (row pitch), ceil32(n - I TB)
   int32_t nsplit;  // column splits of the band
   int32_t cps;     // chunks per split
+  int32_t row0;    // 16-bit storage (spmm_tc): first row of a 512-row piece of the band; else 0
+  int32_t rows;    // stored rows
 };
 
 // Row group descriptor: sorted positions [p0, p0 + cnt) of the band, all with label lab.
