@@ -150,12 +150,13 @@ inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, boo
 
 // [m x ncov] view of out (row pitch ldo elements) for the TMA stores: fp32 boxes of 32 rows x 16
 // columns (ldo % 4 == 0), or with half_out fp16 boxes of 32 x 32 (ldo % 8 == 0); 64-byte swizzle.
-inline int tc_make_out_map(TcGemm &g, void *out, int64_t m, int64_t ncov, int64_t ldo, bool half_out = false) {
+inline int tc_encode_out_map(CUtensorMap *map, void *out, int64_t m, int64_t ncov, int64_t ldo, bool half_out) {
+  if (tc_encode_ready()) return 1;
   cuuint64_t dims[2] = {(cuuint64_t)ncov, (cuuint64_t)m};
   cuuint64_t strides[1] = {(cuuint64_t)ldo * (half_out ? 2 : 4)};
   cuuint32_t box[2] = {half_out ? 32u : 16u, 32u};
   cuuint32_t es[2] = {1u, 1u};
-  CUresult r = tc_encode_fn()(&g.map_out, half_out ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+  CUresult r = tc_encode_fn()(map, half_out ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                               2, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -164,6 +165,9 @@ inline int tc_make_out_map(TcGemm &g, void *out, int64_t m, int64_t ncov, int64_
     return 1;
   }
   return 0;
+}
+inline int tc_make_out_map(TcGemm &g, void *out, int64_t m, int64_t ncov, int64_t ldo, bool half_out = false) {
+  return tc_encode_out_map(&g.map_out, out, m, ncov, ldo, half_out);
 }
 
 

@@ -90,7 +90,7 @@ struct Plan {
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_gregs, o_gmaps, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
       o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
 };
 
@@ -305,7 +305,13 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
         P.bands.push_back(b);
       }
   }
-  if (P.sym && P.kh) {  // f4: units = (piece, 512-row slab, <= 16 chunks of 128 columns)
+  if (P.sym && P.kh) {  // f4: units = (piece, 512-row slab, <= split chunks of 128 columns)
+    // split: 16 chunks, or 8 when that leaves fewer than ~32 units per SM (the last wave of 4 MB
+    // units idled SMs at config 2 on 4 GPUs; at config 3 the smaller units cost ~6 %)
+    int64_t cslabs = 0;
+    for (const SymBand &sb : P.bands)
+      cslabs += ceil_div(sb.rows, TS_SLAB_TILES * TS_ROWS) * ceil_div(sb.ldb, TS_CH);
+    const int split = cslabs / 16 >= 32 * 148 ? 16 : 8;
     for (size_t b = 0; b < P.bands.size(); ++b) {
       const SymBand &sb = P.bands[b];
       TsBand t;
@@ -315,13 +321,12 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       t.ldb = sb.ldb;
       t.rows = sb.rows;
       const int nchunks = (int)ceil_div(t.ldb, TS_CH);
-      t.nsplit = (int)ceil_div(nchunks, TS_SPLIT_CHUNKS);
+      t.nsplit = (int)ceil_div(nchunks, split);
       const int slabs = (int)ceil_div(t.rows, TS_SLAB_TILES * TS_ROWS);
       P.ts_nsm = std::max(P.ts_nsm, t.nsplit);
       for (int sl = 0; sl < slabs; ++sl)
         for (int sp = 0; sp < t.nsplit; ++sp)
-          P.tunits.push_back(TsUnit{(int32_t)b, sl, sp * TS_SPLIT_CHUNKS,
-                                    std::min(TS_SPLIT_CHUNKS, nchunks - sp * TS_SPLIT_CHUNKS)});
+          P.tunits.push_back(TsUnit{(int32_t)b, sl, sp * split, std::min(split, nchunks - sp * split)});
       P.tbands.push_back(t);
     }
   }
@@ -445,6 +450,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_work = take(2 * 4);  // spmm_sym's item scheduler
     P.o_gfirst = take((size_t)P.T * (P.k + 1) * 4);
     P.o_Sfin = take((size_t)P.npad * P.k * 8);
+    if (P.tc) {  // one GEMM launch over all owned band pieces: regions + output maps
+      P.o_gregs = take(std::max<size_t>(P.bands.size(), 1) * sizeof(T2Region));
+      P.o_gmaps = take(std::max<size_t>(P.bands.size() * (P.kh ? P.kplanes : 1), 1) * sizeof(CUtensorMap));
+    }
   }
   if (P.sym && P.kh) {
     P.o_tmaps = take(std::max<size_t>(P.tbands.size() * P.kplanes, 1) * sizeof(CUtensorMap));
@@ -1286,13 +1295,44 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
                              h->st));
         CK(cudaStreamSynchronize(h->st));  // (host vectors go out of scope)
       }
-      for (const SymBand &b : P.bands) {
-        const int64_t j0 = (int64_t)b.band * SYM_TB, i0 = j0 + b.row0;  // rows of the piece, columns >= band start
-        if (P.kh)
-          CKR(launch_gemm(h, i0, b.rows, j0, b.ldb, (__half *)h->K + b.koff, b.ldb, h->kscale,
-                          P.kplanes > 1 ? (__half *)h->K + P.kelems + b.koff : nullptr));
-        else
+      if (P.tc && !P.bands.empty()) {  // all owned pieces in one tcgen05 launch
+        const int planes = P.kh ? P.kplanes : 1;
+        std::vector<T2Region> regs(P.bands.size());
+        std::vector<CUtensorMap> maps(P.bands.size() * planes);
+        int64_t items = 0;
+        for (size_t r = 0; r < P.bands.size(); ++r) {
+          const SymBand &b = P.bands[r];
+          T2Region &g = regs[r];
+          g.j0 = (int64_t)b.band * SYM_TB;  // rows of the piece, columns >= the band start
+          g.i0 = g.j0 + b.row0;
+          g.m = b.rows;
+          g.ncov = b.ldb;
+          g.item0 = items;
+          g.tiles_m = (int32_t)ceil_div(b.rows, T2_BM);
+          g.tiles_n = (int32_t)ceil_div(b.ldb, 256);
+          items += (int64_t)g.tiles_m * g.tiles_n;
+          for (int pl = 0; pl < planes; ++pl) {
+            void *out = P.kh ? (void *)((__half *)h->K + pl * P.kelems + b.koff) : (void *)(h->K + b.koff);
+            if (tc_encode_out_map(&maps[r * planes + pl], out, b.rows, b.ldb, b.ldb, P.kh))
+              return fail(KKM_ECUDA, "%s", tc_gemm_error());
+          }
+        }
+        T2Region *gregs = (T2Region *)((uint8_t *)h->ws + P.o_gregs);
+        CUtensorMap *gmaps = (CUtensorMap *)((uint8_t *)h->ws + P.o_gmaps);
+        CK(cudaMemcpyAsync(gregs, regs.data(), regs.size() * sizeof(T2Region), cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(gmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
+        if (tc2_gemm_launch_multi(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, gregs,
+                                  (int)regs.size(), items, gmaps, h->norms, h->kp, P.kh ? h->kscale : 0.f, planes,
+                                  h->st, &h->launches)) {
+          h->poisoned = true;
+          return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
+        }
+        CK(cudaStreamSynchronize(h->st));  // (host copies of the regions and maps go out of scope)
+      } else {
+        for (const SymBand &b : P.bands) {
+          const int64_t j0 = (int64_t)b.band * SYM_TB, i0 = j0 + b.row0;  // rows of the piece, columns >= band start
           CKR(launch_gemm(h, i0, b.rows, j0, b.ldb, h->K + b.koff, b.ldb));
+        }
       }
     } else if (P.materialize) {
       CKR(launch_gemm(h, P.a0, P.nA, P.b0, P.ldk, h->K, P.ldk));

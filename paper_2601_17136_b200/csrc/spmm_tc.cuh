@@ -11,7 +11,7 @@
 // the labels. Accumulators live in TMEM (fp32); no per-element instruction touches K, so the
 // kernel is a pure HBM stream of half the bytes of the fp32 bands.
 //
-// Work unit = (owned band piece, 512-row slab = 4 row tiles, split of <= 8 chunks of 128 columns).
+// Work unit = (owned band piece, 512-row slab = 4 row tiles, split of <= 8 or 16 chunks of 128 columns).
 // Per chunk and row tile the row MMAs go to D_row[tile] and the column MMAs to D_col (skipped on
 // the diagonal block K_II, which the row part covers whole); an accumulator holds 2 chunks (row
 // sums) or 2 row tiles (column sums) and is then drained into fp64 registers: the column sums of
@@ -37,10 +37,6 @@ constexpr int TS_TB = 1024;            // band height (rows) = SYM_TB
 constexpr int TS_ROWS = 128;           // row tile
 constexpr int TS_CH = 128;             // chunk columns
 constexpr int TS_SLAB_TILES = 4;       // row tiles per unit (512 rows)
-#ifndef KKM_TS_SPLIT
-#define KKM_TS_SPLIT 8
-#endif
-constexpr int TS_SPLIT_CHUNKS = KKM_TS_SPLIT;  // chunks per unit (1024 columns: 4 MB units of the two planes were too coarse for 4 GPUs)
 constexpr int TS_STAGES = 5;
 constexpr uint32_t TS_TILE_BYTES = TS_ROWS * TS_CH * 2;  // 32 KB: 2 column halves x [128 rows x 128 B]
 constexpr uint32_t TS_OH_BYTES = 16 * 128 * 2;           // one-hot: 2 halves x [16 labels x 128 B]

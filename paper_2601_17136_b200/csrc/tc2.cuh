@@ -307,7 +307,17 @@ __device__ __forceinline__ void tmem_ld2_32(uint32_t t_main, uint32_t t_corr, fl
 struct T2GemmSched {
   int64_t nitems;
   int tiles_m, tiles_n;  // pair tiles (256 rows) x 256-column tiles
-  int64_t i0, j0;
+  int64_t i0, j0, m, ncov;
+  // the output region of work item u (one region: the kernel's tm_out / tm_out2, ridx = -1)
+  __device__ __forceinline__ void region(int64_t u, int &tm, int &tn, int64_t &ri0, int64_t &rm, int64_t &rj0,
+                                         int64_t &rncov, int &ridx) const {
+    coords(u, tm, tn);
+    ri0 = i0;
+    rm = m;
+    rj0 = j0;
+    rncov = ncov;
+    ridx = -1;
+  }
   __device__ __forceinline__ void coords(int64_t u, int &tm, int &tn) const {
     const int64_t per_group = (int64_t)T2_GROUP_M * tiles_n;
     const int64_t g = u / per_group;
@@ -326,15 +336,58 @@ struct T2GemmSched {
   }
 };
 
+// Several output regions in one launch (the f1 band pieces): region r = rows [i0, i0 + m) x
+// columns [j0, j0 + ncov) stored through the tensor map(s) omaps[r * planes + plane] (global
+// memory); its tiles are work items [item0, item0 + tiles_m * tiles_n), row tiles fastest.
+struct T2Region {
+  int64_t i0, m, j0, ncov, item0;
+  int32_t tiles_m, tiles_n;
+};
+struct T2MultiSched {
+  int64_t nitems;
+  int nreg;
+  const T2Region *reg;
+  __device__ __forceinline__ int find(int64_t u) const {
+    int lo = 0, hi = nreg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (reg[mid].item0 <= u) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+  __device__ __forceinline__ void region(int64_t u, int &tm, int &tn, int64_t &ri0, int64_t &rm, int64_t &rj0,
+                                         int64_t &rncov, int &ridx) const {
+    ridx = find(u);
+    const T2Region g = reg[ridx];
+    const int64_t lu = u - g.item0;
+    tm = (int)(lu % g.tiles_m);
+    tn = (int)(lu / g.tiles_m);
+    ri0 = g.i0;
+    rm = g.m;
+    rj0 = g.j0;
+    rncov = g.ncov;
+  }
+  __device__ __forceinline__ void item(int64_t u, int &ra, int &rb0, int &ntn) const {
+    int tm, tn, r;
+    int64_t i0, m, j0, nc;
+    region(u, tm, tn, i0, m, j0, nc, r);
+    ra = (int)(i0 + (int64_t)tm * T2_BM);
+    rb0 = (int)(j0 + (int64_t)tn * 256);
+    ntn = 1;
+  }
+};
+
 constexpr size_t T2_GEMM_EXTRA = TC_EPI_WARPS * (TC_STAGING_BYTES + TC_COLC_BYTES);
 constexpr size_t T2_GEMM_SMEM = (size_t)T2_STAGES * T2_STAGE_BYTES + T2_GEMM_EXTRA + 1024 + 128;
 
+template <class Sched>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
                     const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_out2,
-                    uint32_t idesc, int nkb, int64_t n,
-                    int64_t i0, int64_t m, int64_t j0, int64_t ncov, const float *__restrict__ norms,
-                    const float *__restrict__ rscale, KappaParams kp, T2GemmSched sc, float oscale, int planes) {
+                    const CUtensorMap *__restrict__ omaps, uint32_t idesc, int nkb, int64_t n,
+                    const float *__restrict__ norms, const float *__restrict__ rscale, KappaParams kp, Sched sc,
+                    float oscale, int planes) {
   // oscale == 0: fp32 output; > 0: fp16 output of K' = K * oscale (f4 K storage): planes == 1
   // hi = RN(K') only, planes == 2 also lo = RN(K' - hi) through tm_out2 (hi + lo = K' to ~2^-22)
   extern __shared__ uint8_t smem_raw[];
@@ -361,8 +414,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     int64_t it = 0;
     for (int64_t u = cl; u < sc.nitems; u += ncl, ++it) {
-      int tm, tn;
-      sc.coords(u, tm, tn);
+      int tm, tn, ridx;
+      int64_t i0, m, j0, ncov;
+      sc.region(u, tm, tn, i0, m, j0, ncov, ridx);
+      const CUtensorMap *out1 = ridx < 0 ? &tm_out : omaps + (int64_t)ridx * planes;
+      const CUtensorMap *out2 = ridx < 0 ? &tm_out2 : out1 + 1;
       const int64_t ibase = i0 + (int64_t)tm * T2_BM + (int64_t)cr * 128 + quarter * 32;
       const int64_t i = ibase + lane;
       const bool row_ok = i < i0 + m && i < n;
@@ -418,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(pl ? &tm_out2 : &tm_out, (int)(jb - j0), (int)(ibase - i0), stg, evict);
+              tma_store_2d(pl ? out2 : out1, (int)(jb - j0), (int)(ibase - i0), stg, evict);
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
           }
@@ -437,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0 && jb + hh * 16 < j0 + ncov) {
-            tma_store_2d(&tm_out, (int)(jb + hh * 16 - j0), (int)(ibase - i0), stg, evict);
+            tma_store_2d(out1, (int)(jb + hh * 16 - j0), (int)(ibase - i0), stg, evict);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
@@ -801,8 +857,8 @@ inline int tc2_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, 
   if (!out_lo) g.map_out2 = g.map_out;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(tc2_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T2_GEMM_SMEM) !=
-        cudaSuccess) {
+    if (cudaFuncSetAttribute(tc2_gemm_kernel<T2GemmSched>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)T2_GEMM_SMEM) != cudaSuccess) {
       tc_err_slot() = "cudaFuncSetAttribute(tc2_gemm_kernel) failed";
       return 1;
     }
@@ -819,10 +875,53 @@ inline int tc2_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, 
   sc.nitems = (int64_t)sc.tiles_m * sc.tiles_n;
   sc.i0 = i0;
   sc.j0 = j0;
+  sc.m = m;
+  sc.ncov = ncov;
   const int64_t clusters = sc.nitems < g.num_sms / 2 ? sc.nitems : g.num_sms / 2;
-  tc2_gemm_kernel<<<(unsigned)(2 * clusters), T2_THREADS, T2_GEMM_SMEM, st>>>(
-      g.map_hi, g.map_lo, g.map_out, g.map_out2, t2_idesc(fp16), (int)(dp / TC_BK), n, i0, m, j0, ncov, norms,
+  tc2_gemm_kernel<T2GemmSched><<<(unsigned)(2 * clusters), T2_THREADS, T2_GEMM_SMEM, st>>>(
+      g.map_hi, g.map_lo, g.map_out, g.map_out2, nullptr, t2_idesc(fp16), (int)(dp / TC_BK), n, norms,
       fp16 ? rscale : nullptr, kp, sc, oscale, out_lo ? 2 : 1);
+  if (launches) ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    tc_err_slot() = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
+// Several output regions (the f1 band pieces) in ONE launch: the per-band launches left each
+// piece's last wave of CTA pairs partly idle. regs_dev: nreg regions (device), omaps: nreg * planes
+// output maps (device, 64-B aligned; fp32 maps when oscale == 0). nitems = total pair tiles.
+inline int tc2_gemm_launch_multi(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bool fp16,
+                                 const float *rscale, int64_t rows, int64_t dp, int64_t n, const T2Region *regs_dev,
+                                 int nreg, int64_t nitems, const CUtensorMap *omaps, const float *norms,
+                                 const KappaParams &kp, float oscale, int planes, cudaStream_t st, int64_t *launches) {
+  if (nitems <= 0) return 0;
+  if (g.hi != Xhi || g.lo != Xlo || g.fp16 != fp16)
+    if (tc_make_maps(g, Xhi, Xlo, fp16, rows, dp)) return 1;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc2_gemm_kernel<T2MultiSched>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)T2_GEMM_SMEM) != cudaSuccess) {
+      tc_err_slot() = "cudaFuncSetAttribute(tc2_gemm_kernel multi) failed";
+      return 1;
+    }
+    attr = true;
+  }
+  if (!g.num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  T2MultiSched sc;
+  sc.nitems = nitems;
+  sc.nreg = nreg;
+  sc.reg = regs_dev;
+  const int64_t clusters = nitems < g.num_sms / 2 ? nitems : g.num_sms / 2;
+  tc2_gemm_kernel<T2MultiSched><<<(unsigned)(2 * clusters), T2_THREADS, T2_GEMM_SMEM, st>>>(
+      g.map_hi, g.map_lo, g.map_hi, g.map_hi, omaps, t2_idesc(fp16), (int)(dp / TC_BK), n, norms,
+      fp16 ? rscale : nullptr, kp, sc, oscale, planes);
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
