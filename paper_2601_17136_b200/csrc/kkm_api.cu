@@ -71,6 +71,7 @@ struct Plan {
   // sizes / changed allreduce remain: one collective per iteration instead of three
   bool repl;
   int64_t a_row0, a_n, a_B;  // the a3/a4 rows: [a_row0, a_row0 + a_n), buffers of a_B rows
+  bool a3fix;  // a3 reads the int64 S of spmm_tc directly and finishes c / J in its last block
   int64_t dmax, dpad;
   // f1 symmetric storage (sym.cuh): bands of SYM_TB rows, the rank's share spread by area
   bool sym;
@@ -90,7 +91,7 @@ struct Plan {
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_gregs, o_gmaps, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_gregs, o_gmaps, o_a3ctr, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
       o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
 };
 
@@ -349,6 +350,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.a_B = P.repl ? P.npad : P.B;
   if (P.repl) P.s_rows_pad = P.npad;
   P.fused = (nranks == 1 || P.repl) && n <= FUSED_MAX_ROWS && P.k <= 16;
+  P.a3fix = P.kh && P.sym && !P.inc && !P.fused && (nranks == 1 || P.repl);
   if (P.inc && (P.pr > 1 || !P.tc))
     return fail(KKM_EUNSUP, "incremental S needs the 1D algorithm and a tensor-core precision");
   P.dmax = std::max<int64_t>(1, n / 16);
@@ -464,6 +466,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_tSmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
     P.o_fxmax = take(16);
   }
+  P.o_a3ctr = take(16);
   P.total = off;
   return KKM_OK;
 }
@@ -526,6 +529,7 @@ struct kkm_ctx {
   float *colpart = nullptr;
   double *colsum = nullptr, *Sfin = nullptr;
   int32_t *work = nullptr;  // spmm_sym's item scheduler (2 counters, zero between launches)
+  unsigned *a3ctr = nullptr;  // finalize's last-block counter (zero between launches)
   // f4 fp16 K storage
   CUtensorMap *tmaps = nullptr;
   TsBand *tbands = nullptr;
@@ -797,6 +801,10 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
     const unsigned gr = (unsigned)ceil_div(P.npad * k, 256);
     if (P.repl)  // S of all points on every rank (exact int64 sum)
       CKN(ncclAllReduce(h->tSfix, h->tSfix, (size_t)P.npad * k, ncclInt64, ncclSum, h->comm, h->st));
+    if (P.a3fix) {  // run_cnorm's finalize reads tSfix directly
+      *s_out = nullptr;
+      return KKM_OK;
+    }
     if (P.nranks == 1 || P.repl) {
       ts_fix_out_kernel<<<gr, 256, 0, h->st>>>(h->tSfix, P.n, P.npad, k, h->tfx_inv, nullptr, h->Sfin);
       CKL();
@@ -922,6 +930,15 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
   const int32_t *sizes = h->sizes[h->cur];
   const int k1 = P.k + 1;
   const int nr = P.repl ? 1 : P.nranks, r = P.repl ? 0 : P.rank;  // replicated a3: one "rank"
+  if (P.a3fix && P.a_n > 0) {  // int64 S in, c and J from the last block (same sums as below)
+    int fth = FIN_THREADS;
+    while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
+    finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
+        nullptr, 1, P.a_n, P.npad, P.k, sizes, labels + P.a_row0, h->diag, P.rows_per_block, E_out, h->blockpart,
+        h->tSfix, h->tfx_inv, A3Fused{h->a3ctr, sizes, cnorm_out, J_out, sizes_next, changed_out});
+    CKL();
+    return KKM_OK;
+  }
   if (P.a_n > 0) {
     int fth = FIN_THREADS;  // power of two with (k+1) * fth doubles <= 48 KB
     while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
@@ -1099,6 +1116,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   }
   h->Spart = (double *)(w + P.o_Spart);
   h->E = (double *)(w + P.o_E);
+  h->a3ctr = (unsigned *)(w + P.o_a3ctr);
   h->blockpart = (double *)(w + P.o_blockpart);
   h->rankpart = (double *)(w + P.o_rankpart);
   h->cnorm = (double *)(w + P.o_cnorm);
@@ -1264,6 +1282,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
                            h->st));
       CK(cudaMemcpyAsync(h->band_desc, P.band_desc.data(), (size_t)P.T * 4, cudaMemcpyHostToDevice, h->st));
       CK(cudaMemsetAsync(h->work, 0, 2 * 4, h->st));
+      CK(cudaMemsetAsync(h->a3ctr, 0, 16, h->st));
       if (P.kh) {  // f4: storage scale 2^e with |K| 2^e <= 60000 (|K_ij| <= max_i K_ii, bounded as for ssym)
         max_norm_kernel<<<1, 1024, 0, h->st>>>(h->norms, P.n, h->fxmax);
         CKL();

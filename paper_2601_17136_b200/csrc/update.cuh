@@ -17,12 +17,57 @@ constexpr int FIN_THREADS = 128;
 
 // grid: nblocks; block b handles rows [b * rows_per_block, ...). blockDim.x: a power of two
 // <= FIN_THREADS; dynamic smem: (k + 1) * blockDim.x doubles.
+// Sfix (optional): read S as int64 fixed point, Sfix[c * rows_pad + i] * inv (the 16-bit band
+// path, spmm_tc.cuh) instead of the fp64 partials. fin (optional): the last block to finish also
+// does cnorm_local + cnorm_final for a single "rank" (one rank, or the replicated a3 of §6) -- the
+// same fixed-order sums, so the results are bitwise those of the separate kernels.
+struct A3Fused {
+  unsigned *counter;       // zero between launches (the last block resets it)
+  const int32_t *sizes;
+  double *cnorm, *J_out;
+  int32_t *sizes_next;
+  unsigned long long *changed_out;
+};
+
+__device__ __forceinline__ void cnorm_reduce_last(const double *__restrict__ blockpart, int nblocks, int k,
+                                                  const A3Fused &f) {
+  // = cnorm_local_kernel (one warp per c, lanes over blocks, fixed shuffle tree) + cnorm_final_kernel
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x >> 5; c <= k; c += nw) {
+    double sum = 0.0;
+    int b = lane;
+    for (; b + 32 * 7 < nblocks; b += 32 * 8) {  // 8 L2 loads in flight, added in the same order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(blockpart + (int64_t)(b + 32 * u) * (k + 1) + c);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; b < nblocks; b += 32) sum += __ldcg(blockpart + (int64_t)b * (k + 1) + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+      const double s = 0.0 + sum;  // (cnorm_final: the sum over one rank)
+      if (c < k) {
+        const int32_t sz = f.sizes[c];
+        f.cnorm[c] = sz > 0 ? s / (double)sz : __longlong_as_double(0x7ff0000000000000LL);  // +inf
+        if (f.sizes_next) f.sizes_next[c] = 0;
+      } else if (f.J_out) {
+        *f.J_out = s;
+      }
+    }
+  }
+  if (threadIdx.x == 0 && f.changed_out) *f.changed_out = 0ull;
+}
+
 __global__ void __launch_bounds__(128) finalize_kernel(
     const double *__restrict__ Spart, int nsplit, int64_t nrows, int64_t rows_pad, int k,
     const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl_local,
     const double *__restrict__ diag, int64_t rows_per_block, double *__restrict__ E,
-    double *__restrict__ blockpart) {
+    double *__restrict__ blockpart, const long long *__restrict__ Sfix = nullptr, double inv = 1.0,
+    A3Fused fin = A3Fused{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}) {
   extern __shared__ double sacc[];  // [(k + 1)][blockDim.x]
+  __shared__ unsigned s_last;
   const int T = blockDim.x;
   const int t = threadIdx.x;
   for (int c = 0; c <= k; ++c) sacc[c * T + t] = 0.0;
@@ -31,13 +76,32 @@ __global__ void __launch_bounds__(128) finalize_kernel(
   for (int64_t i = rb + t; i < re; i += T) {
     const int li = cl_local[i];
     double zi = 0.0;
-    for (int c = 0; c < k; ++c) {
-      double s = 0.0;
-      for (int p = 0; p < nsplit; ++p) s += Spart[((int64_t)p * rows_pad + i) * k + c];
-      const int32_t sz = sizes[c];
-      const double e = sz > 0 ? s / (double)sz : 0.0;
-      E[i * k + c] = e;
-      if (c == li) zi = e;
+    if (Sfix && k <= 16) {  // all k loads in flight first (the caller guarantees k <= 16 here)
+      long long sv[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) sv[c] = c < k ? Sfix[(int64_t)c * rows_pad + i] : 0ll;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < k) {
+          const double s = 0.0 + (double)sv[c] * inv;
+          const int32_t sz = sizes[c];
+          const double e = sz > 0 ? s / (double)sz : 0.0;
+          E[i * k + c] = e;
+          if (c == li) zi = e;
+        }
+    } else {
+      for (int c = 0; c < k; ++c) {
+        double s = 0.0;
+        if (Sfix) {
+          s += (double)Sfix[(int64_t)c * rows_pad + i] * inv;
+        } else {
+          for (int p = 0; p < nsplit; ++p) s += Spart[((int64_t)p * rows_pad + i) * k + c];
+        }
+        const int32_t sz = sizes[c];
+        const double e = sz > 0 ? s / (double)sz : 0.0;
+        E[i * k + c] = e;
+        if (c == li) zi = e;
+      }
     }
     sacc[li * T + t] += zi;
     sacc[k * T + t] += diag[i] - zi;
@@ -49,6 +113,18 @@ __global__ void __launch_bounds__(128) finalize_kernel(
     __syncthreads();
   }
   for (int c = t; c <= k; c += T) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sacc[c * T];
+  if (!fin.counter) return;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    s_last = atomicAdd(fin.counter, 1u) == gridDim.x - 1;
+    if (s_last) {
+      *fin.counter = 0u;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (s_last) cnorm_reduce_last(blockpart, gridDim.x, k, fin);
 }
 
 // out[c] = sum_b blockpart[b][c]: one warp per c, lane l sums b = l, l + 32, ... in order,
