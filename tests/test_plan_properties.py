@@ -14,10 +14,12 @@ ERRS = ("EINVAL", "EUNSUP")
 @settings(max_examples=300, deadline=None)
 @given(n=st.integers(1, 300000), d=st.integers(1, 1200), k=st.integers(1, 80), nranks=st.sampled_from([1, 2, 3, 4, 8]),
        grid_rows=st.sampled_from([0, 1, 2, 4]), path=st.sampled_from([0, 1, 2]), prec=st.sampled_from([0, 1, 2]),
-       sym=st.sampled_from([0, 1, 2]), inc=st.sampled_from([0, 1]), kind=st.sampled_from([0, 1, 2]))
-def test_workspace_plan(n, d, k, nranks, grid_rows, path, prec, sym, inc, kind):
+       sym=st.sampled_from([0, 1, 2]), inc=st.sampled_from([0, 1]), kind=st.sampled_from([0, 1, 2]),
+       kstore=st.sampled_from([0, 1, 2, 3]))
+def test_workspace_plan(n, d, k, nranks, grid_rows, path, prec, sym, inc, kind, kstore):
     p = kkm.default_params()
     p.k, p.kind, p.path, p.precision, p.symmetric, p.incremental = k, kind, path, prec, sym, inc
+    p.kstore = kstore
     p.grid_rows = grid_rows
     sizes, errs = [], []
     for r in range(nranks):
@@ -37,3 +39,10 @@ def test_workspace_plan(n, d, k, nranks, grid_rows, path, prec, sym, inc, kind):
         assert grid_rows <= 1 and prec != kkm.PREC_FP32_SIMT
     if path == kkm.PATH_STREAM:
         assert prec != kkm.PREC_FP32_SIMT
+    if kstore in (kkm.KSTORE_FP16, kkm.KSTORE_FP16X2):  # 16-bit bands: materialised 1D f1 only
+        assert prec != kkm.PREC_FP32_SIMT and k <= 16 and grid_rows <= 1 and sym != kkm.SYM_OFF
+        assert path != kkm.PATH_STREAM
+        # the bands (about n^2 / 2 values over the ranks) at 2 or 4 bytes per value
+        tot = sum(sizes)
+        per = 2 if kstore == kkm.KSTORE_FP16 else 4
+        assert tot >= 0.45 * per * n * n * 0.999 - 1e6
