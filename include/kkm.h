@@ -266,6 +266,15 @@ int kkm_debug_read(kkm_handle h, int32_t what, void *dst);
  * row-major). Test hook for kernel-value parity. Independent of the stored K. */
 int kkm_kernel_tile(kkm_handle h, int64_t i0, int64_t j0, int32_t m, int32_t nc, float *dst);
 
+/* Reads back row i (global index) of the K this rank STORED when materialising, as the a2
+ * kernels will read it: dst (host) receives n doubles, dst[j] = the stored K(i, j) (fp32 bands
+ * or full rows as stored; 16-bit bands: (hi + lo) * 2^-e, or hi * 2^-e for FP16) for every
+ * column j the rank stores for row i -- the f1 band piece holding row i stores j >= the band
+ * start, full K rows the rank's B set -- and NaN for the others. KKM_ESTATE when the handle
+ * streams (nothing stored) or the rank does not store row i. Synchronises. Test hook for the
+ * kernel-value parity of the storage formats (DESIGN A27). */
+int kkm_stored_k_row(kkm_handle h, int64_t i, double *dst);
+
 /* Per-phase milliseconds (KKM_NPHASES floats, host) accumulated since init
  * when params.timing = 1; zeros otherwise. */
 int kkm_phase_ms(kkm_handle h, float *ms);

@@ -1754,6 +1754,51 @@ int kkm_debug_read(kkm_handle h, int32_t what, void *dst) {
   return KKM_OK;
 }
 
+int kkm_stored_k_row(kkm_handle h, int64_t i, double *dst) {
+  if (!h || !dst) return fail(KKM_EINVAL, "NULL argument");
+  if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");
+  const Plan &P = h->P;
+  if (i < 0 || i >= P.n) return fail(KKM_EINVAL, "row %lld out of range", (long long)i);
+  if (!P.materialize) return fail(KKM_ESTATE, "the handle streams K: nothing is stored");
+  std::vector<double> out((size_t)P.n, std::nan(""));
+  if (P.sym) {
+    const SymBand *piece = nullptr;
+    for (const SymBand &b : P.bands) {
+      const int64_t r0 = (int64_t)b.band * SYM_TB + b.row0;
+      if (i >= r0 && i < r0 + b.rows) piece = &b;
+    }
+    if (!piece) return fail(KKM_ESTATE, "row %lld is not stored on this rank", (long long)i);
+    const int64_t j0 = (int64_t)piece->band * SYM_TB;
+    const int64_t r = i - j0 - piece->row0, cols = P.n - j0;
+    if (P.kh) {
+      std::vector<__half> hi((size_t)cols), lo((size_t)cols);
+      const __half *base = (const __half *)h->K + piece->koff + r * piece->ldb;
+      CK(cudaMemcpyAsync(hi.data(), base, (size_t)cols * 2, cudaMemcpyDeviceToHost, h->st));
+      if (P.kplanes > 1)
+        CK(cudaMemcpyAsync(lo.data(), base + P.kelems, (size_t)cols * 2, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      const double inv = 1.0 / (double)h->kscale;
+      for (int64_t j = 0; j < cols; ++j)
+        out[(size_t)(j0 + j)] = ((double)__half2float(hi[(size_t)j]) +
+                                 (P.kplanes > 1 ? (double)__half2float(lo[(size_t)j]) : 0.0)) * inv;
+    } else {
+      std::vector<float> v((size_t)cols);
+      CK(cudaMemcpyAsync(v.data(), h->K + piece->koff + r * piece->ldb, (size_t)cols * 4, cudaMemcpyDeviceToHost,
+                         h->st));
+      CK(cudaStreamSynchronize(h->st));
+      for (int64_t j = 0; j < cols; ++j) out[(size_t)(j0 + j)] = v[(size_t)j];
+    }
+  } else {  // full K rows: the A set's rows x the B set's columns
+    if (i < P.a0 || i >= P.a0 + P.nA) return fail(KKM_ESTATE, "row %lld is not stored on this rank", (long long)i);
+    std::vector<float> v((size_t)P.nB);
+    CK(cudaMemcpyAsync(v.data(), h->K + (i - P.a0) * P.ldk, (size_t)P.nB * 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    for (int64_t j = 0; j < P.nB; ++j) out[(size_t)(P.b0 + j)] = v[(size_t)j];
+  }
+  std::memcpy(dst, out.data(), (size_t)P.n * 8);
+  return KKM_OK;
+}
+
 int kkm_kernel_tile(kkm_handle h, int64_t i0, int64_t j0, int32_t m, int32_t nc, float *dst) {
   if (!h || !dst) return fail(KKM_EINVAL, "NULL argument");
   if (h->poisoned) return fail(KKM_ESTATE, "handle is poisoned");

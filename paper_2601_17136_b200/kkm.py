@@ -69,6 +69,7 @@ def lib():
             "kkm_seed_kmeanspp": [P, P, P],
             "kkm_debug_read": [P, i32, P],
             "kkm_kernel_tile": [P, i64, i64, i32, i32, P],
+            "kkm_stored_k_row": [P, i64, P],
             "kkm_phase_ms": [P, P],
             "kkm_launch_count": [P, P],
             "kkm_destroy": [P],
@@ -264,6 +265,12 @@ class KernelKMeans:
     def kernel_tile(self, i0: int, j0: int, m: int, nc: int) -> np.ndarray:
         out = np.zeros((m, nc), dtype=np.float32)
         _check(lib().kkm_kernel_tile(self.h, i0, j0, m, nc, _ptr(out)))
+        return out
+
+    def stored_k_row(self, i: int) -> np.ndarray:
+        """Row i of the K this rank stored (kkm_stored_k_row): n doubles, NaN where not stored."""
+        out = np.empty(self.n, dtype=np.float64)
+        _check(lib().kkm_stored_k_row(self.h, int(i), _ptr(out)))
         return out
 
     def phase_ms(self) -> dict:

@@ -15,7 +15,7 @@ import pytest
 
 import oracle
 import synth
-from parity import check_iteration, j_tol
+from parity import check_iteration, check_kernel_values, j_tol
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -129,3 +129,34 @@ def test_errors():
     with pytest.raises(kkm.KKMError, match="EUNSUP"):
         kkm.KernelKMeans(Xd, 500, 3, kkm.KERNEL_GAUSSIAN, 0.1, 0.0, 1, path=kkm.PATH_STREAM,
                          kstore=kkm.KSTORE_FP16)
+
+
+@pytest.mark.parametrize("name,n", [("mnist60k", 3000), ("har200k", 2500)])
+@pytest.mark.parametrize("kstore,tau", [(kkm.KSTORE_FP32, 1e-4), (kkm.KSTORE_FP16X2, 1e-4),
+                                        (kkm.KSTORE_FP16, U * 1.01 + 2e-6)],
+                         ids=["fp32", "fp16x2", "fp16"])
+def test_stored_k_values(name, n, kstore, tau):
+    """The K each storage format holds (kkm_stored_k_row, the values a2 reads) against the oracle's
+    fp64 rows under the A10 K rule: fp32 bands and the hi + lo planes within 1e-4 (the north star's
+    kernel-value tolerance; hi + lo is fp32-class), the fp16 plane within its 2^-11 (A27). Rows at
+    band edges and in the ragged last band; the stored part of a row is columns >= its band start."""
+    X, cfg = synth.make_config(name, n=n)
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    h = kkm.KernelKMeans(torch.from_numpy(X).cuda(), n, cfg["k"], *args, max_iter=0,
+                         precision=kkm.PREC_FP16X3, path=kkm.PATH_MATERIALIZE, symmetric=kkm.SYM_ON, kstore=kstore)
+    diag = oracle.kernel_diag(X, *args)
+    rows = [0, 1023, 1024, 2047, n - 1]
+    Kr = oracle.kernel_rows(X, np.array(rows), *args)
+    for a, i in enumerate(rows):
+        row = h.stored_k_row(i)
+        j0 = (i // 1024) * 1024
+        assert np.isnan(row[:j0]).all() and not np.isnan(row[j0:]).any()
+        check_kernel_values(row[None, j0:], Kr[a:a + 1, j0:], diag[i:i + 1], diag[j0:], tau=tau)
+    h.destroy()
+    # full K rows (symmetric off): every column of the rank's rows, fp32
+    if kstore == kkm.KSTORE_FP32:
+        f = kkm.KernelKMeans(torch.from_numpy(X).cuda(), n, cfg["k"], *args, max_iter=0,
+                             precision=kkm.PREC_FP16X3, path=kkm.PATH_MATERIALIZE, symmetric=kkm.SYM_OFF)
+        row = f.stored_k_row(rows[2])
+        check_kernel_values(row[None, :], Kr[2:3], diag[rows[2]:rows[2] + 1], diag)
+        f.destroy()
