@@ -83,7 +83,7 @@ struct Plan {
   // f4 fp16 K storage (spmm_tc.cuh): the f1 bands in fp16, a2 on the tensor cores
   bool kh;
   int kplanes;                      // 16-bit planes per K value: 1 (FP16) or 2 (FP16X2: hi + lo)
-  int ts_nsm;                       // max column splits of a band (Srow pitch)
+  int ts_nsm;                       // max column splits of a band (informational)
   std::vector<TsBand> tbands;       // owned bands (same order as bands)
   std::vector<TsUnit> tunits;
   std::vector<int4> units;          // its work units on this rank

@@ -1,5 +1,7 @@
-// spmm_tc.cuh -- f4 low-precision K storage (the paper's mixed-precision future
-// work P:875): a2 over the f1 upper-triangle bands (sym.cuh) stored in fp16, on the tensor cores.
+// spmm_tc.cuh -- a2 on the tensor cores over the f1 upper-triangle bands (sym.cuh) stored in 16-bit
+// planes: the default (kstore AUTO / FP16X2: hi = RN(K 2^e), lo = RN(K 2^e - hi), fp32-class) and
+// f4's low-precision storage (FP16: hi only, the paper's mixed-precision future
+// work P:875).
 //
 // With K in a 16-bit type the SpMM's two reductions are dense contractions with 0/1 matrices:
 //   row part:    S_row(i, c) += sum_j K(i, j) [cl_j = c]        = (K . Onehot_colsᵀ)(i, c)
@@ -9,7 +11,8 @@
 // K-major for the row sums (M = rows) and MN-major for the column sums (M = columns, Kᵀ) -- the
 // same bytes, two descriptors. The 0/1 B operands (N = 16 labels) are built in shared memory from
 // the labels. Accumulators live in TMEM (fp32); no per-element instruction touches K, so the
-// kernel is a pure HBM stream of half the bytes of the fp32 bands.
+// kernel is a pure HBM stream (hi + lo: the fp32 band bytes at ~0.97 of the copy peak; FP16:
+// half of them). Both planes of a tile are fed as two stages into the same accumulators.
 //
 // Work unit = (owned band piece, 512-row slab = 4 row tiles, split of <= 8 or 16 chunks of 128 columns).
 // Per chunk and row tile the row MMAs go to D_row[tile] and the column MMAs to D_col (skipped on
