@@ -530,6 +530,13 @@ struct kkm_ctx {
   double *colsum = nullptr, *Sfin = nullptr;
   int32_t *work = nullptr;  // spmm_sym's item scheduler (2 counters, zero between launches)
   unsigned *a3ctr = nullptr;  // finalize's last-block counter (zero between launches)
+  // peer-memory exchange of S (16-bit bands, replicated a3, several ranks): own IPC buffer
+  // [2 epochs][k][npad] int64 + flag + peer table; peers' buffers mapped with cudaIpcOpenMemHandle
+  bool p2p = false;
+  uint8_t *xbuf = nullptr;
+  std::vector<void *> xpeers;  // opened peer mappings (closed in destroy)
+  const uint8_t **xtable = nullptr;  // device [nranks] bases (inside xbuf)
+  unsigned long long epoch = 0;
   // f4 fp16 K storage
   CUtensorMap *tmaps = nullptr;
   TsBand *tbands = nullptr;
@@ -788,16 +795,28 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
       CK(cudaFuncSetAttribute(spmm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM));
       attr_set = true;
     }
-    CK(cudaMemsetAsync(h->tSfix, 0, (size_t)P.npad * k * 8, h->st));
+    long long *Sx = h->tSfix;
+    if (h->p2p) {  // this epoch's half of the own exchange buffer (the other half may still be read)
+      ++h->epoch;
+      Sx = (long long *)(h->xbuf + (h->epoch & 1) * (size_t)P.npad * k * 8);
+    }
+    CK(cudaMemsetAsync(Sx, 0, (size_t)P.npad * k * 8, h->st));
     a2_mark(h);
     if (!P.tunits.empty()) {
       const int grid = (int)std::min<int64_t>((int64_t)P.tunits.size(), h->num_sms);
       spmm_tc_kernel<<<grid, TS_THREADS, TS_SMEM, h->st>>>(h->tmaps, h->tbands, h->tunits, (int)P.tunits.size(),
-                                                           labels, P.n, k, P.npad, h->tfxm, h->tSfix, h->work,
+                                                           labels, P.n, k, P.npad, h->tfxm, Sx, h->work,
                                                            P.kplanes);
       CKL();
     }
     a2_mark(h);
+    if (h->p2p) {  // publish; run_cnorm's finalize sums the ranks' S over NVLink
+      peer_signal_kernel<<<1, 1, 0, h->st>>>(
+          (unsigned long long *)(h->xbuf + 2 * (size_t)P.npad * k * 8), h->epoch);
+      CKL();
+      *s_out = nullptr;
+      return KKM_OK;
+    }
     const unsigned gr = (unsigned)ceil_div(P.npad * k, 256);
     if (P.repl)  // S of all points on every rank (exact int64 sum)
       CKN(ncclAllReduce(h->tSfix, h->tSfix, (size_t)P.npad * k, ncclInt64, ncclSum, h->comm, h->st));
@@ -933,9 +952,12 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
   if (P.a3fix && P.a_n > 0) {  // int64 S in, c and J from the last block (same sums as below)
     int fth = FIN_THREADS;
     while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
+    const A3Peers peers = h->p2p ? A3Peers{h->xtable, P.nranks, (int64_t)((h->epoch & 1) * (size_t)P.npad * P.k * 8),
+                                           (int64_t)(2 * (size_t)P.npad * P.k * 8), h->epoch}
+                                 : A3Peers{nullptr, 0, 0, 0, 0ull};
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
         nullptr, 1, P.a_n, P.npad, P.k, sizes, labels + P.a_row0, h->diag, P.rows_per_block, E_out, h->blockpart,
-        h->tSfix, h->tfx_inv, A3Fused{h->a3ctr, sizes, cnorm_out, J_out, sizes_next, changed_out});
+        h->tSfix, h->tfx_inv, A3Fused{h->a3ctr, sizes, cnorm_out, J_out, sizes_next, changed_out}, peers);
     CKL();
     return KKM_OK;
   }
@@ -1073,6 +1095,70 @@ int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, 
 }
 
 const char *kkm_last_error(void) { return g_err; }
+
+// Peer-memory exchange of S for the replicated a3 (16-bit bands, several ranks, §6): an own
+// cudaMalloc'd buffer [2 epochs of k x npad int64 | epoch flag | peer table], its IPC handle
+// allgathered over NCCL and the peers' buffers opened here. All ranks must agree: the outcome is
+// allreduced (min) and any failure leaves every rank on the NCCL allreduce path. Collective.
+int setup_p2p(kkm_ctx *h) {
+  const Plan &P = h->P;
+  const size_t sbytes = (size_t)P.npad * P.k * 8;
+  const size_t xbytes = 2 * sbytes + 256 + (size_t)P.nranks * 8;
+  int ok = 1;
+  char *dh = nullptr;
+  std::vector<char> hs((size_t)64 * P.nranks);
+  std::vector<const uint8_t *> bases((size_t)P.nranks, nullptr);
+  if (cudaMalloc(&h->xbuf, xbytes) != cudaSuccess) {
+    h->xbuf = nullptr;
+    ok = 0;
+  }
+  if (ok && cudaMemset(h->xbuf, 0, xbytes) != cudaSuccess) ok = 0;
+  cudaIpcMemHandle_t mine;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (ok && cudaIpcGetMemHandle(&mine, h->xbuf) != cudaSuccess) ok = 0;
+  if (cudaMalloc(&dh, hs.size() + 8) != cudaSuccess) return fail(KKM_ECUDA, "cudaMalloc (IPC handles) failed");
+  if (ok) CK(cudaMemcpy(dh + 64 * (size_t)P.rank, &mine, 64, cudaMemcpyHostToDevice));
+  CKN(ncclAllGather(dh + 64 * (size_t)P.rank, dh, 64, ncclChar, h->comm, h->st));
+  CK(cudaMemcpyAsync(hs.data(), dh, hs.size(), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (ok) {
+    for (int r = 0; r < P.nranks; ++r) {
+      if (r == P.rank) {
+        bases[(size_t)r] = h->xbuf;
+        continue;
+      }
+      cudaIpcMemHandle_t hr;
+      std::memcpy(&hr, hs.data() + 64 * (size_t)r, 64);
+      void *q = nullptr;
+      if (cudaIpcOpenMemHandle(&q, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      h->xpeers.push_back(q);
+      bases[(size_t)r] = (const uint8_t *)q;
+    }
+  }
+  // every rank on the same path
+  int *dok = (int *)(dh + hs.size());
+  CK(cudaMemcpy(dok, &ok, 4, cudaMemcpyHostToDevice));
+  CKN(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, h->comm, h->st));
+  CK(cudaMemcpyAsync(&ok, dok, 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(dh);
+  if (ok) {
+    h->xtable = (const uint8_t **)(h->xbuf + 2 * sbytes + 256);
+    CK(cudaMemcpy((void *)h->xtable, bases.data(), (size_t)P.nranks * 8, cudaMemcpyHostToDevice));
+    h->p2p = true;
+    return KKM_OK;
+  }
+  for (void *q : h->xpeers) cudaIpcCloseMemHandle(q);
+  h->xpeers.clear();
+  if (h->xbuf) cudaFree(h->xbuf);
+  h->xbuf = nullptr;
+  cudaGetLastError();
+  return KKM_OK;  // NCCL allreduce path
+}
 
 int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t n, int64_t d,
              int64_t ldx, int32_t rank, int32_t nranks, const int32_t *init_labels, void *workspace,
@@ -1379,6 +1465,8 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
       else if (cudaStreamSynchronize(h->st) != cudaSuccess) rc = fail(KKM_ECUDA, "warm-up sync failed");
     }
   }
+  // (p2p needs the a3 that reads the int64 S itself: a3fix; the single-CTA fused path reads fp64 S)
+  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1 && !std::getenv("KKM_NO_P2P")) rc = setup_p2p(h);
   if (rc) {
     delete h;
     return rc;
@@ -1835,6 +1923,14 @@ int kkm_launch_count(kkm_handle h, int64_t *count) {
 int kkm_destroy(kkm_handle h) {
   if (!h) return KKM_OK;
   cudaStreamSynchronize(h->st);
+  if (h->xbuf) {  // collective: no rank frees its exchange buffer while a peer may still read it
+    if (h->comm && !h->poisoned) {
+      ncclAllReduce(h->xbuf, h->xbuf, 1, ncclInt8, ncclMax, h->comm, h->st);  // (a barrier)
+      cudaStreamSynchronize(h->st);
+    }
+    for (void *q : h->xpeers) cudaIpcCloseMemHandle(q);
+    cudaFree(h->xbuf);
+  }
   if (h->colcomm) ncclCommDestroy(h->colcomm);
   delete h;
   return KKM_OK;
