@@ -22,9 +22,11 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="rings,mnist60k,har200k")
 ap.add_argument("--iters", type=int, default=0, help="override iterations (0 = config's)")
-ap.add_argument("--n", type=int, default=0, help="override n (labelled in the output)")
+ap.add_argument("--points", "--n", dest="n", type=int, default=0, help="override n (labelled in the output)")
 ap.add_argument("--grid-rows", type=int, default=1)
 ap.add_argument("--path", default="auto", choices=["auto", "mat", "stream"])
+ap.add_argument("--kstore", default="auto", choices=["auto", "fp32", "fp16", "fp16x2"],
+                help="materialised band storage (f4: fp16 = low-precision storage)")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -72,7 +74,9 @@ for name in a.configs.split(","):
     e0.record()
     h = kkm.KernelKMeans(Xd, n, cfg["k"], cfg["kind"], gamma, cfg.get("coef0", 0.0),
                          cfg.get("degree", 1), max_iter=iters, rank=rank, nranks=world, comm=comm,
-                         timing=True, path=path, grid_rows=a.grid_rows)
+                         timing=True, path=path, grid_rows=a.grid_rows,
+                         kstore={"auto": kkm.KSTORE_AUTO, "fp32": kkm.KSTORE_FP32, "fp16": kkm.KSTORE_FP16,
+                                 "fp16x2": kkm.KSTORE_FP16X2}[a.kstore])
     e1.record()
     it, J, ch = h.fit()
     e2.record()
@@ -94,9 +98,11 @@ for name in a.configs.split(","):
         d = Xl.shape[1]
         B = -(-n // world)
         loop_ms = (spmm_ms + cn_ms + as_ms) / it
-        out = {"config": name, "n": n, "d": d, "k": cfg["k"], "n_gpus": world,
+        out = {"config": name, "n": n, "d": d, "k": cfg["k"], "n_gpus": world, "kstore": a.kstore,
                "grid": f"{a.grid_rows}x{world // a.grid_rows}", "iterations": it,
-               "path": (("materialised (f1 bands, hi + lo fp16 planes, a2 on tensor cores)" if sym else "materialised")
+               "path": ((("materialised (f1 bands, " + {"fp16": "fp16 plane", "fp32": "fp32"}.get(
+                            a.kstore, "hi + lo fp16 planes") + (", a2 on tensor cores)" if a.kstore != "fp32" else ")"))
+                         if sym else "materialised")
                         if mat else
                         ("streaming (f1 upper triangle)" if cfg["k"] <= 16 and a.grid_rows <= 1
                          else "streaming")),
@@ -107,7 +113,10 @@ for name in a.configs.split(","):
         useful = 2.0 * B * n * d
         if mat:
             ldk = -(-n // 32) * 32
-            gbs = B * ldk * 4 / (spmm_ms / it * 1e-3) / 1e9
+            kbytes = B * ldk * 4  # full K rows of the rank
+            if sym:  # the rank's share of the upper-triangle bands, at the storage's bytes per value
+                kbytes = (n * (n + 1024) / 2) / world * (2 if a.kstore == "fp16" else 4)
+            gbs = kbytes / (spmm_ms / it * 1e-3) / 1e9
             out["a2_roofline"] = {"achieved_GBs": gbs, "frac_of_measured_hbm": gbs / peaks["hbm_gbs"]}
             if gemm_ms > 0:
                 tf = useful / (gemm_ms * 1e-3) / 1e12
