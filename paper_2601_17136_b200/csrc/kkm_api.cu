@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "kkm.h"
@@ -536,6 +538,7 @@ struct kkm_ctx {
   uint8_t *xbuf = nullptr;
   std::vector<void *> xpeers;  // opened peer mappings (closed in destroy)
   const uint8_t **xtable = nullptr;  // device [nranks] bases (inside xbuf)
+  size_t xflag_off = 0;              // byte offset of the epoch flag in every exchange buffer
   unsigned long long epoch = 0;
   // f4 fp16 K storage
   CUtensorMap *tmaps = nullptr;
@@ -1148,6 +1151,7 @@ int setup_p2p(kkm_ctx *h) {
   cudaFree(dh);
   if (ok) {
     h->xtable = (const uint8_t **)(h->xbuf + 2 * sbytes + 256);
+    h->xflag_off = 2 * sbytes;
     CK(cudaMemcpy((void *)h->xtable, bases.data(), (size_t)P.nranks * 8, cudaMemcpyHostToDevice));
     h->p2p = true;
     return KKM_OK;
@@ -1923,13 +1927,22 @@ int kkm_launch_count(kkm_handle h, int64_t *count) {
 int kkm_destroy(kkm_handle h) {
   if (!h) return KKM_OK;
   cudaStreamSynchronize(h->st);
-  if (h->xbuf) {  // collective: no rank frees its exchange buffer while a peer may still read it
-    if (h->comm && !h->poisoned) {
-      ncclAllReduce(h->xbuf, h->xbuf, 1, ncclInt8, ncclMax, h->comm, h->st);  // (a barrier)
-      cudaStreamSynchronize(h->st);
+  if (h->xbuf) {
+    // no rank frees its exchange buffer while a peer may still read it: raise the own flag to
+    // DONE (after the stream is idle) and wait, bounded, for every peer's DONE -- no NCCL here, so
+    // destroy stays safe after the communicator is gone or when handles die in any order
+    const unsigned long long done = ~0ull;
+    cudaMemcpy(h->xbuf + h->xflag_off, &done, 8, cudaMemcpyHostToDevice);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (void *q : h->xpeers) {
+      unsigned long long v = 0;
+      while (cudaMemcpy(&v, (uint8_t *)q + h->xflag_off, 8, cudaMemcpyDeviceToHost) == cudaSuccess && v != done &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::seconds(20))
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
     }
     for (void *q : h->xpeers) cudaIpcCloseMemHandle(q);
     cudaFree(h->xbuf);
+    cudaGetLastError();
   }
   if (h->colcomm) ncclCommDestroy(h->colcomm);
   delete h;
