@@ -1470,7 +1470,13 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     }
   }
   // (p2p needs the a3 that reads the int64 S itself: a3fix; the single-CTA fused path reads fp64 S)
-  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1 && !std::getenv("KKM_NO_P2P")) rc = setup_p2p(h);
+  // Every rank reads all (P - 1) peers' whole S, so the peer bytes grow with P while NCCL's (NVLS)
+  // allreduce does not: peer exchange up to 4 ranks (measured faster there), NCCL above
+  // (KKM_P2P_MAX_RANKS overrides; the same value on every rank, so all ranks take the same path).
+  int p2p_max = 4;
+  if (const char *e = std::getenv("KKM_P2P_MAX_RANKS")) p2p_max = std::atoi(e);
+  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1 && P.nranks <= p2p_max && !std::getenv("KKM_NO_P2P"))
+    rc = setup_p2p(h);
   if (rc) {
     delete h;
     return rc;
