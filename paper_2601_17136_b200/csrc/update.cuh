@@ -162,12 +162,22 @@ __global__ void __launch_bounds__(128) finalize_kernel(
     sacc[k * T + t] += diag[i] - zi;
   }
   __syncthreads();
-  for (int w = T / 2; w > 0; w >>= 1) {
+  // fixed tree over the T threads: levels w >= 32 in shared memory, the last five levels as warp
+  // shuffles (lane t adds lane t + w: the same pairs, so the same bits as the all-smem tree)
+  for (int w = T / 2; w >= 32; w >>= 1) {
     if (t < w)
       for (int c = 0; c <= k; ++c) sacc[c * T + t] += sacc[c * T + t + w];
     __syncthreads();
   }
-  for (int c = t; c <= k; c += T) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sacc[c * T];
+  {
+    const int lane = t & 31, nw = T >> 5;
+    for (int c = t >> 5; c <= k; c += nw) {
+      double v = sacc[c * T + lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) blockpart[(int64_t)blockIdx.x * (k + 1) + c] = v;
+    }
+  }
   if (!fin.counter) return;
   __threadfence();
   __syncthreads();
