@@ -367,11 +367,18 @@ __global__ void __launch_bounds__(FUSED_THREADS) fused_update_kernel(
     sacc[k * T + t] += diag[i] - zi;
   }
   __syncthreads();
-  for (int w = T / 2; w > 0; w >>= 1) {
+  for (int w = T / 2; w >= 32; w >>= 1) {  // the same fixed tree as finalize (last five levels shuffled)
     if (t < w)
       for (int c = 0; c <= k; ++c) sacc[c * T + t] += sacc[c * T + t + w];
     __syncthreads();
   }
+  for (int c = t >> 5; c <= k; c += T >> 5) {
+    double v = sacc[c * T + (t & 31)];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((t & 31) == 0) sacc[c * T] = v;
+  }
+  __syncthreads();
   if (t < k) {
     const int32_t sz = sizes[t];
     const double v = sz > 0 ? sacc[t * T] / (double)sz : __longlong_as_double(0x7ff0000000000000LL);
