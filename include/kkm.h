@@ -100,8 +100,9 @@ extern "C" {
 #define KKM_PH_SPMM 2       /* a2 per fit (sum over iterations)                 */
 #define KKM_PH_CNORM 3      /* a3 incl. its collective                          */
 #define KKM_PH_ASSIGN 4     /* a4 incl. the labels allgather                    */
-#define KKM_PH_A2_KERNEL 5  /* the dominant a2 kernel alone (spmm_sym / spmm_onehot /
-                               the streaming kernel), summed over the loop's launches */
+#define KKM_PH_A2_KERNEL 5  /* the dominant a2 kernel alone (spmm_tc over the 16-bit bands /
+                               spmm_sym / spmm_onehot / spmm_group / the streaming kernels),
+                               summed over the loop's launches */
 #define KKM_NPHASES 6
 
 typedef struct kkm_params {
@@ -109,7 +110,7 @@ typedef struct kkm_params {
   double gamma;            /* poly: > 0; Gaussian: >= 0; ignored for linear        */
   double coef0;            /* poly offset c of Eq. (k)                             */
   int32_t degree;          /* poly degree >= 1                                    */
-  int32_t k;               /* clusters, 1 <= k <= n                               */
+  int32_t k;               /* clusters, 1 <= k <= min(n, 900) (KKM_EUNSUP above 900)  */
   int32_t max_iter;        /* iterations per kkm_fit call, >= 0 (100)      */
   int32_t stop_on_no_change; /* 1: stop early when no label changes (A4)          */
   int32_t path;            /* KKM_PATH_*                                           */
@@ -140,7 +141,7 @@ typedef struct kkm_params {
                               lo = RN(K 2^e - hi), with 2^e the largest power of two such that
                               a bound on |K| times 2^e is <= 60000 (linear: max ||x||^2; poly:
                               (gamma max ||x||^2 + |coef0|)^degree; Gaussian: 1): 4 bytes per
-                              value like fp32, relative error <= ~2^-22 (fp32-class), and a2 on
+                              value like fp32, relative error <= 2^-21 + 2^-24 (fp32-class), and a2 on
                               the tensor cores (spmm_tc.cuh) with S summed in int64 fixed point.
                               KKM_KSTORE_FP16 (2): the hi plane only -- half the bytes, each
                               value rounded to 2^-11 relative (DESIGN A27 bounds E / D / J).
@@ -192,8 +193,9 @@ int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, 
  *             owned by the caller, must outlive the handle.
  *   cuda_stream: cudaStream_t (NULL = legacy default stream).
  *   nccl_comm:   ncclComm_t of nranks ranks (NULL iff nranks == 1). Borrowed.
- * Computes norms, the bf16 hi/lo split, diag K(i,i) and, when materialising,
- * K[rows, :] with the a1 GEMM + kappa epilogue. Collective. */
+ * Computes norms, the 16-bit hi/lo split of X (fp16 with a per-row power-of-two scale for
+ * FP16X3, the default; bf16 for BF16X3), diag K(i,i) and, when materialising, K[rows, :] with
+ * the a1 GEMM + kappa epilogue. Collective. */
 int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t n, int64_t d,
              int64_t ldx, int32_t rank, int32_t nranks, const int32_t *init_labels,
              void *workspace, size_t ws_bytes, void *cuda_stream, void *nccl_comm);

@@ -47,6 +47,7 @@ def lib():
             "orc_E_rows": [P, i64, i64, P, i32, P],
             "orc_cnorm": [P, P, i64, i32, P],
             "orc_objective": [P, P, i64, i32, P, P],
+            "orc_objective_X": [P, i64, i64, i64, P, i32, ctypes.c_int, f64, f64, ctypes.c_int, P],
             "orc_assign": [P, P, P, i64, i32, P, P],
             "orc_fit": [P, P, i64, i32, i32, i32, P, P, P, P, P],
             "orc_predict": [P, i64, P, i64, i64, P, i32, P, ctypes.c_int, f64, f64, ctypes.c_int, P, P],
@@ -151,6 +152,17 @@ def objective(diag, labels, k, cn) -> float:
     cn = np.ascontiguousarray(cn, dtype=np.float64)
     J = np.zeros(1, dtype=np.float64)
     _check(lib().orc_objective(_p(diag), _p(labels), labels.size, k, _p(cn), _p(J)), "objective")
+    return float(J[0])
+
+
+def objective_X(X, labels, k, kind, gamma=1.0, coef0=0.0, degree=1) -> float:
+    """J of the labelling straight from the points (reading A8: tr K minus the within-cluster
+    double sums over |L_c|), without storing K: for the full-size configs."""
+    X = _X(X)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    J = np.zeros(1, dtype=np.float64)
+    _check(lib().orc_objective_X(_p(X), X.shape[0], X.shape[1], X.shape[1], _p(labels), k, kind,
+                                 gamma, coef0, degree, _p(J)), "objective_X")
     return float(J[0])
 
 

@@ -201,6 +201,70 @@ int orc_objective(const double *diag, const int32_t *labels, int64_t n, int32_t 
   return rc;
 }
 
+/* J of a given labelling straight from the points, for sizes where K cannot be stored (the
+ * BASELINE configs 2-3 at full size). Reading A8 with the centroid of Eq. (c) (P:144-158,
+ * mu_c = (1/|L_c|) sum_{j in L_c} phi(x_j)):
+ *   J = sum_i ||phi(x_i) - mu_cl(i)||^2 = tr K - sum_{c: |L_c| > 0} (1/|L_c|) sum_{i in L_c} sum_{j in L_c} K(i,j)
+ * (expanding the square; the mean of Eq. z/c is this double sum over |L_c|^2). kappa is the
+ * definition (orc_kappa) and is symmetric exactly (same operations in the same order for (i,j) and
+ * (j,i)), so each cluster's double sum is taken as sum_i K(i,i) + 2 sum_{i<j} K(i,j):
+ *   W(i) = sum_{j in L_cl(i), j > i} K(i,j)   (ascending j; parallel over i only),
+ *   T_c  = sum_{i in L_c} K(i,i) + 2 sum_{i in L_c} W(i)   (ascending i).
+ * Every sum runs in a fixed order: the result is independent of the thread count.
+ * labels: n int32 in [0,k). Out: *J. Cost sum_c |L_c|^2 / 2 kernel evaluations. */
+int orc_objective_X(const float *X, int64_t n, int64_t d, int64_t ldx, const int32_t *labels, int32_t k,
+                    int kind, double gamma, double coef0, int degree, double *J) {
+  if (n < 1 || d < 1 || ldx < d || k < 1 || check_kernel(kind, gamma, degree)) return ORC_EINVAL;
+  int64_t *sizes = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+  int64_t *start = (int64_t *)malloc(sizeof(int64_t) * (size_t)(k + 1));
+  int64_t *members = (int64_t *)malloc(sizeof(int64_t) * (size_t)n); /* points of each cluster, ascending */
+  int64_t *rank = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);    /* position of i in its cluster */
+  double *W = (double *)malloc(sizeof(double) * (size_t)n);
+  double *Kii = (double *)malloc(sizeof(double) * (size_t)n);
+  int rc = (!sizes || !start || !members || !rank || !W || !Kii) ? ORC_ENOMEM : ORC_OK;
+  if (rc == ORC_OK) rc = orc_sizes(labels, n, k, sizes);
+  if (rc == ORC_OK) {
+    start[0] = 0;
+    for (int32_t c = 0; c < k; ++c) start[c + 1] = start[c] + sizes[c];
+    for (int32_t c = 0; c < k; ++c) sizes[c] = 0; /* reused as fill counters */
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t c = labels[i];
+      rank[i] = sizes[c];
+      members[start[c] + sizes[c]++] = i;
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t c = labels[i];
+      const float *xi = X + i * ldx;
+      Kii[i] = orc_kappa(xi, xi, d, kind, gamma, coef0, degree);
+      double w = 0.0;
+      for (int64_t p = start[c] + rank[i] + 1; p < start[c + 1]; ++p)
+        w += orc_kappa(xi, X + members[p] * ldx, d, kind, gamma, coef0, degree);
+      W[i] = w;
+    }
+    double tr = 0.0, within = 0.0;
+    for (int64_t i = 0; i < n; ++i) tr += Kii[i];
+    for (int32_t c = 0; c < k; ++c) {
+      const int64_t sz = start[c + 1] - start[c];
+      if (sz == 0) continue; /* empty clusters are excluded (reading A7) */
+      double diag_sum = 0.0, off = 0.0;
+      for (int64_t p = start[c]; p < start[c + 1]; ++p) {
+        diag_sum += Kii[members[p]];
+        off += W[members[p]];
+      }
+      within += (diag_sum + 2.0 * off) / (double)sz;
+    }
+    *J = tr - within;
+  }
+  free(sizes);
+  free(start);
+  free(members);
+  free(rank);
+  free(W);
+  free(Kii);
+  return rc;
+}
+
 /* D = -2E + C~, Eq. (d) P:160-167 (C~'s rows all equal c, Eq. ct), plus the
  * omitted K(i,i) (reading A3) for Dfull; row-wise argmin with the lowest index
  * winning ties (reading A6), computed on the shifted D. Empty clusters

@@ -5,7 +5,31 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace kkm {
+
+constexpr int KKM_MAX_K = 900;  // finalize keeps (k + 1) x 32 doubles per block in smem (<= 227 KB)
+
+// Opts kernel `fn` in to `bytes` of dynamic shared memory on the CURRENT device. The attribute
+// belongs to a (function, device) pair, so the cache is keyed by both (a second handle on another
+// device sets it again) and guarded by a mutex (handles may live on different host threads).
+inline cudaError_t ensure_smem_attr(const void *fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(fn, dev);
+  const auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
 
 // Kernel-function parameters as the device sees them (fp32 epilogue math).
 struct KappaParams {

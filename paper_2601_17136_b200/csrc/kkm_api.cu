@@ -27,6 +27,7 @@
 #include "spmm_tc.cuh"
 #include "sym.cuh"
 #include "tc2.cuh"
+#include "ssym.cuh"
 #include "update.cuh"
 
 using namespace kkm;
@@ -103,6 +104,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (nranks < 1 || rank < 0 || rank >= nranks)
     return fail(KKM_EINVAL, "rank %d / nranks %d out of range", rank, nranks);
   if (p->k < 1 || p->k > n) return fail(KKM_EINVAL, "k=%d must satisfy 1 <= k <= n=%lld", p->k, (long long)n);
+  if (p->k > KKM_MAX_K) return fail(KKM_EUNSUP, "k=%d > %d clusters is not supported", p->k, KKM_MAX_K);
   if (p->max_iter < 0) return fail(KKM_EINVAL, "max_iter=%d < 0", p->max_iter);
   if (p->kind < 0 || p->kind > 2) return fail(KKM_EINVAL, "unknown kernel kind %d", p->kind);
   if (p->kind == KKM_KERNEL_POLY && (p->degree < 1 || !(p->gamma > 0.0)))
@@ -539,7 +541,9 @@ struct kkm_ctx {
   std::vector<void *> xpeers;  // opened peer mappings (closed in destroy)
   const uint8_t **xtable = nullptr;  // device [nranks] bases (inside xbuf)
   size_t xflag_off = 0;              // byte offset of the epoch flag in every exchange buffer
+                                     // (+64: this rank's timed-out word, checked by check_p2p)
   unsigned long long epoch = 0;
+  unsigned long long p2p_timeout_ns = 0;
   // f4 fp16 K storage
   CUtensorMap *tmaps = nullptr;
   TsBand *tbands = nullptr;
@@ -624,12 +628,7 @@ int copy_any(kkm_ctx *h, void *dst, const void *src, size_t bytes) {
 template <int KP>
 int launch_spmm_kp(kkm_ctx *h, const int32_t *labels, int c0) {
   const Plan &P = h->P;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(spmm_onehot_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)spmm_smem_bytes<KP>()));
-    attr_set = true;
-  }
+  CK(ensure_smem_attr((const void *)spmm_onehot_kernel<KP>, spmm_smem_bytes<KP>()));
   const int64_t items = ceil_div(P.nA, SpRows<KP>::R) * P.nsplit;
   const int grid = (int)std::min<int64_t>(items, h->num_sms);
   spmm_onehot_kernel<KP><<<grid, SpRows<KP>::THREADS, spmm_smem_bytes<KP>(), h->st>>>(
@@ -728,12 +727,7 @@ int launch_spmm_mat_body(kkm_ctx *h, const int32_t *labels) {
     const int64_t ngroups = P.ldk / 32;
     group_code_kernel<<<(unsigned)ceil_div(ngroups, 8), 256, 0, h->st>>>(labels + P.b0, P.nB, P.ldk, h->codes);
     CKL();
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(spmm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sg_smem_bytes(SG_MAX_K)));
-      attr = true;
-    }
+    CK(ensure_smem_attr((const void *)spmm_group_kernel, sg_smem_bytes(SG_MAX_K)));
     const int64_t items = ceil_div(P.nA, SG_ROWS) * P.nsplit;
     const int grid = (int)std::min<int64_t>(items, h->num_sms);
     spmm_group_kernel<<<grid, SG_THREADS, sg_smem_bytes(P.k), h->st>>>(h->K, P.ldk, P.nA, h->codes, P.k, P.nsplit,
@@ -766,12 +760,7 @@ int launch_spmm_mat_body(kkm_ctx *h, const int32_t *labels) {
 template <int KP>
 int launch_spmm_sym_kp(kkm_ctx *h, const int32_t *labels) {
   const Plan &P = h->P;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(spmm_sym_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)spmm_sym_smem_bytes()));
-    attr_set = true;
-  }
+  CK(ensure_smem_attr((const void *)spmm_sym_kernel<KP>, spmm_sym_smem_bytes()));
   if (P.sym_items == 0) {
     a2_mark(h);
     a2_mark(h);
@@ -793,11 +782,7 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   const Plan &P = h->P;
   const int k = P.k;
   if (P.kh) {  // f4: 16-bit bands, a2 on the tensor cores (spmm_tc.cuh), S in int64 fixed point
-    static bool attr_set = false;
-    if (!attr_set) {
-      CK(cudaFuncSetAttribute(spmm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM));
-      attr_set = true;
-    }
+    CK(ensure_smem_attr((const void *)spmm_tc_kernel, TS_SMEM));
     long long *Sx = h->tSfix;
     if (h->p2p) {  // this epoch's half of the own exchange buffer (the other half may still be read)
       ++h->epoch;
@@ -953,11 +938,11 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
   const int k1 = P.k + 1;
   const int nr = P.repl ? 1 : P.nranks, r = P.repl ? 0 : P.rank;  // replicated a3: one "rank"
   if (P.a3fix && P.a_n > 0) {  // int64 S in, c and J from the last block (same sums as below)
-    int fth = FIN_THREADS;
-    while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
+    const int fth = fin_threads(P.k);
     const A3Peers peers = h->p2p ? A3Peers{h->xtable, P.nranks, (int64_t)((h->epoch & 1) * (size_t)P.npad * P.k * 8),
-                                           (int64_t)(2 * (size_t)P.npad * P.k * 8), h->epoch}
-                                 : A3Peers{nullptr, 0, 0, 0, 0ull};
+                                           (int64_t)h->xflag_off, h->epoch, h->p2p_timeout_ns,
+                                           (int *)(h->xbuf + h->xflag_off + 64)}
+                                 : A3Peers{nullptr, 0, 0, 0, 0ull, 0ull, nullptr};
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
         nullptr, 1, P.a_n, P.npad, P.k, sizes, labels + P.a_row0, h->diag, P.rows_per_block, E_out, h->blockpart,
         h->tSfix, h->tfx_inv, A3Fused{h->a3ctr, sizes, cnorm_out, J_out, sizes_next, changed_out}, peers);
@@ -965,8 +950,7 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
     return KKM_OK;
   }
   if (P.a_n > 0) {
-    int fth = FIN_THREADS;  // power of two with (k+1) * fth doubles <= 48 KB
-    while (fth > 32 && (size_t)k1 * fth * 8 > 48 * 1024) fth >>= 1;
+    const int fth = fin_threads(P.k);
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
         S, nsplit, P.a_n, rows_pad, P.k, sizes, labels + P.a_row0, h->diag, P.rows_per_block,
         E_out, h->blockpart);
@@ -1099,11 +1083,40 @@ int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, 
 
 const char *kkm_last_error(void) { return g_err; }
 
+// *v = the minimum of *v over all ranks (a collective on the handle's communicator).
+static int agree_min(kkm_ctx *h, int *v) {
+  int *d = nullptr;
+  if (cudaMallocAsync((void **)&d, 4, h->st) != cudaSuccess) return fail(KKM_ECUDA, "cudaMallocAsync failed");
+  int rc = [&]() -> int {
+    CK(cudaMemcpyAsync(d, v, 4, cudaMemcpyHostToDevice, h->st));
+    CKN(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, h->comm, h->st));
+    CK(cudaMemcpyAsync(v, d, 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return KKM_OK;
+  }();
+  cudaFreeAsync(d, h->st);
+  return rc;
+}
+
+// After a synchronised a3 on the peer path: a finalize that gave up waiting for a peer poisons the
+// handle (KKM_ENCCL: the exchange failed) instead of trapping the context.
+static int check_p2p(kkm_ctx *h) {
+  if (!h->p2p) return KKM_OK;
+  int to = 0;
+  CK(cudaMemcpy(&to, h->xbuf + h->xflag_off + 64, 4, cudaMemcpyDeviceToHost));
+  if (to) {
+    h->poisoned = true;
+    return fail(KKM_ENCCL, "peer-memory S exchange: a peer's flag did not arrive within %.0f s",
+                (double)h->p2p_timeout_ns * 1e-9);
+  }
+  return KKM_OK;
+}
+
 // Peer-memory exchange of S for the replicated a3 (16-bit bands, several ranks, §6): an own
 // cudaMalloc'd buffer [2 epochs of k x npad int64 | epoch flag | peer table], its IPC handle
 // allgathered over NCCL and the peers' buffers opened here. All ranks must agree: the outcome is
 // allreduced (min) and any failure leaves every rank on the NCCL allreduce path. Collective.
-int setup_p2p(kkm_ctx *h) {
+static int setup_p2p(kkm_ctx *h) {
   const Plan &P = h->P;
   const size_t sbytes = (size_t)P.npad * P.k * 8;
   const size_t xbytes = 2 * sbytes + 256 + (size_t)P.nranks * 8;
@@ -1280,14 +1293,8 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   h->kp.neg_gamma_log2e = (float)(-p->gamma * 1.4426950408889634);
 
   int rc = [&]() -> int {
-    if (P.fused) {
-      static bool attr = false;
-      if (!attr) {
-        CK(cudaFuncSetAttribute(fused_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(17 * FUSED_THREADS * 8 + 16 * 8)));
-        attr = true;
-      }
-    }
+    if (P.fused) CK(ensure_smem_attr((const void *)fused_update_kernel, 17 * FUSED_THREADS * 8 + 16 * 8));
+    if (fin_smem_bytes(P.k) > 48 * 1024) CK(ensure_smem_attr((const void *)finalize_kernel, fin_smem_bytes(P.k)));
     EventList evs;  // init phases: prep, GEMM
     if (!evs.record(h->st)) return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
     // ---- X (Alg. 1 line 1: allgather P) into Xf [npad x ldf], zero padded
@@ -1470,13 +1477,21 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     }
   }
   // (p2p needs the a3 that reads the int64 S itself: a3fix; the single-CTA fused path reads fp64 S)
-  // Every rank reads all (P - 1) peers' whole S, so the peer bytes grow with P while NCCL's (NVLS)
-  // allreduce does not: peer exchange up to 4 ranks (measured faster there), NCCL above
-  // (KKM_P2P_MAX_RANKS overrides; the same value on every rank, so all ranks take the same path).
-  int p2p_max = 4;
-  if (const char *e = std::getenv("KKM_P2P_MAX_RANKS")) p2p_max = std::atoi(e);
-  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1 && P.nranks <= p2p_max && !std::getenv("KKM_NO_P2P"))
-    rc = setup_p2p(h);
+  // Opt-in (KKM_P2P=1): measured only 2 % faster than the NCCL allreduce at 4 GPUs, and
+  // every rank reads all (P - 1) peers' whole S, so it is limited to P <= KKM_P2P_MAX_RANKS (4).
+  // The decision is agreed by all ranks (an allreduce of the local wish) before the collective
+  // setup, so ranks with different environments cannot issue mismatched collectives.
+  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1) {
+    int p2p_max = 4;
+    if (const char *e = std::getenv("KKM_P2P_MAX_RANKS")) p2p_max = std::atoi(e);
+    const char *want_env = std::getenv("KKM_P2P");
+    int want = (want_env && std::atoi(want_env) == 1 && P.nranks <= p2p_max) ? 1 : 0;
+    double tmo = 600.0;  // seconds a finalize waits for a peer's flag before it reports a timeout
+    if (const char *e = std::getenv("KKM_P2P_TIMEOUT_S")) tmo = std::max(1.0, std::atof(e));
+    h->p2p_timeout_ns = (unsigned long long)(tmo * 1e9);
+    rc = agree_min(h, &want);
+    if (rc == KKM_OK && want) rc = setup_p2p(h);
+  }
   if (rc) {
     delete h;
     return rc;
@@ -1574,6 +1589,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   CK(cudaMemcpyAsync(J.data(), h->J, (size_t)(t + 1) * 8, cudaMemcpyDeviceToHost, h->st));
   if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  CKR(check_p2p(h));
   if (timing) {
     const std::vector<cudaEvent_t> &e5 = ev.v;
     for (size_t i = 0; i + 4 < e5.size(); i += 5) {  // the a2 phase includes the f3 S update
@@ -1621,6 +1637,7 @@ int kkm_objective(kkm_handle h, double *J) {
   h->cnorm2_valid = true;
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  CKR(check_p2p(h));
   return KKM_OK;
 }
 
@@ -1940,14 +1957,17 @@ int kkm_destroy(kkm_handle h) {
     const unsigned long long done = ~0ull;
     cudaMemcpy(h->xbuf + h->xflag_off, &done, 8, cudaMemcpyHostToDevice);
     const auto t0 = std::chrono::steady_clock::now();
+    bool all_done = true;
     for (void *q : h->xpeers) {
       unsigned long long v = 0;
       while (cudaMemcpy(&v, (uint8_t *)q + h->xflag_off, 8, cudaMemcpyDeviceToHost) == cudaSuccess && v != done &&
              std::chrono::steady_clock::now() - t0 < std::chrono::seconds(20))
         std::this_thread::sleep_for(std::chrono::microseconds(200));
+      all_done = all_done && v == done;
     }
     for (void *q : h->xpeers) cudaIpcCloseMemHandle(q);
-    cudaFree(h->xbuf);
+    // a peer that never reported DONE may still read this buffer: keep it (leak) rather than free
+    if (all_done) cudaFree(h->xbuf);
     cudaGetLastError();
   }
   if (h->colcomm) ncclCommDestroy(h->colcomm);

@@ -94,14 +94,14 @@ __device__ __forceinline__ T2Smem t2_carve(uint8_t *smem_raw, uint32_t extra, ui
   return s;
 }
 
-__device__ __forceinline__ void t2_setup(const T2Smem &s, int warp) {
+__device__ __forceinline__ void t2_setup(const T2Smem &s, int warp, uint32_t tempty_count = 2 * TC_EPI_WARPS) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < T2_STAGES; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
     }
     mbar_init(s.tfull, 1);
-    mbar_init(s.tempty, 2 * TC_EPI_WARPS);
+    mbar_init(s.tempty, tempty_count);  // every epilogue warp of both CTAs arrives
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -389,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     const float *__restrict__ norms, const float *__restrict__ rscale, KappaParams kp, Sched sc,
                     float oscale, int planes) {
   // oscale == 0: fp32 output; > 0: fp16 output of K' = K * oscale (f4 K storage): planes == 1
-  // hi = RN(K') only, planes == 2 also lo = RN(K' - hi) through tm_out2 (hi + lo = K' to ~2^-22)
+  // hi = RN(K') only, planes == 2 also lo = RN(K' - hi) through tm_out2 (hi + lo = K' to 2^-21 + 2^-24 relative)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *extra;
   const T2Smem s = t2_carve(smem_raw, (uint32_t)T2_GEMM_EXTRA, &extra);
@@ -855,14 +855,9 @@ inline int tc2_gemm_launch(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, 
   }
   if (tc_make_out_map(g, out, m, ncov, ldo, oscale > 0.f)) return 1;
   if (!out_lo) g.map_out2 = g.map_out;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc2_gemm_kernel<T2GemmSched>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)T2_GEMM_SMEM) != cudaSuccess) {
-      tc_err_slot() = "cudaFuncSetAttribute(tc2_gemm_kernel) failed";
-      return 1;
-    }
-    attr = true;
+  if (ensure_smem_attr((const void *)tc2_gemm_kernel<T2GemmSched>, T2_GEMM_SMEM) != cudaSuccess) {
+    tc_err_slot() = "cudaFuncSetAttribute(tc2_gemm_kernel) failed";
+    return 1;
   }
   if (!g.num_sms) {
     int dev = 0;
@@ -900,14 +895,9 @@ inline int tc2_gemm_launch_multi(TcGemm &g, const uint16_t *Xhi, const uint16_t 
   if (nitems <= 0) return 0;
   if (g.hi != Xhi || g.lo != Xlo || g.fp16 != fp16)
     if (tc_make_maps(g, Xhi, Xlo, fp16, rows, dp)) return 1;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc2_gemm_kernel<T2MultiSched>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)T2_GEMM_SMEM) != cudaSuccess) {
-      tc_err_slot() = "cudaFuncSetAttribute(tc2_gemm_kernel multi) failed";
-      return 1;
-    }
-    attr = true;
+  if (ensure_smem_attr((const void *)tc2_gemm_kernel<T2MultiSched>, T2_GEMM_SMEM) != cudaSuccess) {
+    tc_err_slot() = "cudaFuncSetAttribute(tc2_gemm_kernel multi) failed";
+    return 1;
   }
   if (!g.num_sms) {
     int dev = 0;
@@ -932,18 +922,14 @@ inline int tc2_gemm_launch_multi(TcGemm &g, const uint16_t *Xhi, const uint16_t 
 }
 
 template <int KMAX>
-inline int t2s_launch_k(bool &attr, unsigned grid, cudaStream_t st, const TcStream &g, uint32_t idesc, int nkb,
+inline int t2s_launch_k(unsigned grid, cudaStream_t st, const TcStream &g, uint32_t idesc, int nkb,
                         int64_t n, int64_t b0, int64_t nloc, int64_t rows_pad, const float *norms,
                         const float *rscale, const float *snorms, const float *srscale, const int32_t *pos,
                         int64_t npos, const int32_t *seg, int k, const KappaParams &kp, const T2StreamSched &sc,
                         double *Spart, int kstride, int c0) {
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc2_stream_kernel<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)T2_STREAM_SMEM) != cudaSuccess) {
-      tc_err_slot() = "cudaFuncSetAttribute(tc2_stream_kernel) failed";
-      return 1;
-    }
-    attr = true;
+  if (ensure_smem_attr((const void *)tc2_stream_kernel<KMAX>, T2_STREAM_SMEM) != cudaSuccess) {
+    tc_err_slot() = "cudaFuncSetAttribute(tc2_stream_kernel) failed";
+    return 1;
   }
   tc2_stream_kernel<KMAX><<<grid, T2_THREADS, T2_STREAM_SMEM, st>>>(g.a_hi, g.a_lo, g.b_hi, g.b_lo, idesc, nkb, n,
                                                                     b0, nloc, rows_pad, norms, rscale, snorms,
@@ -999,7 +985,6 @@ inline int tc2_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
   const unsigned grid = (unsigned)(2 * clusters);
   const uint32_t idesc = t2_idesc(fp16);
   const int nkb = (int)(dp / TC_BK);
-  static bool a4 = false, a8 = false, a16 = false;
   const float *rs = fp16 ? rscale : nullptr;
   int rc;
   if (k > 16) {
@@ -1007,13 +992,13 @@ inline int tc2_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
     return 1;
   }
   if (k <= 4)
-    rc = t2s_launch_k<4>(a4, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, npos,
+    rc = t2s_launch_k<4>(grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, npos,
                          seg, k, kp, sc, Spart, kstride, c0);
   else if (k <= 8)
-    rc = t2s_launch_k<8>(a8, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, npos,
+    rc = t2s_launch_k<8>(grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos, npos,
                          seg, k, kp, sc, Spart, kstride, c0);
   else
-    rc = t2s_launch_k<16>(a16, grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos,
+    rc = t2s_launch_k<16>(grid, st, g, idesc, nkb, n, b0, nloc, rows_pad, norms, rs, snorms, srscale, pos,
                           npos, seg, k, kp, sc, Spart, kstride, c0);
   if (rc) return rc;
   if (launches) ++*launches;
@@ -1028,16 +1013,12 @@ inline int tc2_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
 // f1 streaming launcher: A = B = the sorted operand (Shi/Slo, rows rows). units: device array
 // of nunits int4 (tm, tn0, ntn, 0). Sfix (n x k int64) must be zeroed by the caller.
 template <int KMAX>
-inline int t2sym_launch_k(bool &attr, unsigned grid, cudaStream_t st, const TcStream &g, uint32_t idesc, int nkb,
+inline int t2sym_launch_k(unsigned grid, cudaStream_t st, const TcStream &g, uint32_t idesc, int nkb,
                           int64_t n, const float *snorms, const float *rs, const int32_t *seg, int k,
                           const KappaParams &kp, const T2SymSched &sc, double fx_scale, long long *Sfix) {
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc2_stream_sym_kernel<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)T2_STREAM_SMEM) != cudaSuccess) {
-      tc_err_slot() = "cudaFuncSetAttribute(tc2_stream_sym_kernel) failed";
-      return 1;
-    }
-    attr = true;
+  if (ensure_smem_attr((const void *)tc2_stream_sym_kernel<KMAX>, T2_STREAM_SMEM) != cudaSuccess) {
+    tc_err_slot() = "cudaFuncSetAttribute(tc2_stream_sym_kernel) failed";
+    return 1;
   }
   tc2_stream_sym_kernel<KMAX><<<grid, T2_THREADS, T2_STREAM_SMEM, st>>>(g.a_hi, g.a_lo, idesc, nkb, n, snorms, rs,
                                                                         seg, k, kp, sc, fx_scale, Sfix);
@@ -1081,13 +1062,12 @@ inline int tc2_stream_sym_launch(TcStream &g, const uint16_t *Shi, const uint16_
   const uint32_t idesc = t2_idesc(fp16);
   const int nkb = (int)(dp / TC_BK);
   const float *rs = fp16 ? srscale : nullptr;
-  static bool a4 = false, a8 = false, a12 = false, a16 = false;
   int rc;
-  if (k <= 4) rc = t2sym_launch_k<4>(a4, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
-  else if (k <= 8) rc = t2sym_launch_k<8>(a8, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  if (k <= 4) rc = t2sym_launch_k<4>(grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  else if (k <= 8) rc = t2sym_launch_k<8>(grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
   else if (k <= 12)
-    rc = t2sym_launch_k<12>(a12, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
-  else rc = t2sym_launch_k<16>(a16, grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+    rc = t2sym_launch_k<12>(grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
+  else rc = t2sym_launch_k<16>(grid, st, g, idesc, nkb, n, snorms, rs, seg, k, kp, sc, fx_scale, Sfix);
   if (rc) return rc;
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();

@@ -15,6 +15,15 @@ namespace kkm {
 
 constexpr int FIN_THREADS = 128;
 
+// finalize's block size: the largest power of two <= FIN_THREADS with (k + 1) * threads doubles in
+// the default 48 KB; from k = 192 on 32 threads and more than 48 KB (opted in by kkm_init).
+inline int fin_threads(int k) {
+  int fth = FIN_THREADS;
+  while (fth > 32 && (size_t)(k + 1) * fth * 8 > 48 * 1024) fth >>= 1;
+  return fth;
+}
+inline size_t fin_smem_bytes(int k) { return (size_t)(k + 1) * fin_threads(k) * 8; }
+
 // grid: nblocks; block b handles rows [b * rows_per_block, ...). blockDim.x: a power of two
 // <= FIN_THREADS; dynamic smem: (k + 1) * blockDim.x doubles.
 // Sfix (optional): read S as int64 fixed point, Sfix[c * rows_pad + i] * inv (the 16-bit band
@@ -38,7 +47,15 @@ struct A3Peers {
   int64_t s_off;                // byte offset of this epoch's S in a buffer
   int64_t flag_off;             // byte offset of the epoch flag in a buffer
   unsigned long long epoch;
+  unsigned long long timeout_ns;  // bound on the wait for a peer's flag (globaltimer)
+  int *timed_out;                 // set to 1 when a wait ran out (the host checks it and poisons)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
   unsigned long long v;
@@ -89,18 +106,21 @@ __global__ void __launch_bounds__(128) finalize_kernel(
     const double *__restrict__ diag, int64_t rows_per_block, double *__restrict__ E,
     double *__restrict__ blockpart, const long long *__restrict__ Sfix = nullptr, double inv = 1.0,
     A3Fused fin = A3Fused{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr},
-    A3Peers peers = A3Peers{nullptr, 0, 0, 0, 0ull}) {
+    A3Peers peers = A3Peers{nullptr, 0, 0, 0, 0ull, 0ull, nullptr}) {
   extern __shared__ double sacc[];  // [(k + 1)][blockDim.x]
   __shared__ unsigned s_last;
   const int T = blockDim.x;
   const int t = threadIdx.x;
-  if (peers.bases) {  // wait for every rank's S of this epoch (bounded: a lost peer traps, no hang)
-    if (t < peers.nranks) {
+  if (peers.bases) {  // wait for every rank's S of this epoch; bounded: a lost peer raises timed_out
+    if (t < peers.nranks) {  // (the kernel then finishes on whatever S it reads; the host poisons the handle)
       const unsigned long long *flag =
           reinterpret_cast<const unsigned long long *>(peers.bases[t] + peers.flag_off);
-      const long long t0 = clock64();
+      const unsigned long long t0 = globaltimer_ns();
       while (ld_acquire_sys(flag) < peers.epoch)
-        if (clock64() - t0 > 40000000000ll) asm volatile("trap;");
+        if (globaltimer_ns() - t0 > peers.timeout_ns) {
+          atomicExch(peers.timed_out, 1);
+          break;
+        }
     }
     __syncthreads();
   }

@@ -412,3 +412,64 @@ def test_quality_rings_and_blobs_recovered():
     _, lb = oracle.kmeanspp(Xb, 5, np.random.default_rng(1).random(5), oracle.LINEAR)
     fb = oracle.fit(Xb, 5, oracle.LINEAR, max_iter=30, init_labels=lb)
     assert adjusted_rand_score(tb, fb["labels"]) == 1.0
+
+
+# ---------------------------------------------------------------- objective_X (J from the points)
+@pytest.mark.parametrize("kind,args", [(oracle.LINEAR, ()), (oracle.POLY, (1.0, 1.0, 2)),
+                                       (oracle.POLY, (0.7, 0.4, 3))])
+def test_objective_X_bruteforce_feature_space(kind, args):
+    """A8 by brute force: J(cl) = sum_i ||phi(x_i) - mu_cl(i)||^2 with explicit features (linear:
+    x itself; poly deg 2: the explicit map), for all 2^9 labelings of 9 points; poly deg 3 against
+    the K V^T path (orc_objective) instead (no explicit map here)."""
+    X = synth.blobs(9, 2, 2, seed=23, sep=1.5)
+    K = oracle.kernel_matrix(X, kind, *args)
+    diag = np.diag(K).copy()
+    F = None
+    if kind == oracle.LINEAR:
+        F = X.astype(np.float64)
+    elif args[2] == 2:
+        F = feature_map_poly2(X, args[0], args[1])
+    for bits in itertools.product([0, 1], repeat=9):
+        lab = np.array(bits, dtype=np.int32)
+        J = oracle.objective_X(X, lab, 2, kind, *args)
+        if F is not None:
+            Jb = sum(((F[lab == c] - F[lab == c].mean(axis=0)) ** 2).sum() for c in (0, 1) if (lab == c).any())
+        else:
+            Jb = oracle.objective(diag, lab, 2, oracle.cnorm(oracle.E_rows(K, lab, 2), lab, 2))
+        assert abs(J - Jb) <= 1e-10 * max(1.0, abs(Jb)), (bits, J, Jb)
+
+
+@pytest.mark.parametrize("name,n,k", [("mnist60k", 500, 10), ("har200k", 400, 6), ("rings", 300, 2)])
+def test_objective_X_equals_iteration_J(name, n, k):
+    """The same J as the iteration's E / c path (Eqs. e, z, c + A8) on the configs' recipes, for
+    round-robin, random and empty-cluster labelings; Gaussian gamma = 0 gives J = 0 (K = 1)."""
+    X, cfg = synth.make_config(name, n=n)
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    K = oracle.kernel_matrix(X, *args)
+    diag = np.diag(K).copy()
+    rng = np.random.default_rng(5)
+    labs = [oracle.round_robin(n, k), rng.integers(0, k, n).astype(np.int32)]
+    e = rng.integers(0, k, n).astype(np.int32)
+    e[e == 1] = 0  # cluster 1 empty
+    labs.append(e)
+    for lab in labs:
+        Jd = oracle.objective(diag, lab, k, oracle.cnorm(oracle.E_rows(K, lab, k), lab, k))
+        J = oracle.objective_X(X, lab, k, *args)
+        assert abs(J - Jd) <= 1e-11 * float(np.abs(diag).sum()), (J, Jd)
+    if cfg["kind"] == oracle.GAUSSIAN:
+        assert oracle.objective_X(X, labs[1], k, oracle.GAUSSIAN, 0.0) == 0.0
+
+
+def test_objective_X_thread_independence(monkeypatch):
+    X = synth.blobs(700, 5, 4, seed=9)
+    lab = np.random.default_rng(1).integers(0, 4, 700).astype(np.int32)
+    a = oracle.objective_X(X, lab, 4, oracle.GAUSSIAN, 0.1)
+    import subprocess
+    import sys
+    code = ("import numpy as np, oracle, synth; X = synth.blobs(700, 5, 4, seed=9); "
+            "lab = np.random.default_rng(1).integers(0, 4, 700).astype(np.int32); "
+            "print(repr(oracle.objective_X(X, lab, 4, oracle.GAUSSIAN, 0.1)))")
+    env = dict(os.environ, OMP_NUM_THREADS="1",
+               PYTHONPATH=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = subprocess.check_output([sys.executable, "-c", code], env=env, text=True).strip()
+    assert float(out) == a

@@ -9,6 +9,9 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from parity import j_tol  # noqa: E402
 import paper_2601_17136_b200 as kkm  # noqa: E402
 import synth  # noqa: E402
 
@@ -35,11 +38,17 @@ cases += [("har200k", 3001, 6, kkm.PATH_MATERIALIZE, 1, dict(symmetric=kkm.SYM_O
           # n > 32768: the a3 that reads the int64 S itself and, on several ranks, the peer-memory
           # exchange of S over NVLink (setup_p2p); checked against the 1-GPU run (bitwise), no oracle
           ("mnist60k", 36001, 6, kkm.PATH_MATERIALIZE, 1, {}),
+          ("mnist60k", 36001, 6, kkm.PATH_MATERIALIZE, 1, dict(p2p=True)),
           ("rings", 1000, 60, kkm.PATH_STREAM, 1, dict(stop_on_no_change=True, incremental=True))]
 for name, n, iters, path, g, opt in cases:
     X, cfg = synth.make_config(name, n=n)
     args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
     r0, r1 = kkm.shard_begin(n, rank, world), kkm.shard_begin(n, rank + 1, world)
+    opt = dict(opt)
+    if opt.pop("p2p", False):  # the opt-in peer-memory exchange (read by kkm_init, agreed by all ranks)
+        os.environ["KKM_P2P"] = "1"
+    else:
+        os.environ.pop("KKM_P2P", None)
     h = kkm.KernelKMeans(torch.from_numpy(X[r0:r1]).cuda(), n, cfg["k"], *args, max_iter=iters,
                          rank=rank, nranks=world, comm=comm, path=path, grid_rows=g, **opt)
     it, J, ch = h.fit()
@@ -53,9 +62,18 @@ for name, n, iters, path, g, opt in cases:
         one = kkm.KernelKMeans(torch.from_numpy(X).cuda(), n, cfg["k"], *args, max_iter=iters, path=path, **opt)
         it1, J1, _ = one.fit()
         lab1 = one.assign().cpu().numpy()
+        have_ref = n <= 10000
         ref = (oracle.fit(X, cfg["k"], *args, max_iter=iters, stop_on_no_change=bool(opt.get("stop_on_no_change")))
-               if n <= 10000 else dict(labels=lab1, J_trace=J1))
+               if have_ref else dict(labels=lab1, J_trace=J1))
         same &= it == it1
+        diag = oracle.kernel_diag(X, *args)
+        if have_ref:  # the oracle ran: labels identical, J trace within the north_star rule
+            ok &= np.array_equal(lab, ref["labels"]) and it == ref["iters"]
+            ok &= all(abs(a - b) <= j_tol(b, diag) for a, b in zip(J, ref["J_trace"]))
+        else:  # J of the final labels from the points (oracle.objective_X, reading A8)
+            Jx = oracle.objective_X(X, lab, cfg["k"], *args)
+            ok &= abs(J[-1] - Jx) <= j_tol(Jx, diag)
+            print(f"  J(final) {J[-1]:.10e} oracle {Jx:.10e} rel {abs(J[-1] - Jx) / abs(Jx):.2e}", flush=True)
         msg = (f"{name} n={n} P={world} grid {g}x{world // g} {'stream' if path == kkm.PATH_STREAM else 'mat'} "
                f"{opt}: iters {it}/{it1} "
                f"ranks identical={same} labels==1gpu {np.array_equal(lab, lab1)} "
