@@ -152,6 +152,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   // f1: symmetric band storage (1D, k <= 16). Bands go to ranks largest first, each to the
   // least-loaded rank (lowest rank on ties): deterministic, area-balanced.
   const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= SP_KPMAX;
+  const bool ssym_elig = p->symmetric != KKM_SYM_OFF && pr == 1;  // streaming f1: any k (ssym.cuh)
   P.kh = p->kstore == KKM_KSTORE_FP16 || p->kstore == KKM_KSTORE_FP16X2;  // AUTO: decided below
   const bool kh_pitch = P.kh || (p->kstore == KKM_KSTORE_AUTO && P.tc);  // the bands if stored are 16-bit
   P.kplanes = p->kstore == KKM_KSTORE_FP16 ? 1 : 2;
@@ -249,21 +250,36 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.sym = P.materialize && sym_ok;
   // f1 on the streaming path: upper-triangle pair tiles of the label-sorted K, work units
   // (row tile, first column tile, count) of <= 512 tiles, spread over the ranks largest first
-  P.ssym = !P.materialize && sym_elig && P.tc;
+  P.ssym = !P.materialize && ssym_elig && P.tc;
   P.units.clear();
   if (P.ssym) {
     const int64_t Tt = ceil_div(n, 256);
     std::vector<int4> all;
-    // units = (row tile, globally aligned block of <= 64 column tiles): the ~74 pairs running
-    // at once hold a few row tiles x the same column blocks, sweeping the same B tiles in step,
-    // so the working set stays far below L2 (unaligned per-row ranges: 46 % L2 hits, 0.9 MB of
-    // DRAM per tile at n = 200k)
-    constexpr int64_t BS = 64;
-    for (int64_t tm = 0; tm < Tt; ++tm)
-      for (int64_t b = tm / BS; b * BS < Tt; ++b) {
-        const int64_t a = std::max(tm, b * BS), e = std::min(Tt, (b + 1) * BS);
-        all.push_back(make_int4((int)tm, (int)a, (int)(e - a), 0));
-      }
+    // units = (row tile, globally aligned block of <= BS column tiles); a rank's units run
+    // block-major (below), so the ~74 pairs running at once sweep the same block of B tiles
+    // with different row tiles: the block (BS x 256 rows of the split operand) and the pairs'
+    // A tiles stay L2-resident
+    int64_t BS = 32;
+    if (const char *e = std::getenv("KKM_SSYM_BS")) BS = std::max<int64_t>(1, std::atoll(e));
+    const bool tile_major = std::getenv("KKM_SSYM_TILE_MAJOR") != nullptr;  // (the round-1 order, A/B only)
+    // G > 0: single-tile units in a supertile raster -- G x G patches of the upper triangle, patch
+    // by patch, each patch column by column -- so the ~74 tiles in flight cover a compact patch
+    // (~9 row tiles x ~9 column tiles: ~15 MB of operands in L2 instead of 74 row tiles + a block)
+    int64_t G = 0;
+    if (const char *e = std::getenv("KKM_SSYM_G")) G = std::max<int64_t>(0, std::atoll(e));
+    if (G > 0) {
+      for (int64_t I = 0; I * G < Tt; ++I)
+        for (int64_t J = I; J * G < Tt; ++J)
+          for (int64_t tn = J * G; tn < std::min(Tt, (J + 1) * G); ++tn)
+            for (int64_t tm = I * G; tm < std::min(Tt, (I + 1) * G) && tm <= tn; ++tm)
+              all.push_back(make_int4((int)tm, (int)tn, 1, 0));
+    } else {
+      for (int64_t tm = 0; tm < Tt; ++tm)
+        for (int64_t b = tm / BS; b * BS < Tt; ++b) {
+          const int64_t a = std::max(tm, b * BS), e = std::min(Tt, (b + 1) * BS);
+          all.push_back(make_int4((int)tm, (int)a, (int)(e - a), 0));
+        }
+    }
     std::vector<int64_t> load(nranks, 0);
     std::vector<int> order(all.size());
     for (size_t i = 0; i < all.size(); ++i) order[i] = (int)i;
@@ -276,8 +292,13 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
       load[r] += all[i].z;
       if (r == rank) mine[i] = 1;
     }
-    for (size_t i = 0; i < all.size(); ++i)  // tile-major order on the rank (A reuse in L2)
+    for (size_t i = 0; i < all.size(); ++i)
       if (mine[i]) P.units.push_back(all[i]);
+    if (!tile_major && G == 0)  // block-major order on the rank: (column block, row tile)
+      std::stable_sort(P.units.begin(), P.units.end(), [&](const int4 &x, const int4 &y) {
+        const int64_t bx = x.y / BS, by = y.y / BS;
+        return bx != by ? bx < by : x.x < y.x;
+      });
     P.nsplit = 1;
   }
   P.tbands.clear();
@@ -568,6 +589,7 @@ struct kkm_ctx {
   int *bad;
   int cur = 0;  // labels[cur] / sizes[cur] are the labels entering the next iteration
   bool poisoned = false;
+  bool ssym_v1 = false;  // KKM_SSYM_V1=1: the round-1 streaming f1 kernel (A/B measurements, k <= 16)
   bool have_last = false;
   bool cnorm2_valid = false;  // cnorm2 holds c of the current labels (after kkm_fit / kkm_objective)
   int64_t launches = 0;
@@ -873,9 +895,12 @@ int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   CKR(sort_gather(h, labels, 0, P.n, P.npad, B));
   CK(cudaMemsetAsync(h->Sfix, 0, (size_t)P.npad * k * 8, h->st));
   a2_mark(h);
-  int rc = tc2_stream_sym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg,
-                                 k, h->kp, h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st,
-                                 &h->launches);
+  int rc = h->ssym_v1 ? tc2_stream_sym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms,
+                                               h->srscale, h->seg, k, h->kp, h->units, (int64_t)P.units.size(),
+                                               h->fx_scale, h->Sfix, h->st, &h->launches)
+                      : ssym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg,
+                                    k, h->kp, h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st,
+                                    &h->launches);
   a2_mark(h);
   if (rc) {
     h->poisoned = true;
@@ -1286,6 +1311,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->gfirst = (int32_t *)(w + P.o_gfirst);
     h->Sfin = (double *)(w + P.o_Sfin);
   }
+  h->ssym_v1 = std::getenv("KKM_SSYM_V1") && std::atoi(std::getenv("KKM_SSYM_V1")) == 1 && P.k <= 16;
   h->kp.kind = p->kind;
   h->kp.degree = p->degree;
   h->kp.gamma = (float)p->gamma;

@@ -69,6 +69,71 @@ __device__ __forceinline__ int ss_segment_of(const int32_t *seg, int k, int64_t 
 
 __device__ __forceinline__ long long ss_fix(double v, double fx) { return __double2ll_rn(v * fx); }
 
+// One 32-column chunk of a tile (columns p0 .. p0 + 31, this thread's row p): kappa, the row part
+// into the running sum (flushed on a segment change), the column part (off-diagonal tiles).
+// cn: the chunk's column norms at cn[0..32) and rscale at cn[SS_COLS..SS_COLS + 32).
+__device__ __forceinline__ void ss_chunk(float (&x)[32], int64_t p0, const float *cn, const KappaParams &kp,
+                                         const RowK &rk, bool diag, int64_t p, bool row_ok, int64_t n,
+                                         const int32_t *seg, int k, int &cseg, int &cur, double &run, int r0, int r1,
+                                         int mylab, int lane, double fx_scale, long long *__restrict__ Sfix) {
+  if (p0 >= n) return;
+  kappa_chunk_sum(x, cn, cn + SS_COLS, kp, rk);
+  if (diag && kp.kind == 2 && p >= p0 && p < p0 + 32) {  // kappa(x_p, x_p) = 1 exactly (A1)
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (p0 + q == p) x[q] = 1.f;
+  }
+  if (p0 + 32 > n) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (p0 + q >= n) x[q] = 0.f;
+  }
+  if (!row_ok) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) x[q] = 0.f;
+  }
+  // row part: the chunk's columns are segments c0 .. c1 (the warp's pointer only moves forward)
+  const int64_t p1 = p0 + 31 < n ? p0 + 31 : n - 1;
+  while (cseg + 1 < k && seg[cseg + 1] <= p0) ++cseg;
+  const int c0 = cseg;
+  int c1 = c0;
+  while (c1 + 1 < k && seg[c1 + 1] <= p1) ++c1;
+  if (c0 == c1) {
+    float2 s2 = make_float2(x[0], x[1]);
+#pragma unroll
+    for (int q = 2; q < 32; q += 2) s2 = f2add(s2, make_float2(x[q], x[q + 1]));
+    if (c0 != cur) {
+      if (cur >= 0 && row_ok) red_add_s64(Sfix + p * k + cur, ss_fix(run, fx_scale));
+      run = 0.0;
+      cur = c0;
+    }
+    run += (double)(s2.x + s2.y);
+  } else {
+    for (int cc = c0; cc <= c1; ++cc) {
+      const int64_t lo = seg[cc] - p0, hi = (cc + 1 < k ? (int64_t)seg[cc + 1] : n) - p0;
+      float sum = 0.f;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) sum += (q >= lo && q < hi) ? x[q] : 0.f;
+      if (cc != cur) {
+        if (cur >= 0 && row_ok) red_add_s64(Sfix + p * k + cur, ss_fix(run, fx_scale));
+        run = 0.0;
+        cur = cc;
+      }
+      run += (double)sum;
+    }
+  }
+  if (diag) return;
+  // column part: column p0 + l gets the sum over the warp's rows of each row label
+  if (r0 == r1) {  // one label (almost always): the butterfly consumes x
+    const float cs = lane_column_sum(x, lane);
+    if (p0 + lane < n) red_add_s64(Sfix + (p0 + lane) * k + r0, ss_fix((double)cs, fx_scale));
+  } else if (row_ok) {  // the rows straddle a segment boundary: element by element
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (p0 + q < n) red_add_s64(Sfix + (p0 + q) * k + mylab, ss_fix((double)x[q], fx_scale));
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
     ssym_kernel(const __grid_constant__ CUtensorMap t_hi, const __grid_constant__ CUtensorMap t_lo, uint32_t idesc,
                 int nkb, int64_t n, const float *__restrict__ snorms, const float *__restrict__ srscale,
@@ -123,26 +188,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
         mbar_wait(s.tfull, (uint32_t)(it & 1));
         tc_fence_after();
         // 1. drain main + correction into registers, give TMEM back
-        float v[SS_COLS];
+        float va[32], vb[32];
         {
           float w[32];
-          tmem_ld32_nowait(tq, *reinterpret_cast<float(*)[32]>(&v[0]));
+          tmem_ld32_nowait(tq, va);
           tmem_ld32_nowait(tq + 256u, w);
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 32; q += 2) {
-            const float2 t = f2add(make_float2(v[q], v[q + 1]), make_float2(w[q], w[q + 1]));
-            v[q] = t.x;
-            v[q + 1] = t.y;
+            const float2 t = f2add(make_float2(va[q], va[q + 1]), make_float2(w[q], w[q + 1]));
+            va[q] = t.x;
+            va[q + 1] = t.y;
           }
-          tmem_ld32_nowait(tq + 32u, *reinterpret_cast<float(*)[32]>(&v[32]));
+          tmem_ld32_nowait(tq + 32u, vb);
           tmem_ld32_nowait(tq + 256u + 32u, w);
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 32; q += 2) {
-            const float2 t = f2add(make_float2(v[32 + q], v[33 + q]), make_float2(w[q], w[q + 1]));
-            v[32 + q] = t.x;
-            v[33 + q] = t.y;
+            const float2 t = f2add(make_float2(vb[q], vb[q + 1]), make_float2(w[q], w[q + 1]));
+            vb[q] = t.x;
+            vb[q + 1] = t.y;
           }
         }
         tc_fence_before();
@@ -150,67 +215,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
         if (lane == 0) mbar_arrive_cluster(s.tempty, 0);
         if (rw >= n) continue;
         // 2. per chunk: kappa, row part, column part
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float(&x)[32] = *reinterpret_cast<float(*)[32]>(&v[32 * c]);
-          const int64_t p0 = pbase + 32 * c;
-          if (p0 >= n) continue;
-          kappa_chunk_sum(x, cn + 32 * c, cn + SS_COLS + 32 * c, kp, rk);
-          if (diag && kp.kind == 2 && p >= p0 && p < p0 + 32) {  // kappa(x_p, x_p) = 1 exactly (A1)
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (p0 + q == p) x[q] = 1.f;
-          }
-          if (p0 + 32 > n) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (p0 + q >= n) x[q] = 0.f;
-          }
-          if (!row_ok) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) x[q] = 0.f;
-          }
-          // row part: the chunk's columns are segments c0 .. c1 (advance the warp's pointer)
-          const int64_t p1 = p0 + 31 < n ? p0 + 31 : n - 1;
-          while (cseg + 1 < k && seg[cseg + 1] <= p0) ++cseg;
-          const int c0 = cseg;
-          int c1 = c0;
-          while (c1 + 1 < k && seg[c1 + 1] <= p1) ++c1;
-          if (c0 == c1) {
-            float2 s2 = make_float2(x[0], x[1]);
-#pragma unroll
-            for (int q = 2; q < 32; q += 2) s2 = f2add(s2, make_float2(x[q], x[q + 1]));
-            if (c0 != cur) {
-              if (cur >= 0 && row_ok) red_add_s64(Sfix + p * k + cur, ss_fix(run, fx_scale));
-              run = 0.0;
-              cur = c0;
-            }
-            run += (double)(s2.x + s2.y);
-          } else {
-            for (int cc = c0; cc <= c1; ++cc) {
-              const int64_t lo = seg[cc] - p0, hi = (cc + 1 < k ? seg[cc + 1] : n) - p0;
-              float sum = 0.f;
-#pragma unroll
-              for (int q = 0; q < 32; ++q) sum += (q >= lo && q < hi) ? x[q] : 0.f;
-              if (cc != cur) {
-                if (cur >= 0 && row_ok) red_add_s64(Sfix + p * k + cur, ss_fix(run, fx_scale));
-                run = 0.0;
-                cur = cc;
-              }
-              run += (double)sum;
-            }
-          }
-          if (diag) continue;
-          // column part: column p0 + l gets the sum over the warp's rows of each row label
-          if (r0 == r1) {  // one label (almost always): the butterfly consumes x
-            const float cs = lane_column_sum(x, lane);
-            if (p0 + lane < n) red_add_s64(Sfix + (p0 + lane) * k + r0, ss_fix((double)cs, fx_scale));
-          } else if (row_ok) {  // rows straddle a segment boundary: element by element
-#pragma unroll 4
-            for (int q = 0; q < 32; ++q)
-              if (p0 + q < n) red_add_s64(Sfix + (p0 + q) * k + mylab, ss_fix((double)x[q], fx_scale));
-          }
-        }
+        ss_chunk(va, pbase, cn, kp, rk, diag, p, row_ok, n, seg, k, cseg, cur, run, r0, r1, mylab, lane, fx_scale,
+                 Sfix);
+        ss_chunk(vb, pbase + 32, cn + 32, kp, rk, diag, p, row_ok, n, seg, k, cseg, cur, run, r0, r1, mylab, lane,
+                 fx_scale, Sfix);
       }
       if (cur >= 0 && row_ok) red_add_s64(Sfix + p * k + cur, ss_fix(run, fx_scale));
     }

@@ -338,3 +338,13 @@ def test_extreme_feature_dims(precision, d):
 def test_large_d_objective_limit():
     X = synth.blobs(700, 3000, 4, seed=3080, sep=4.0)
     teacher_forced(X, 4, oracle.GAUSSIAN, 0.5 / 3000, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE))
+
+
+@pytest.mark.parametrize("k", [17, 32, 64])
+def test_stream_symmetric_large_k(k):
+    """f1 on the streaming path for k > 16 (ssym.cuh: one running sum per row flushed at each
+    column-segment change, no per-cluster register array): n = 9001 spans several aligned column
+    blocks of the upper-triangle units; teacher-forced against the oracle."""
+    X = synth.blobs(9001, 24, k, seed=90 + k, sep=3.0)
+    teacher_forced(X, k, oracle.GAUSSIAN, 0.02, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_STREAM))
+    teacher_forced(X, k, oracle.POLY, 0.05, 1.0, 2, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_STREAM))
