@@ -156,6 +156,28 @@ typedef struct kkm_params {
 
 typedef struct kkm_ctx *kkm_handle;
 
+/* ---- planner introspection (kkm_plan_query) ------------------------------- */
+#define KKM_LAYOUT_FULL 0         /* K rows of the A set x the B set, materialised (Alg. 1 / Alg. 2)  */
+#define KKM_LAYOUT_STREAM 1       /* the same tile recomputed per iteration, K never stored             */
+#define KKM_LAYOUT_SYM_BANDS 2    /* f1: upper-triangle bands of 1024 rows, fp32 (sym.cuh)             */
+#define KKM_LAYOUT_SYM_BANDS16 3  /* f1: the bands as 16-bit planes in pieces of <= 1024 rows (spmm_tc) */
+#define KKM_LAYOUT_SYM_STREAM 4   /* f1: upper-triangle tiles of the label-sorted K, recomputed (ssym) */
+#define KKM_XCHG_NONE 0           /* one rank                                                           */
+#define KKM_XCHG_PARTIALS 1       /* per iteration: allgather of (k+1) partials, labels, sizes (1D/1.5D) */
+#define KKM_XCHG_S_ALLREDUCE 2    /* per iteration: one allreduce of S (n x k), a3/a4 replicated        */
+#define KKM_XCHG_S_REDUCE_SCATTER 3 /* per iteration: reduce-scatter of S to the 1D blocks + partials   */
+typedef struct kkm_plan_info {
+  int32_t path;          /* effective KKM_PATH_MATERIALIZE or KKM_PATH_STREAM                    */
+  int32_t layout;        /* KKM_LAYOUT_*                                                          */
+  int32_t exchange;      /* KKM_XCHG_* (before the opt-in peer-memory variant, see kkm_init)      */
+  int32_t grid_rows, grid_cols;
+  int32_t reserved;
+  int64_t row0, nloc;    /* the rank's own 1D block of points                                     */
+  int64_t a0, nA, b0, nB;/* KKM_LAYOUT_FULL / STREAM: the K tile's rows (A set) and columns (B set) */
+  int64_t npieces;       /* rectangles of K (or of the label-sorted K) this rank computes           */
+  int64_t ws_bytes;      /* = kkm_workspace_size                                                  */
+} kkm_plan_info;
+
 /* Fills *p with defaults: polynomial kernel (gamma 1, coef0 1, degree 2, the paper's
  * benchmark kernel P:640), k = 2, max_iter = 100, AUTO, FP16X3. */
 int kkm_default_params(kkm_params *p);
@@ -173,6 +195,18 @@ int64_t kkm_shard_begin(int64_t n, int32_t rank, int32_t nranks);
  * columns each, bands spread over the ranks by area): ~n^2/(2P) floats. */
 int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks,
                        size_t *bytes);
+
+/* Pure planner introspection (no CUDA): what rank `rank` of `nranks` computes and exchanges, so the
+ * decomposition can be checked for any P on a host without GPUs (tests/test_plan_cover.py).
+ *   info:   out (required).
+ *   pieces: NULL, or host int64[cap][5]: the rank's rectangles (r0, nr, c0, nc, cdiag) of K in
+ *           global indices -- of the label-sorted K for KKM_LAYOUT_SYM_STREAM. The rank adds the
+ *           row part S(i, cl(j)) += K(i, j) for every (i, j) of the rectangle and, for columns
+ *           j >= cdiag, also the column part S(j, cl(i)) += K(i, j) (symmetry); cdiag = n for
+ *           layouts without column parts. At most cap rectangles are written; info->npieces is the
+ *           total. Same errors as kkm_workspace_size. */
+int kkm_plan_query(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, kkm_plan_info *info,
+                   int64_t *pieces, int64_t cap);
 
 /* Creates a handle and runs the one-time part of the path.
  * Sharding (P = nranks, B = ceil(n / P), pr = grid_rows, pc = P / pr, rank = i + j * pr):

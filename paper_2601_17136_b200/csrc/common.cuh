@@ -53,7 +53,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // kappa applied to b = x_i . x_j (Eqs. b, k; Gaussian by reading A1 with
-// r^2 = ||x_i||^2 + ||x_j||^2 - 2 b clamped at 0, reading A23; on the diagonal (same
+// r^2 = (||x_i||^2 - b) + (||x_j||^2 - b) clamped at 0, reading A23; on the diagonal (same
 // point, `same`) r^2 = 0 exactly so K_ii = 1 as the definition gives).
 __device__ __forceinline__ float kappa_epilogue(const KappaParams &kp, float b, float ni, float nj,
                                                 bool same = false) {
@@ -64,7 +64,7 @@ __device__ __forceinline__ float kappa_epilogue(const KappaParams &kp, float b, 
     for (int e = 1; e < kp.degree; ++e) r *= base;
     return r;
   }
-  float r2 = same ? 0.0f : fmaxf(fmaf(-2.0f, b, ni + nj), 0.0f);
+  float r2 = same ? 0.0f : fmaxf((ni - b) + (nj - b), 0.0f);  // exact differences for near points
   return ex2_approx(kp.neg_gamma_log2e * r2);
 }
 

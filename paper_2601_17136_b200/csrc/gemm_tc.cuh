@@ -1,10 +1,8 @@
 // gemm_tc.cuh -- shared tcgen05 / TMA building blocks of the tensor-core kernels in tc2.cuh:
 // operand split reading A9 (bf16x3 or fp16x3: b = hi*hi + (hi*lo + lo*hi), 3 MMAs with fp32 TMEM
 // accumulation, product error ~2^-16..2^-22 relative instead of bf16's 2^-8), the UMMA smem
-// descriptor (128-byte swizzle, K-major), TMEM loads, L2 cache policies, TMA stores, the
-// per-column constant staging of the epilogue, and the host-side tensor-map encoders.
-// (A first 1-CTA M=128 GEMM and streaming kernel lived here and in stream.cuh; the CTA-pair
-// kernels of tc2.cuh replaced them -- DESIGN.md §5.1.)
+// descriptor (128-byte swizzle, K-major), TMEM loads, L2 cache policies, TMA stores and the
+// host-side operand tensor-map encoder (the kernels: tc3.cuh, ssym.cuh on chain.cuh).
 #pragma once
 #include <cuda.h>
 
@@ -52,28 +50,6 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32])
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 
-// Lane-parallel load of 128 per-column constants (norm_j, rscale_j) of columns [j, j+128) into
-// smem cn[0..128) / cn[128..256); missing columns get (0, 1). Ends with __syncwarp.
-__device__ __forceinline__ void stage_column_constants(float *cn, const float *__restrict__ norms,
-                                                       const float *__restrict__ rscale, int64_t j,
-                                                       int64_t nvalid, bool need_norm, int lane) {
-  const int64_t p = j + lane * 4;
-  float4 nv = make_float4(0.f, 0.f, 0.f, 0.f), rv = make_float4(1.f, 1.f, 1.f, 1.f);
-  float *pn = &nv.x, *pr = &rv.x;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (p + q < nvalid) {
-      if (need_norm) pn[q] = __ldg(norms + p + q);
-      if (rscale) pr[q] = __ldg(rscale + p + q);
-    }
-  __syncwarp();
-  reinterpret_cast<float4 *>(cn)[lane] = nv;
-  reinterpret_cast<float4 *>(cn + 128)[lane] = rv;
-  __syncwarp();
-}
-
-
-
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int c1, const void *smem_src,
                                              uint64_t pol) {
   asm volatile(
@@ -83,9 +59,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int
       : "memory");
 }
 
-constexpr int TC_EPI_WARPS = 8;
-constexpr uint32_t TC_STAGING_BYTES = 32 * 16 * 4;  // per epilogue warp: 32 rows x 16 fp32 (SW64 box)
-constexpr uint32_t TC_COLC_BYTES = 256 * 4;          // per epilogue warp: 128 x (norm_j, rscale_j)
 // ---------------------------------------------------------------- host side
 struct TcGemm {
   const void *hi = nullptr, *lo = nullptr;  // operands the tensor maps describe
@@ -146,28 +119,6 @@ inline int tc_make_maps(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, boo
   g.lo = Xlo;
   g.fp16 = fp16;
   return 0;
-}
-
-// [m x ncov] view of out (row pitch ldo elements) for the TMA stores: fp32 boxes of 32 rows x 16
-// columns (ldo % 4 == 0), or with half_out fp16 boxes of 32 x 32 (ldo % 8 == 0); 64-byte swizzle.
-inline int tc_encode_out_map(CUtensorMap *map, void *out, int64_t m, int64_t ncov, int64_t ldo, bool half_out) {
-  if (tc_encode_ready()) return 1;
-  cuuint64_t dims[2] = {(cuuint64_t)ncov, (cuuint64_t)m};
-  cuuint64_t strides[1] = {(cuuint64_t)ldo * (half_out ? 2 : 4)};
-  cuuint32_t box[2] = {half_out ? 32u : 16u, 32u};
-  cuuint32_t es[2] = {1u, 1u};
-  CUresult r = tc_encode_fn()(map, half_out ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                              2, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    tc_err_slot() = "cuTensorMapEncodeTiled (output) failed";
-    return 1;
-  }
-  return 0;
-}
-inline int tc_make_out_map(TcGemm &g, void *out, int64_t m, int64_t ncov, int64_t ldo, bool half_out = false) {
-  return tc_encode_out_map(&g.map_out, out, m, ncov, ldo, half_out);
 }
 
 

@@ -28,6 +28,7 @@
 #include "sym.cuh"
 #include "tc2.cuh"
 #include "ssym.cuh"
+#include "tc3.cuh"
 #include "update.cuh"
 
 using namespace kkm;
@@ -61,6 +62,7 @@ struct Plan {
   int sort_blocks;              // streaming: blocks of the counting sort
   bool spmm_v2;                 // materialised a2 with label-sorted 32-column groups (k <= 64)
   int nsplit, chunks_per_split, nfin, nspmm_pass;
+  int stream_splits = 1;  // column splits per row tile of the full streaming kernel (tc3_stream_kernel)
   int64_t rows_per_block;
   size_t kelems;       // materialised K elements (per 16-bit plane)
   int64_t s_rows_pad;  // row pitch of the S (or S partials) finalize reads
@@ -82,7 +84,7 @@ struct Plan {
   int64_t sym_items;
   std::vector<SymBand> bands;       // owned bands, ascending I
   std::vector<int32_t> band_desc;   // band -> index into bands, or -1
-  bool ssym;                        // f1 on the streaming path (tc2_stream_sym_kernel)
+  bool ssym;                        // f1 on the streaming path (ssym_kernel, ssym.cuh)
   // f4 fp16 K storage (spmm_tc.cuh): the f1 bands in fp16, a2 on the tensor cores
   bool kh;
   int kplanes;                      // 16-bit planes per K value: 1 (FP16) or 2 (FP16X2: hi + lo)
@@ -95,7 +97,7 @@ struct Plan {
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
       o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_gregs, o_gmaps, o_a3ctr, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
-      o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_mean, o_cmpart, total;
+      o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_Sdx, o_Sx, o_mean, o_cmpart, total;
 };
 
 int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, Plan *pl) {
@@ -233,18 +235,17 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
   } else {
     // work units of the fused kernel = 128-row tiles x column splits; 148 SMs assumed for the
-    // load-balance choice (B200); each split writes one partial per column half
-    // work units = 256-row pair tiles x column splits (74 CTA pairs), ordered tile-major (the
-    // clusters working on one row tile's splits share its A operand in L2). Splits: at most 512
-    // 256-column tiles per unit, which bounds how far the concurrent sweeps over B drift apart
-    // (measured at n = 1M: 4.41 -> 3.92 s per iteration); then the best last-wave fill; fp64
-    // partials <= 16 GB.
+    // load-balance choice (B200). Work units = 256-row pair tiles x column splits (74 CTA pairs),
+    // ordered tile-major (the clusters working on one row tile's splits share its A operand in
+    // L2). Splits: at most 512 256-column tiles per unit, which bounds how far the concurrent
+    // sweeps over B drift apart (measured at n = 1M: 4.41 -> 3.92 s per iteration); then the best
+    // last-wave fill. The kernel sums S in int64 fixed point (one [rows][k] array, any number of
+    // splits), converted once to fp64: one partial for a3 (nsplit = 1).
     const int64_t tiles_n = ceil_div(std::max<int64_t>(P.nB, 1), 256);
-    int64_t s_l2 = ceil_div(tiles_n, 512);
-    const int64_t s_mem = std::max<int64_t>(1, (int64_t)(16e9 / (2.0 * P.nApad * P.k * 8)));
-    s_l2 = std::min(s_l2, s_mem);
+    const int64_t s_l2 = ceil_div(tiles_n, 512);
     const int s_bal = ts_choose_splits((P.nA + 1) / 2, P.nB, 74);
-    P.nsplit = 2 * (int)std::max<int64_t>(s_l2, s_bal);
+    P.stream_splits = (int)std::max<int64_t>(s_l2, s_bal);
+    P.nsplit = 1;
     P.chunks_per_split = 0;
   }
   P.sym = P.materialize && sym_ok;
@@ -436,6 +437,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_seg = take((size_t)(P.k + 1) * 4);
     P.o_bcount = take((size_t)P.sort_blocks * P.k * 4);
     P.o_boff = take((size_t)P.sort_blocks * P.k * 4);
+    if (!P.ssym) P.o_Sx = take((size_t)P.nApad * P.k * 8);  // the full streaming kernel's int64 S
   }
   if (P.materialize && P.spmm_v2) P.o_codes = take((size_t)P.ldk * 4);
   if (P.pr > 1) {
@@ -449,7 +451,6 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_Sfix = take((size_t)P.npad * P.k * 8);
     P.o_Sorig = P.nranks > 1 ? take((size_t)P.npad * P.k * 8) : 0;
     P.o_Sfmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
-    P.o_fxmax = take(16);
   }
   if (P.inc) {
     const int64_t nblk = ceil_div(P.n, SORT_BLOCK);
@@ -464,7 +465,8 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_Dlo = take((size_t)P.dpad * P.dp * 2);
     P.o_Dn = take((size_t)P.dpad * 4);
     P.o_Dr = take((size_t)P.dpad * 4);
-    P.o_Sd = take((size_t)16 * P.B * P.k * 8);
+    P.o_Sd = take((size_t)P.B * P.k * 8);   // fp64 S of the moved points' pass
+    P.o_Sdx = take((size_t)P.B * P.k * 8);  // its int64 fixed-point sums
   }
   if (P.sym) {
     P.o_perm_b = take((size_t)P.T * SYM_TB * 4);
@@ -489,9 +491,9 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_tSfix = take((size_t)P.npad * P.k * 8);  // int64 fixed-point S, [label][row]
     P.o_tSint = P.nranks > 1 ? take((size_t)P.npad * P.k * 8) : 0;
     P.o_tSmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
-    P.o_fxmax = take(16);
   }
   P.o_a3ctr = take(16);
+  P.o_fxmax = take(16);
   P.total = off;
   return KKM_OK;
 }
@@ -579,6 +581,7 @@ struct kkm_ctx {
   double fx_scale = 1.0, fx_inv = 1.0;
   // f3 incremental S
   double *Sinc = nullptr, *Sd = nullptr;
+  long long *Sdx = nullptr;
   int32_t *dkey = nullptr;
   SortedSet dset{};
   bool s_valid = false;  // Sinc holds S of the current labels
@@ -589,7 +592,7 @@ struct kkm_ctx {
   int *bad;
   int cur = 0;  // labels[cur] / sizes[cur] are the labels entering the next iteration
   bool poisoned = false;
-  bool ssym_v1 = false;  // KKM_SSYM_V1=1: the round-1 streaming f1 kernel (A/B measurements, k <= 16)
+  int chain_kb = 0;      // K-blocks per accumulation chain of every tensor-core kernel (0: CH_CKB; KKM_CHAIN_KB)
   bool have_last = false;
   bool cnorm2_valid = false;  // cnorm2 holds c of the current labels (after kkm_fit / kkm_objective)
   int64_t launches = 0;
@@ -684,39 +687,25 @@ struct StreamA {
   int64_t arows, row0, nA, rows_pad;
 };
 
-// One fused a1+a2 pass: Spart[nsplit][rows_pad][k] = per-split sums over the sorted set B (nB
-// points, brows rows) of kappa(a_i, b_p) by cluster. pos (NULL if A and B are disjoint): sorted
-// position of A row i for b0 <= i < b0 + nB (the Gaussian diagonal). k <= 16: one launch; else
-// one launch per group of 16 clusters over that group's contiguous sorted rows (same total
-// work; the host reads the k + 1 segment starts first).
+// One fused a1+a2 pass: S[rows_pad][k] (fp64) = the sums over the sorted set B (nB points, brows
+// rows, k segments) of kappa(a_i, b_p) by cluster -- accumulated by tc3_stream_kernel in int64 fixed
+// point (Sx, exact integer sums in any order, any k in one launch) and converted once. pos (NULL if
+// A and B are disjoint): sorted position of A row i for b0 <= i < b0 + npos (the Gaussian
+// diagonal). fx = 2^s with nB max|K| 2^s < 2^61.
 int stream_pass(kkm_ctx *h, TcStream &ts, const StreamA &A, const SortedSet &B, int64_t brows, int64_t nB,
-                int64_t b0, const int32_t *pos, int64_t npos, int nsplit, double *Spart) {
+                int64_t b0, const int32_t *pos, int64_t npos, int splits, double fx, long long *Sx, double *S) {
   const Plan &P = h->P;
   const int k = P.k;
   if (A.nA == 0) return KKM_OK;
-  auto launch = [&](int64_t s0, int64_t nb, int c0, int kg) -> int {
-    int rc = tc2_stream_launch(ts, A.hi, A.lo, B.hi + s0 * P.dp, B.lo + s0 * P.dp, P.fp16, A.arows, brows - s0, P.dp,
-                               nb, b0, A.row0, A.nA, A.rows_pad, A.norms, A.rscale, B.norms + s0, B.rscale + s0, pos,
-                               npos, B.seg + c0, kg, h->kp, nsplit / 2, Spart, k, c0, h->st, &h->launches);
-    if (rc) {
-      h->poisoned = true;
-      return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
-    }
-    return KKM_OK;
-  };
-  if (k <= 16) return launch(0, nB, 0, k);
-  std::vector<int32_t> seg((size_t)k + 1);
-  CK(cudaMemcpyAsync(seg.data(), B.seg, (size_t)(k + 1) * 4, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  for (int c0 = 0; c0 < k; c0 += 16) {
-    const int kg = std::min(16, k - c0);
-    const int64_t s0 = seg[c0], nb = seg[c0 + kg] - s0;
-    if (nb == 0) {  // all clusters of the group empty: their partials are 0
-      CK(cudaMemset2DAsync(Spart + c0, (size_t)k * 8, 0, (size_t)kg * 8, (size_t)nsplit * A.rows_pad, h->st));
-      continue;
-    }
-    CKR(launch(s0, nb, c0, kg));
+  CK(cudaMemsetAsync(Sx, 0, (size_t)A.rows_pad * k * 8, h->st));
+  if (tc3_stream_launch(ts, A.hi, A.lo, B.hi, B.lo, P.fp16, A.arows, brows, P.dp, nB, b0, A.row0, A.nA, A.norms,
+                        A.rscale, B.norms, B.rscale, pos, npos, B.seg, k, h->kp, splits, fx, Sx, h->st, &h->launches,
+                        h->chain_kb)) {
+    h->poisoned = true;
+    return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
   }
+  fx_to_double_kernel<<<(unsigned)ceil_div(A.rows_pad * k, 256), 256, 0, h->st>>>(Sx, A.rows_pad * k, 1.0 / fx, S);
+  CKL();
   return KKM_OK;
 }
 
@@ -728,7 +717,8 @@ int launch_stream(kkm_ctx *h, const int32_t *labels) {
   CKR(sort_gather(h, labels + P.b0, P.b0, P.nB, P.npad, B));
   const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.a0, P.nA, P.nApad};
   a2_mark(h);
-  const int rc = stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, P.nsplit, h->Spart);
+  const int rc = stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, P.stream_splits, h->fx_scale,
+                            (long long *)(h->ws + P.o_Sx), h->Spart);
   a2_mark(h);
   return rc;
 }
@@ -895,12 +885,8 @@ int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   CKR(sort_gather(h, labels, 0, P.n, P.npad, B));
   CK(cudaMemsetAsync(h->Sfix, 0, (size_t)P.npad * k * 8, h->st));
   a2_mark(h);
-  int rc = h->ssym_v1 ? tc2_stream_sym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms,
-                                               h->srscale, h->seg, k, h->kp, h->units, (int64_t)P.units.size(),
-                                               h->fx_scale, h->Sfix, h->st, &h->launches)
-                      : ssym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg,
-                                    k, h->kp, h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st,
-                                    &h->launches);
+  int rc = ssym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg, k, h->kp,
+                       h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st, &h->launches, h->chain_kb);
   a2_mark(h);
   if (rc) {
     h->poisoned = true;
@@ -1019,8 +1005,8 @@ int launch_gemm(kkm_ctx *h, int64_t i0, int64_t m, int64_t j0, int64_t ncov, voi
   const Plan &P = h->P;
   if (m <= 0 || ncov <= 0) return KKM_OK;
   if (P.tc) {
-    int rc = tc2_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0,
-                             ncov, h->norms, h->kp, out, ldo, h->st, &h->launches, oscale, out_lo);
+    int rc = tc3_gemm_launch(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, i0, m, j0, ncov, h->norms,
+                             h->kp, out, ldo, h->st, &h->launches, oscale, out_lo, h->chain_kb);
     if (rc) {
       h->poisoned = true;
       return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
@@ -1043,7 +1029,7 @@ int delta_update(kkm_ctx *h, int64_t m) {
   const int32_t *cl_old = h->lab[h->cur], *cl_new = h->lab[h->cur ^ 1];
   const int nblk = (int)ceil_div(P.n, SORT_BLOCK);
   const int64_t mpad = round_up(m, 256);
-  const int nsplit = 2 * std::min(8, ts_choose_splits((P.nloc + 1) / 2, m, h->num_sms / 2));
+  const int splits = std::min(8, ts_choose_splits((P.nloc + 1) / 2, m, h->num_sms / 2));
   const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.row0, P.nloc, P.B};
   for (int pass = 0; pass < 2; ++pass) {  // 0: + new labels, 1: - old labels
     moved_key_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(cl_old, cl_new, P.n, P.lablen, k,
@@ -1061,8 +1047,8 @@ int delta_update(kkm_ctx *h, int64_t m) {
     CKL();
     // B = the m moved points (clusters 0..k-1 of the k+1 buckets); pos: sorted position of
     // each point (>= m for the points that did not move) for the Gaussian diagonal
-    CKR(stream_pass(h, h->ts_delta, A, D, mpad, m, 0, D.pos, P.n, nsplit, h->Sd));
-    sinc_add_kernel<<<(unsigned)ceil_div(P.nloc * k, 256), 256, 0, h->st>>>(h->Sd, nsplit, P.B, P.nloc, k,
+    CKR(stream_pass(h, h->ts_delta, A, D, mpad, m, 0, D.pos, P.n, splits, h->fx_scale, h->Sdx, h->Sd));
+    sinc_add_kernel<<<(unsigned)ceil_div(P.nloc * k, 256), 256, 0, h->st>>>(h->Sd, 1, P.B, P.nloc, k,
                                                                             pass == 0 ? 1.0 : -1.0, h->Sinc);
     CKL();
   }
@@ -1103,6 +1089,51 @@ int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, 
   Plan P;
   CKR(make_plan(p, n, d, rank, nranks, &P));
   *bytes = P.total;
+  return KKM_OK;
+}
+
+int kkm_plan_query(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks, kkm_plan_info *info,
+                   int64_t *pieces, int64_t cap) {
+  if (!info) return fail(KKM_EINVAL, "info is NULL");
+  Plan P;
+  CKR(make_plan(p, n, d, rank, nranks, &P));
+  std::memset(info, 0, sizeof(*info));
+  info->path = P.materialize ? KKM_PATH_MATERIALIZE : KKM_PATH_STREAM;
+  info->layout = P.sym ? (P.kh ? KKM_LAYOUT_SYM_BANDS16 : KKM_LAYOUT_SYM_BANDS)
+                 : P.ssym ? KKM_LAYOUT_SYM_STREAM : P.materialize ? KKM_LAYOUT_FULL : KKM_LAYOUT_STREAM;
+  info->exchange = nranks == 1 ? KKM_XCHG_NONE
+                   : P.repl ? KKM_XCHG_S_ALLREDUCE
+                   : (P.sym || P.ssym) ? KKM_XCHG_S_REDUCE_SCATTER : KKM_XCHG_PARTIALS;
+  info->grid_rows = P.pr;
+  info->grid_cols = P.pc;
+  info->row0 = P.row0;
+  info->nloc = P.nloc;
+  info->a0 = P.a0;
+  info->nA = P.nA;
+  info->b0 = P.b0;
+  info->nB = P.nB;
+  info->ws_bytes = (int64_t)P.total;
+  std::vector<int64_t> r;
+  auto add = [&](int64_t r0, int64_t nr, int64_t c0, int64_t nc, int64_t cd) {
+    nr = std::min(nr, n - r0);
+    nc = std::min(nc, n - c0);
+    if (nr <= 0 || nc <= 0) return;
+    r.insert(r.end(), {r0, nr, c0, nc, std::min(cd, n)});
+  };
+  if (P.sym) {
+    for (const SymBand &b : P.bands) {
+      const int64_t j0 = (int64_t)b.band * SYM_TB;
+      add(j0 + b.row0, b.rows, j0, n - j0, j0 + SYM_TB);
+    }
+  } else if (P.ssym) {
+    for (const int4 &u : P.units) add((int64_t)u.x * 256, 256, (int64_t)u.y * 256, (int64_t)u.z * 256,
+                                      u.x == u.y ? (int64_t)(u.y + 1) * 256 : (int64_t)u.y * 256);
+  } else {
+    add(P.a0, P.nA, P.b0, P.nB, n);
+  }
+  info->npieces = (int64_t)(r.size() / 5);
+  if (pieces)
+    std::memcpy(pieces, r.data(), (size_t)std::min<int64_t>(cap, info->npieces) * 5 * sizeof(int64_t));
   return KKM_OK;
 }
 
@@ -1265,6 +1296,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->bcount = (int32_t *)(w + P.o_bcount);
     h->boff = (int32_t *)(w + P.o_boff);
   }
+  h->fxmax = (float *)(w + P.o_fxmax);
   if (P.materialize && P.spmm_v2) h->codes = (uint32_t *)(w + P.o_codes);
   if (P.pr > 1) {
     h->labB = (int32_t *)(w + P.o_labB);
@@ -1274,6 +1306,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   if (P.inc) {
     h->Sinc = (double *)(w + P.o_Sinc);
     h->Sd = (double *)(w + P.o_Sd);
+    h->Sdx = (long long *)(w + P.o_Sdx);
     h->dkey = (int32_t *)(w + P.o_dkey);
     h->dset = SortedSet{(uint16_t *)(w + P.o_Dhi), (uint16_t *)(w + P.o_Dlo), (float *)(w + P.o_Dn),
                         (float *)(w + P.o_Dr),      (int32_t *)(w + P.o_dperm), (int32_t *)(w + P.o_dpos),
@@ -1286,7 +1319,6 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
       h->Sorig = (long long *)(w + P.o_Sorig);
       h->Sfmine = (long long *)(w + P.o_Sfmine);
     }
-    h->fxmax = (float *)(w + P.o_fxmax);
   }
   if (P.sym) {
     h->perm_b = (int32_t *)(w + P.o_perm_b);
@@ -1306,12 +1338,11 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         h->tSint = (long long *)(w + P.o_tSint);
         h->tSmine = (long long *)(w + P.o_tSmine);
       }
-      h->fxmax = (float *)(w + P.o_fxmax);
     }
     h->gfirst = (int32_t *)(w + P.o_gfirst);
     h->Sfin = (double *)(w + P.o_Sfin);
   }
-  h->ssym_v1 = std::getenv("KKM_SSYM_V1") && std::atoi(std::getenv("KKM_SSYM_V1")) == 1 && P.k <= 16;
+  if (const char *e = std::getenv("KKM_CHAIN_KB")) h->chain_kb = std::max(0, std::atoi(e));
   h->kp.kind = p->kind;
   h->kp.degree = p->degree;
   h->kp.gamma = (float)p->gamma;
@@ -1351,6 +1382,14 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
           h->Xf, P.ldf, P.n, P.npad, P.d, h->norms, h->Xhi, h->Xlo, P.dp,
           P.tc ? (P.fp16 ? 2 : 1) : 0, h->rscale);
       CKL();
+      // Gaussian: the norms of r^2 = n_i + n_j - 2 b become the tensor core's own x_i . x_i, so the
+      // one-signed accumulation error of b and of the norms cancels for like terms (DESIGN A9)
+      if (p->kind == KKM_KERNEL_GAUSSIAN && P.tc &&
+          tc3_self_dots(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, h->norms, h->st, &h->launches,
+                        h->chain_kb)) {
+        h->poisoned = true;
+        return fail(KKM_ECUDA, "tensor-core self dots failed: %s", tc_gemm_error());
+      }
       if (P.a_n > 0) {
         diag_kernel<<<(unsigned)ceil_div(P.a_n, wpb), wpb * 32, 0, h->st>>>(
             h->Xf, P.ldf, P.d, P.a_row0, P.a_n, p->kind, p->gamma, p->coef0, p->degree, h->diag);
@@ -1383,9 +1422,9 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     if (!evs.record(h->st)) return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
     // ---- a1: K tile [A set, B set] = kappa(X X^T), materialised once; with
     // symmetric storage (f1) the owned upper-triangle bands, one launch each
-    if (P.ssym) {  // units, and the fixed-point scale 2^s with n * max|K| * 2^s < 2^61
-      if (!P.units.empty())
-        CK(cudaMemcpyAsync(h->units, P.units.data(), P.units.size() * sizeof(int4), cudaMemcpyHostToDevice, h->st));
+    if (P.ssym && !P.units.empty())
+      CK(cudaMemcpyAsync(h->units, P.units.data(), P.units.size() * sizeof(int4), cudaMemcpyHostToDevice, h->st));
+    if (P.tc) {  // the fixed-point scale 2^s of the streaming kernels' S (loop, f3 deltas): n max|K| 2^s < 2^61
       max_norm_kernel<<<1, 1024, 0, h->st>>>(h->norms, P.n, h->fxmax);
       CKL();
       float mx = 0.f;
@@ -1455,7 +1494,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
           items += (int64_t)g.tiles_m * g.tiles_n;
           for (int pl = 0; pl < planes; ++pl) {
             void *out = P.kh ? (void *)((__half *)h->K + pl * P.kelems + b.koff) : (void *)(h->K + b.koff);
-            if (tc_encode_out_map(&maps[r * planes + pl], out, b.rows, b.ldb, b.ldb, P.kh))
+            if (tc3_encode_out_map(&maps[r * planes + pl], out, b.rows, b.ldb, b.ldb, P.kh))
               return fail(KKM_ECUDA, "%s", tc_gemm_error());
           }
         }
@@ -1463,9 +1502,9 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         CUtensorMap *gmaps = (CUtensorMap *)((uint8_t *)h->ws + P.o_gmaps);
         CK(cudaMemcpyAsync(gregs, regs.data(), regs.size() * sizeof(T2Region), cudaMemcpyHostToDevice, h->st));
         CK(cudaMemcpyAsync(gmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
-        if (tc2_gemm_launch_multi(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, gregs,
+        if (tc3_gemm_launch_multi(h->tc, h->Xhi, h->Xlo, P.fp16, h->rscale, P.npad, P.dp, P.n, gregs,
                                   (int)regs.size(), items, gmaps, h->norms, h->kp, P.kh ? h->kscale : 0.f, planes,
-                                  h->st, &h->launches)) {
+                                  h->st, &h->launches, h->chain_kb)) {
           h->poisoned = true;
           return fail(KKM_ECUDA, "tcgen05 GEMM launch failed: %s", tc_gemm_error());
         }
@@ -1706,9 +1745,10 @@ namespace {
 // only: streaming handles lend their own), the partials and the outputs.
 struct PredictPlan {
   int64_t mpad;
-  int nsplit, nblk;
+  int splits, nblk;
   bool own_sorted;
-  size_t oYf, oYhi, oYlo, oYn, oYr, oYd, oSp, oLab, oD, oPerm, oPos, oSeg, oBc, oBo, oShi, oSlo, oSn, oSr, total;
+  size_t oYf, oYhi, oYlo, oYn, oYr, oYd, oSp, oSx, oFx, oLab, oD, oPerm, oPos, oSeg, oBc, oBo, oShi, oSlo, oSn, oSr,
+      total;
 };
 
 PredictPlan predict_plan(const kkm_ctx *h, int64_t m) {
@@ -1717,8 +1757,7 @@ PredictPlan predict_plan(const kkm_ctx *h, int64_t m) {
   q.mpad = round_up(std::max<int64_t>(m, 1), 256);
   q.nblk = (int)ceil_div(P.n, SORT_BLOCK);
   const int64_t tiles_n = ceil_div(P.n, 256);
-  q.nsplit = 2 * (int)std::max<int64_t>(ceil_div(tiles_n, 512),
-                                        ts_choose_splits((m + 1) / 2, P.n, h->num_sms / 2));
+  q.splits = (int)std::max<int64_t>(ceil_div(tiles_n, 512), ts_choose_splits((m + 1) / 2, P.n, h->num_sms / 2));
   q.own_sorted = P.materialize;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -1733,7 +1772,9 @@ PredictPlan predict_plan(const kkm_ctx *h, int64_t m) {
   q.oYn = take((size_t)q.mpad * 4);
   q.oYr = take((size_t)q.mpad * 4);
   q.oYd = take((size_t)q.mpad * 8);
-  q.oSp = take((size_t)q.nsplit * q.mpad * k * 8);
+  q.oSp = take((size_t)q.mpad * k * 8);
+  q.oSx = take((size_t)q.mpad * k * 8);
+  q.oFx = take(16);
   q.oLab = take((size_t)q.mpad * 4);
   q.oD = take((size_t)q.mpad * k * 8);
   q.oPerm = take((size_t)P.lablen * 4);
@@ -1772,6 +1813,13 @@ int predict_run(kkm_ctx *h, const PredictPlan &q, uint8_t *t, const float *Y, in
   prep_rows_kernel<<<(unsigned)ceil_div(q.mpad, 8), 256, 0, h->st>>>(Yf, P.ldf, m, q.mpad, P.d, yn, Yhi, Ylo, P.dp,
                                                                      P.fp16 ? 2 : 1, yr);
   CKL();
+  if (h->p.kind == KKM_KERNEL_GAUSSIAN) {  // the tensor core's own y . y, as the training norms (kkm_init)
+    TcGemm gy;
+    if (tc3_self_dots(gy, Yhi, Ylo, P.fp16, yr, q.mpad, P.dp, m, yn, h->st, &h->launches, h->chain_kb)) {
+      h->poisoned = true;
+      return fail(KKM_ECUDA, "tensor-core self dots failed: %s", tc_gemm_error());
+    }
+  }
   diag_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, h->st>>>(Yf, P.ldf, P.d, 0, m, h->p.kind, h->p.gamma, h->p.coef0,
                                                             h->p.degree, yd);
   CKL();
@@ -1779,8 +1827,24 @@ int predict_run(kkm_ctx *h, const PredictPlan &q, uint8_t *t, const float *Y, in
   CKR(sort_gather(h, h->lab[h->cur], 0, P.n, P.npad, B));
   TcStream &ts = h->ts_predict;
   const StreamA A{Yhi, Ylo, yn, yr, q.mpad, 0, m, q.mpad};
-  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, 0, q.nsplit, Sp));
-  predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, q.nsplit, m, q.mpad, k, h->sizes[h->cur],
+  // fixed-point scale of the streaming sums: n max|K(y, x)| 2^s < 2^61, |K(y, x)| <= max(K(y, y), K(x, x))
+  double kmax = 1.0;
+  if (h->p.kind != KKM_KERNEL_GAUSSIAN) {
+    float *fm = (float *)(t + q.oFx);
+    max_norm_kernel<<<1, 1024, 0, h->st>>>(h->norms, P.n, fm);
+    CKL();
+    max_norm_kernel<<<1, 1024, 0, h->st>>>(yn, m, fm + 1);
+    CKL();
+    float mx[2] = {0.f, 0.f};
+    CK(cudaMemcpyAsync(mx, fm, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    const double nm = std::max((double)mx[0], (double)mx[1]);
+    kmax = h->p.kind == KKM_KERNEL_LINEAR ? std::max(1e-30, nm)
+                                          : std::pow(h->p.gamma * nm + std::fabs(h->p.coef0), (double)h->p.degree);
+  }
+  const double fx = std::ldexp(1.0, (int)std::floor(61.0 - std::log2(std::max(1e-300, (double)P.n * kmax * 1.0001))));
+  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, 0, q.splits, fx, (long long *)(t + q.oSx), Sp));
+  predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, 1, m, q.mpad, k, h->sizes[h->cur],
                                                                 h->cnorm2, yd, ylab, Dy);
   CKL();
   CKR(copy_any(h, labels_out, ylab, (size_t)m * 4));

@@ -12,7 +12,7 @@
 // same bytes, two descriptors. The 0/1 B operands (N = 16 labels) are built in shared memory from
 // the labels. Accumulators live in TMEM (fp32); no per-element instruction touches K, so the
 // kernel is a pure HBM stream (hi + lo: the fp32 band bytes at ~0.97 of the copy peak; FP16:
-// half of them). Both planes of a tile are fed as two stages into the same accumulators.
+// half of them). Both planes of a tile are fed as two stages into the same accumulators, lo first.
 //
 // Work unit = (owned band piece, 512-row slab = 4 row tiles, split of <= 8 or 16 chunks of 128 columns).
 // Per chunk and row tile the row MMAs go to D_row[tile] and the column MMAs to D_col (skipped on
@@ -270,8 +270,11 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
               uint8_t *st = s.stages + stage * TS_TILE_BYTES;
               mbar_arrive_expect_tx(&s.full[stage], TS_TILE_BYTES);
               const int row = r0 + t * TS_ROWS;
-              ts_tma_load(st, map + pl, q * TS_CH, row, &s.full[stage]);
-              ts_tma_load(st + TS_TILE_BYTES / 2, map + pl, q * TS_CH + 64, row, &s.full[stage]);
+              // the lo plane first: its small sums reach the accumulator while the running sum is
+              // still small, so only the hi plane's MMAs add truncation error relative to S (A9)
+              const CUtensorMap *pm = map + (planes - 1 - pl);
+              ts_tma_load(st, pm, q * TS_CH, row, &s.full[stage]);
+              ts_tma_load(st + TS_TILE_BYTES / 2, pm, q * TS_CH + 64, row, &s.full[stage]);
               if (++stage == TS_STAGES) {
                 stage = 0;
                 sphase ^= 1u;

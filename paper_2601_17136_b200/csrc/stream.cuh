@@ -1,26 +1,10 @@
-// stream.cuh -- host side and helpers of the fused streaming a1+a2 (K never stored; the
-// kernel is tc2_stream_kernel in tc2.cuh): for the rank's rows i and all points j
-// in cluster-sorted order p (sort.cuh), S(i, c) = sum_{p in segment c} kappa(x_i . x_perm[p])
-// (Eqs. b, k, e), the paper's sliding-window recompute done tile by tile
-// in TMEM instead of b x n block rows in HBM.
-//
-// Work unit = one 256-row CTA-pair tile x one split of the sorted column range; the epilogue warps (thread = row, 8 warps = 4 lane
-// quarters x 2 column halves) apply kappa to each 32-column chunk and add its sum into the row's
-// per-cluster fp64 accumulator. Chunks lie inside one cluster except at the <= k-1 segment
-// boundaries, which are handled by a warp-uniform per-segment split, so the reduction costs
-// ~1 FADD per element. Partials go to Spart[2*split + half][row][c], reduced in fixed order by
-// finalize_kernel exactly like the materialised SpMM's output.
+// stream.cuh -- host side of the fused streaming a1+a2 (K never stored; the kernels are
+// tc3_stream_kernel in tc3.cuh and ssym_kernel in ssym.cuh): operand tensor maps of the A set and
+// of the label-sorted B set (sort.cuh), and the choice of column splits per row tile.
 #pragma once
 #include "gemm_tc.cuh"
 
 namespace kkm {
-
-template <int KMAX>
-__device__ __forceinline__ void acc_add(double (&acc)[KMAX], int c, double s) {
-#pragma unroll
-  for (int cc = 0; cc < KMAX; ++cc)
-    if (cc == c) acc[cc] += s;
-}
 
 // ---------------------------------------------------------------- host side
 struct TcStream {

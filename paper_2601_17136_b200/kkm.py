@@ -29,6 +29,18 @@ class KKMError(RuntimeError):
         self.code = code
 
 
+LAYOUT_FULL, LAYOUT_STREAM, LAYOUT_SYM_BANDS, LAYOUT_SYM_BANDS16, LAYOUT_SYM_STREAM = range(5)
+XCHG_NONE, XCHG_PARTIALS, XCHG_S_ALLREDUCE, XCHG_S_REDUCE_SCATTER = range(4)
+
+
+class KKMPlanInfo(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("layout", ctypes.c_int32), ("exchange", ctypes.c_int32),
+                ("grid_rows", ctypes.c_int32), ("grid_cols", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("row0", ctypes.c_int64), ("nloc", ctypes.c_int64), ("a0", ctypes.c_int64), ("nA", ctypes.c_int64),
+                ("b0", ctypes.c_int64), ("nB", ctypes.c_int64), ("npieces", ctypes.c_int64),
+                ("ws_bytes", ctypes.c_int64)]
+
+
 class KKMParams(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("gamma", ctypes.c_double), ("coef0", ctypes.c_double),
                 ("degree", ctypes.c_int32), ("k", ctypes.c_int32), ("max_iter", ctypes.c_int32),
@@ -59,6 +71,7 @@ def lib():
         sig = {
             "kkm_default_params": [P],
             "kkm_workspace_size": [P, i64, i64, i32, i32, P],
+            "kkm_plan_query": [P, i64, i64, i32, i32, P, P, i64],
             "kkm_init": [P, P, P, i64, i64, i64, i32, i32, P, P, ctypes.c_size_t, P, P],
             "kkm_fit": [P, P, P, P],
             "kkm_assign": [P, P],
@@ -108,6 +121,16 @@ def workspace_size(p: KKMParams, n: int, d: int, rank: int = 0, nranks: int = 1)
     b = ctypes.c_size_t(0)
     _check(lib().kkm_workspace_size(ctypes.byref(p), n, d, rank, nranks, ctypes.byref(b)))
     return int(b.value)
+
+
+def plan_query(p: KKMParams, n: int, d: int, rank: int = 0, nranks: int = 1):
+    """(info, pieces int64[npieces, 5]) of the C++ planner for one rank (pure host code, no CUDA)."""
+    info = KKMPlanInfo()
+    _check(lib().kkm_plan_query(ctypes.byref(p), n, d, rank, nranks, ctypes.byref(info), None, 0))
+    pieces = np.zeros((max(int(info.npieces), 1), 5), dtype=np.int64)
+    _check(lib().kkm_plan_query(ctypes.byref(p), n, d, rank, nranks, ctypes.byref(info),
+                                pieces.ctypes.data_as(ctypes.c_void_p), int(info.npieces)))
+    return info, pieces[:int(info.npieces)]
 
 
 def get_unique_id() -> bytes:

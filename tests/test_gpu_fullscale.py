@@ -148,4 +148,5 @@ def test_full_size_objective_at_convergence(name, iters):
     h.destroy()
     Jref = oracle.objective_X(X, lab, k, *args)
     diag = oracle.kernel_diag(X, *args)
+    print(f"\n{name}: J {J:.12e} oracle {Jref:.12e} rel {(J - Jref) / abs(Jref):+.3e}")
     assert abs(J - Jref) <= j_tol(Jref, diag), (J, Jref, abs(J - Jref) / abs(Jref))

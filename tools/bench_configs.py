@@ -25,6 +25,7 @@ ap.add_argument("--iters", type=int, default=0, help="override iterations (0 = c
 ap.add_argument("--points", "--n", dest="n", type=int, default=0, help="override n (labelled in the output)")
 ap.add_argument("--grid-rows", type=int, default=1)
 ap.add_argument("--path", default="auto", choices=["auto", "mat", "stream"])
+ap.add_argument("--symmetric", default="auto", choices=["auto", "off", "on"])
 ap.add_argument("--kstore", default="auto", choices=["auto", "fp32", "fp16", "fp16x2"],
                 help="materialised band storage (f4: fp16 = low-precision storage)")
 a = ap.parse_args()
@@ -75,6 +76,7 @@ for name in a.configs.split(","):
     h = kkm.KernelKMeans(Xd, n, cfg["k"], cfg["kind"], gamma, cfg.get("coef0", 0.0),
                          cfg.get("degree", 1), max_iter=iters, rank=rank, nranks=world, comm=comm,
                          timing=True, path=path, grid_rows=a.grid_rows,
+                         symmetric={"auto": kkm.SYM_AUTO, "off": kkm.SYM_OFF, "on": kkm.SYM_ON}[a.symmetric],
                          kstore={"auto": kkm.KSTORE_AUTO, "fp32": kkm.KSTORE_FP32, "fp16": kkm.KSTORE_FP16,
                                  "fp16x2": kkm.KSTORE_FP16X2}[a.kstore])
     e1.record()
