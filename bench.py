@@ -390,7 +390,10 @@ def run_ours(args):
             s1.record(stream)
             barrier()
         ph1 = hs.phase_ms()
-        s_ms = s0.elapsed_time(s1) / args.stream_iters
+        # sec/iteration of the loop (phase timers: a2 + a3 + a4 of the timed iterations; the fit's extra
+        # objective pass for the final labels is outside, as in the metric's line)
+        s_ms = sum(ph1[key] - ph0[key] for key in ("spmm", "cnorm", "assign")) / args.stream_iters
+        fit_ms = s0.elapsed_time(s1)
         a2k = (ph1["a2_kernel"] - ph0["a2_kernel"]) / args.stream_iters
         T = -(-sn // 256)
         exec_flops = 2.0 * 784 * 256 * 256 * T * (T + 1) / 2  # the upper-triangle tiles the kernel computes
@@ -398,6 +401,7 @@ def run_ours(args):
         stream_info = {"workload": "mnist1m: BASELINE.json configs[3] recipe, n=1000000 d=784 k=10 Gaussian "
                                    "(median gamma), K streamed (never stored), 1 GPU",
                        "value": s_ms / 1e3, "unit": "s/iteration", "iterations_timed": args.stream_iters,
+                       "fit_s": fit_ms / 1e3,
                        "kernel": "ssym_kernel (upper triangle of the label-sorted K, chained fp16x3 tcgen05)",
                        "kernel_ms": a2k,
                        "roofline": {"bound": "tensor", "unit": "TFLOP/s",

@@ -1,0 +1,154 @@
+// api_ctx.cuh -- the handle (kkm_ctx) of kkm_api.cu, the status macros and small helpers.
+#pragma once
+
+// CUDA events owned for one scope (destroyed on every exit path, errors included).
+struct EventList {
+  std::vector<cudaEvent_t> v;
+  EventList() = default;
+  EventList(const EventList &) = delete;
+  EventList &operator=(const EventList &) = delete;
+  ~EventList() { clear(); }
+  void clear() {
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
+    v.clear();
+  }
+  // creates and records one event; false if the runtime refused
+  bool record(cudaStream_t st) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return false;
+    v.push_back(e);
+    return cudaEventRecord(e, st) == cudaSuccess;
+  }
+};
+
+// Label-sorted copy of a point set (the B operand of the streaming kernel) and its sort.
+struct SortedSet {
+  uint16_t *hi, *lo;
+  float *norms, *rscale;
+  int32_t *perm, *pos, *seg, *bcount, *boff;
+};
+
+struct kkm_ctx {
+  kkm_params p;
+  Plan P;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  uint8_t *ws = nullptr;
+  float *Xf = nullptr, *norms = nullptr, *K = nullptr;
+  float *mean = nullptr;  // Gaussian: the column means X was centered on (0 otherwise)
+  uint16_t *Xhi = nullptr, *Xlo = nullptr;  // bf16 or fp16 split of X (P.tc)
+  float *rscale = nullptr;                   // 1 / s_i of the fp16 split
+  double *diag, *Spart, *E, *blockpart, *rankpart, *cnorm, *J, *Dfull;
+  double *E2, *cnorm2;  // E / c of the final-labels pass (kept apart from the last iteration's)
+  // streaming path: cluster-sorted operands and the sort
+  uint16_t *Shi = nullptr, *Slo = nullptr;
+  float *snorms = nullptr, *srscale = nullptr;
+  int32_t *perm = nullptr, *pos = nullptr, *seg = nullptr, *bcount = nullptr, *boff = nullptr;
+  TcStream ts, ts_predict;  // tensor maps of the clustering loop / of kkm_predict
+  // 1.5D: padded labels of the B set, column-block partials, own-block sums; column comm
+  int32_t *labB = nullptr;
+  double *Scol = nullptr, *Smine = nullptr;
+  uint32_t *codes = nullptr;  // SpMM v2 per-iteration group codes
+  // f1 symmetric storage
+  int32_t *perm_b = nullptr, *ngroups = nullptr, *band_desc = nullptr, *gfirst = nullptr;
+  SymGroup *groups = nullptr;
+  SymBand *bands = nullptr;
+  float *colpart = nullptr;
+  double *colsum = nullptr, *Sfin = nullptr;
+  int32_t *work = nullptr;  // spmm_sym's item scheduler (2 counters, zero between launches)
+  unsigned *a3ctr = nullptr;  // finalize's last-block counter (zero between launches)
+  // peer-memory exchange of S (16-bit bands, replicated a3, several ranks): own IPC buffer
+  // [2 epochs][k][npad] int64 + flag + peer table; peers' buffers mapped with cudaIpcOpenMemHandle
+  bool p2p = false;
+  uint8_t *xbuf = nullptr;
+  std::vector<void *> xpeers;  // opened peer mappings (closed in destroy)
+  const uint8_t **xtable = nullptr;  // device [nranks] bases (inside xbuf)
+  size_t xflag_off = 0;              // byte offset of the epoch flag in every exchange buffer
+                                     // (+64: this rank's timed-out word, checked by check_p2p)
+  unsigned long long epoch = 0;
+  unsigned long long p2p_timeout_ns = 0;
+  // f4 fp16 K storage
+  CUtensorMap *tmaps = nullptr;
+  TsBand *tbands = nullptr;
+  TsUnit *tunits = nullptr;
+  long long *tSfix = nullptr, *tSint = nullptr, *tSmine = nullptr;
+  float kscale = 1.f;  // stored K = K * kscale (a power of two)
+  double tfxm = 1.0, tfx_inv = 1.0;  // S fixed point: drained (scaled) sums x tfxm; back x tfx_inv
+  // f1 streaming: units, int64 fixed-point S (sorted order), its original-order copy
+  int4 *units = nullptr;
+  long long *Sfix = nullptr, *Sorig = nullptr, *Sfmine = nullptr;
+  float *fxmax = nullptr;
+  double fx_scale = 1.0, fx_inv = 1.0;
+  // f3 incremental S
+  double *Sinc = nullptr, *Sd = nullptr;
+  long long *Sdx = nullptr;
+  int32_t *dkey = nullptr;
+  SortedSet dset{};
+  bool s_valid = false;  // Sinc holds S of the current labels
+  TcStream ts_delta;
+  ncclComm_t colcomm = nullptr;
+  int32_t *lab[2], *sizes[2];
+  unsigned long long *changed;
+  int *bad;
+  int cur = 0;  // labels[cur] / sizes[cur] are the labels entering the next iteration
+  bool poisoned = false;
+  int chain_kb = 0;      // K-blocks per accumulation chain of every tensor-core kernel (0: CH_CKB; KKM_CHAIN_KB)
+  bool have_last = false;
+  bool cnorm2_valid = false;  // cnorm2 holds c of the current labels (after kkm_fit / kkm_objective)
+  int64_t launches = 0;
+  float phase_ms[KKM_NPHASES] = {0, 0, 0, 0, 0, 0};
+  bool time_a2 = false;             // timing mode, inside the kkm_fit loop
+  EventList a2ev;                   // (start, end) pairs around the dominant a2 kernel
+  KappaParams kp;
+  TcGemm tc;
+};
+
+namespace {
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      h->poisoned = true;                                                                \
+      return fail(KKM_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    }                                                                                    \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    ++h->launches;                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) {                                                             \
+      h->poisoned = true;                                                                \
+      return fail(KKM_ECUDA, "%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+    }                                                                                    \
+  } while (0)
+
+#define CKN(call)                                                                        \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) {                                                             \
+      h->poisoned = true;                                                                \
+      return fail(KKM_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(r_)); \
+    }                                                                                    \
+  } while (0)
+
+#define CKR(expr)        \
+  do {                   \
+    int rc_ = (expr);    \
+    if (rc_) return rc_; \
+  } while (0)
+
+// Brackets the dominant a2 kernel launch(es) with CUDA events (timing mode, kkm_fit loop).
+void a2_mark(kkm_ctx *h) {
+  if (h->time_a2) h->a2ev.record(h->st);
+}
+
+// Host or device pointer copy on the handle's stream.
+int copy_any(kkm_ctx *h, void *dst, const void *src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st));
+  return KKM_OK;
+}
+
+}  // namespace
