@@ -145,6 +145,35 @@ void a2_mark(kkm_ctx *h) {
   if (h->time_a2) h->a2ev.record(h->st);
 }
 
+// Waits for the handle's stream. With a communicator the wait polls the stream and NCCL's
+// asynchronous error state instead of blocking: a failed or aborted peer turns into KKM_ENCCL (handle
+// poisoned; the caller aborts the communicator) rather than a hang, and a collective that has not
+// completed within KKM_NCCL_TIMEOUT_S seconds (default 1800) is reported the same way.
+int sync_stream(kkm_ctx *h) {
+  if (!h->comm) {
+    CK(cudaStreamSynchronize(h->st));
+    return KKM_OK;
+  }
+  double tmo = 1800.0;
+  if (const char *e = std::getenv("KKM_NCCL_TIMEOUT_S")) tmo = std::max(1.0, std::atof(e));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(h->st);
+    if (q == cudaSuccess) return KKM_OK;
+    if (q != cudaErrorNotReady) CK(q);
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(h->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+      h->poisoned = true;
+      return fail(KKM_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ar));
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > tmo) {
+      h->poisoned = true;
+      return fail(KKM_ENCCL, "collective did not complete within %.0f s (KKM_NCCL_TIMEOUT_S)", tmo);
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 // Host or device pointer copy on the handle's stream.
 int copy_any(kkm_ctx *h, void *dst, const void *src, size_t bytes) {
   CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st));

@@ -230,7 +230,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     // block-major (below), so the ~74 pairs running at once sweep the same block of B tiles
     // with different row tiles: the block (BS x 256 rows of the split operand) and the pairs'
     // A tiles stay L2-resident
-    int64_t BS = 32;
+    int64_t BS = 16;  // measured at n = 200k: 8 / 16 / 32 tiles -> 67.2 / 68.1 / 70.4 ms, DRAM 134 vs 205 GB (16 vs 32)
     if (const char *e = std::getenv("KKM_SSYM_BS")) BS = std::max<int64_t>(1, std::atoll(e));
     const bool tile_major = std::getenv("KKM_SSYM_TILE_MAJOR") != nullptr;  // (the round-1 order, A/B only)
     // G > 0: single-tile units in a supertile raster -- G x G patches of the upper triangle, patch

@@ -500,7 +500,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
     unsigned long long c = 1;
     if (h->p.stop_on_no_change || P.inc) {
       CK(cudaMemcpyAsync(&c, h->changed + t, 8, cudaMemcpyDeviceToHost, h->st));
-      CK(cudaStreamSynchronize(h->st));
+      CKR(sync_stream(h));
     }
     if (P.inc) {  // S for the new labels: unchanged, by the moved points, or a full pass next time
       if (c > 0 && (int64_t)c <= P.dmax) {
@@ -538,7 +538,7 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   std::vector<unsigned long long> ch((size_t)std::max(t, 1));
   CK(cudaMemcpyAsync(J.data(), h->J, (size_t)(t + 1) * 8, cudaMemcpyDeviceToHost, h->st));
   if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
+  CKR(sync_stream(h));
   CKR(check_p2p(h));
   if (timing) {
     const std::vector<cudaEvent_t> &e5 = ev.v;
@@ -586,7 +586,7 @@ int kkm_objective(kkm_handle h, double *J) {
   CKR(run_cnorm(h, S, ns, h->P.s_rows_pad, h->E2, h->cnorm2, slot, nullptr, nullptr));
   h->cnorm2_valid = true;
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
+  CKR(sync_stream(h));
   CKR(check_p2p(h));
   return KKM_OK;
 }
