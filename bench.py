@@ -306,7 +306,7 @@ def run_ours(args):
     # ---- informational, not the metric: the same run with f4 fp16 K storage (the bands in fp16,
     # a2 on the tensor cores; each K value rounded to 2^-11 relative, A27 -- below the
     # paper's fp32 precision, so never the headline)
-    kh_ok = precision != kkm.PREC_FP32_SIMT and kw["symmetric"] == kkm.SYM_AUTO and k <= 16
+    kh_ok = precision != kkm.PREC_FP32_SIMT and kw["symmetric"] == kkm.SYM_AUTO and k <= 32
     kh_ms = kh_a2 = kh_a2k = None
     J_kh = None
     if kh_ok:
@@ -435,7 +435,7 @@ def run_ours(args):
         B = -(-n // world)
         nloc = min(B, n - 0)
         ldk = -(-n // 32) * 32
-        sym = args.symmetric == "auto" and k <= 16
+        sym = args.symmetric == "auto" and (k <= 16 or (k <= 32 and args.kstore != "fp32"))
         # the f1 bands as hi + lo fp16 planes with a2 on the tensor cores (KSTORE_AUTO's choice
         # for a tensor-core precision), or fp32 bands with the one-hot FFMA2 kernel
         tc_a2 = sym and args.kstore != "fp32" and precision != kkm.PREC_FP32_SIMT

@@ -119,9 +119,10 @@ typedef struct kkm_params {
   int32_t grid_rows;       /* 1.5D process grid pr x (nranks/pr), column-major ranks
                               (P:604); 0 or 1 = the 1D algorithm (Alg. 1). Must divide
                               nranks. See kkm_init.                                   */
-  int32_t symmetric;       /* f1, 1D runs with k <= 16 only: compute / store only the upper
-                              triangle of K (half the K bytes and GEMM flops when
-                              materialised, half the MMA work when streaming).
+  int32_t symmetric;       /* f1, 1D runs: compute / store only the upper triangle of K (half
+                              the K bytes and GEMM flops when materialised -- k <= 32 with
+                              16-bit band storage, k <= 16 with fp32 bands -- and half the MMA
+                              work when streaming, any k).
                               KKM_SYM_AUTO (0): streaming always; materialised when
                               n >= 8192 (below, the extra kernels cost more than the
                               halved K read saves). KKM_SYM_ON (2): whenever eligible.
@@ -146,10 +147,10 @@ typedef struct kkm_params {
                               KKM_KSTORE_FP16 (2): the hi plane only -- half the bytes, each
                               value rounded to 2^-11 relative (DESIGN A27 bounds E / D / J).
                               KKM_KSTORE_AUTO (0, default): FP16X2 whenever the run stores the
-                              f1 bands with a tensor-core precision (1D, k <= 16; see
+                              f1 bands with a tensor-core precision (1D, k <= 32; see
                               `symmetric`), else FP32.
                               FP16 and FP16X2 need a tensor-core precision and a materialised
-                              1D run with k <= 16 and symmetric != OFF (they imply the f1 bands
+                              1D run with k <= 32 and symmetric != OFF (they imply the f1 bands
                               for any n); else KKM_EUNSUP.                                */
   int32_t reserved[2];     /* must be zero                                         */
 } kkm_params;
@@ -191,7 +192,7 @@ int64_t kkm_shard_begin(int64_t n, int32_t rank, int32_t nranks);
 /* Bytes of device workspace kkm_init needs for this rank (pure; no CUDA).
  * Includes the materialised K block when the effective path is MATERIALIZE: the
  * rank's n_local x ceil32(n) fp32 rows, or with symmetric storage (KKM_SYM_AUTO, 1D,
- * k <= 16) its share of the upper-triangle bands (1024 rows x ceil32(n - 1024 I)
+ * k <= 32 for 16-bit bands) its share of the upper-triangle bands (1024 rows x ceil(n - 1024 I)
  * columns each, bands spread over the ranks by area): ~n^2/(2P) floats. */
 int kkm_workspace_size(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t nranks,
                        size_t *bytes);

@@ -149,7 +149,9 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   const Plan &P = h->P;
   const int k = P.k;
   if (P.kh) {  // f4: 16-bit bands, a2 on the tensor cores (spmm_tc.cuh), S in int64 fixed point
-    CK(ensure_smem_attr((const void *)spmm_tc_kernel, TS_SMEM));
+    const bool nl32 = P.tnl == 32;
+    if (nl32) CK(ensure_smem_attr((const void *)spmm_tc_kernel<32>, TsCfg<32>::SMEM));
+    else CK(ensure_smem_attr((const void *)spmm_tc_kernel<16>, TsCfg<16>::SMEM));
     long long *Sx = h->tSfix;
     if (h->p2p) {  // this epoch's half of the own exchange buffer (the other half may still be read)
       ++h->epoch;
@@ -159,10 +161,21 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
     a2_mark(h);
     if (!P.tunits.empty()) {
       const int grid = (int)std::min<int64_t>((int64_t)P.tunits.size(), h->num_sms);
-      spmm_tc_kernel<<<grid, TS_THREADS, TS_SMEM, h->st>>>(h->tmaps, h->tbands, h->tunits, (int)P.tunits.size(),
-                                                           labels, P.n, k, P.npad, h->tfxm, Sx, h->work,
-                                                           P.kplanes);
+      float *cpart = nl32 ? (float *)(h->ws + P.o_tcolpart) : nullptr;
+      if (nl32)
+        spmm_tc_kernel<32><<<grid, TS_THREADS, TsCfg<32>::SMEM, h->st>>>(
+            h->tmaps, h->tbands, h->tunits, (int)P.tunits.size(), labels, P.n, k, P.npad, h->tfxm, Sx, h->work,
+            P.kplanes, cpart);
+      else
+        spmm_tc_kernel<16><<<grid, TS_THREADS, TsCfg<16>::SMEM, h->st>>>(
+            h->tmaps, h->tbands, h->tunits, (int)P.tunits.size(), labels, P.n, k, P.npad, h->tfxm, Sx, h->work,
+            P.kplanes, cpart);
       CKL();
+      if (nl32 && !P.tslabs.empty()) {  // the column parts, summed over this rank's slabs
+        ts_colpart_reduce_kernel<<<dim3((unsigned)ceil_div(P.n, 256), (unsigned)k), 256, 0, h->st>>>(
+            cpart, (const TsSlab *)(h->ws + P.o_tslabs), (int)P.tslabs.size(), P.n, k, P.npad, h->tfxm, Sx);
+        CKL();
+      }
     }
     a2_mark(h);
     if (h->p2p) {  // publish; run_cnorm's finalize sums the ranks' S over NVLink

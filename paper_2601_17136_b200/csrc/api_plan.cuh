@@ -61,12 +61,15 @@ struct Plan {
   int ts_nsm;                       // max column splits of a band (informational)
   std::vector<TsBand> tbands;       // owned bands (same order as bands)
   std::vector<TsUnit> tunits;
+  int tnl = 16;                     // labels per spmm_tc launch: 16 (k <= 16) or 32 (k <= 32)
+  std::vector<TsSlab> tslabs;       // NL = 32: this rank's slabs with column partials, by colstart
+  int64_t tcolpart_floats = 0;
   std::vector<int4> units;          // its work units on this rank
   // offsets (bytes) into the workspace
   size_t o_Xf, o_Xhi, o_Xlo, o_norms, o_diag, o_K, o_lab[2], o_sizes[2], o_Spart, o_E,
       o_blockpart, o_rankpart, o_cnorm, o_J, o_changed, o_Dfull, o_bad, o_E2, o_cnorm2, o_rscale,
       o_Shi, o_Slo, o_snorms, o_srscale, o_perm, o_pos, o_seg, o_bcount, o_boff, o_labB, o_Scol, o_Smine,
-      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_gregs, o_gmaps, o_a3ctr, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
+      o_codes, o_perm_b, o_groups, o_ngroups, o_bands, o_band_desc, o_colpart, o_colsum, o_work, o_gfirst, o_tmaps, o_tbands, o_tunits, o_tSfix, o_tSint, o_tSmine, o_tcolpart, o_tslabs, o_gregs, o_gmaps, o_a3ctr, o_Sfin, o_units, o_Sfix, o_Sorig, o_Sfmine, o_fxmax, o_Sinc, o_dkey, o_dperm, o_dpos, o_dseg, o_dbc, o_dbo,
       o_Dhi, o_Dlo, o_Dn, o_Dr, o_Sd, o_Sdx, o_Sx, o_mean, o_cmpart, total;
 };
 
@@ -123,10 +126,11 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   P.fp16 = p->precision == KKM_PREC_FP16X3;
   // f1: symmetric band storage (1D, k <= 16). Bands go to ranks largest first, each to the
   // least-loaded rank (lowest rank on ties): deterministic, area-balanced.
-  const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= SP_KPMAX;
   const bool ssym_elig = p->symmetric != KKM_SYM_OFF && pr == 1;  // streaming f1: any k (ssym.cuh)
   P.kh = p->kstore == KKM_KSTORE_FP16 || p->kstore == KKM_KSTORE_FP16X2;  // AUTO: decided below
   const bool kh_pitch = P.kh || (p->kstore == KKM_KSTORE_AUTO && P.tc);  // the bands if stored are 16-bit
+  // materialised f1 bands: fp32 bands (sym.cuh) for k <= 16, 16-bit planes (spmm_tc.cuh) for k <= 32
+  const bool sym_elig = p->symmetric != KKM_SYM_OFF && pr == 1 && P.k <= (kh_pitch ? TS_MAX_K : SP_KPMAX);
   P.kplanes = p->kstore == KKM_KSTORE_FP16 ? 1 : 2;
   const bool sym_ok = sym_elig && (p->symmetric == KKM_SYM_ON || P.kh || n >= 8 * SYM_TB);
   double kbytes = (double)P.nApad * (double)P.ldk * 4.0;
@@ -186,7 +190,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
   if (p->kstore == KKM_KSTORE_AUTO && P.materialize && sym_ok && P.tc) P.kh = true;
   if (P.kh && !(P.materialize && sym_ok && P.tc))
     return fail(KKM_EUNSUP, "16-bit K storage needs a tensor-core precision and the materialised f1 bands "
-                            "(1D, k <= 16, symmetric != OFF)");
+                            "(1D, k <= 32, symmetric != OFF)");
   // v1 (one-hot FFMA2) is faster for k <= 16 (5.4 TB/s at k = 10); v2 (sorted groups, shuffle
   // bound at ~3.9 TB/s for any k) replaces v1's ceil(k/16) passes over K for 16 < k <= 64.
   P.spmm_v2 = P.k > SP_KPMAX && P.k <= SG_MAX_K;
@@ -309,10 +313,14 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     for (const SymBand &sb : P.bands)
       cslabs += ceil_div(sb.rows, TS_SLAB_TILES * TS_ROWS) * ceil_div(sb.ldb, TS_CH);
     const int split = cslabs / 16 >= 32 * 148 ? 16 : 8;
+    P.tnl = P.k <= 16 ? 16 : 32;
+    P.tslabs.clear();
+    int64_t cpoff = 0;  // NL = 32: the slabs' column partials [slab][NL][ldb - TB]
     for (size_t b = 0; b < P.bands.size(); ++b) {
       const SymBand &sb = P.bands[b];
       TsBand t;
       t.koff = sb.koff;
+      t.cpoff = cpoff;
       t.band = sb.band;
       t.row0 = sb.row0;
       t.ldb = sb.ldb;
@@ -325,7 +333,16 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
         for (int sp = 0; sp < t.nsplit; ++sp)
           P.tunits.push_back(TsUnit{(int32_t)b, sl, sp * split, std::min(split, nchunks - sp * split)});
       P.tbands.push_back(t);
+      const int64_t w = std::max<int64_t>(0, (int64_t)t.ldb - SYM_TB);
+      if (P.tnl == 32 && w > 0)
+        for (int sl = 0; sl < slabs; ++sl) {
+          P.tslabs.push_back(TsSlab{(int64_t)(t.band + 1) * SYM_TB, w, cpoff + (int64_t)sl * P.tnl * w});
+        }
+      if (P.tnl == 32) cpoff += (int64_t)slabs * P.tnl * w;
     }
+    std::stable_sort(P.tslabs.begin(), P.tslabs.end(),
+                     [](const TsSlab &x, const TsSlab &y) { return x.colstart < y.colstart; });
+    P.tcolpart_floats = cpoff;
   }
   if (P.sym) {  // S partials over all rows (owned bands lie anywhere)
     P.nApad = P.npad;
@@ -461,6 +478,10 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_tSfix = take((size_t)P.npad * P.k * 8);  // int64 fixed-point S, [label][row]
     P.o_tSint = P.nranks > 1 ? take((size_t)P.npad * P.k * 8) : 0;
     P.o_tSmine = P.nranks > 1 ? take((size_t)P.B * P.k * 8) : 0;
+    if (P.tnl == 32) {
+      P.o_tcolpart = take((size_t)std::max<int64_t>(P.tcolpart_floats, 1) * 4);
+      P.o_tslabs = take(std::max<size_t>(P.tslabs.size(), 1) * sizeof(TsSlab));
+    }
   }
   P.o_a3ctr = take(16);
   P.o_fxmax = take(16);

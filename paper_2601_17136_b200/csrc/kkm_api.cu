@@ -359,6 +359,9 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         if (!P.tunits.empty())
           CK(cudaMemcpyAsync(h->tunits, P.tunits.data(), P.tunits.size() * sizeof(TsUnit), cudaMemcpyHostToDevice,
                              h->st));
+        if (!P.tslabs.empty())
+          CK(cudaMemcpyAsync(h->ws + P.o_tslabs, P.tslabs.data(), P.tslabs.size() * sizeof(TsSlab),
+                             cudaMemcpyHostToDevice, h->st));
         CK(cudaStreamSynchronize(h->st));  // (host vectors go out of scope)
       }
       if (P.tc && !P.bands.empty()) {  // all owned pieces in one tcgen05 launch
@@ -431,7 +434,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   // every rank reads all (P - 1) peers' whole S, so it is limited to P <= KKM_P2P_MAX_RANKS (4).
   // The decision is agreed by all ranks (an allreduce of the local wish) before the collective
   // setup, so ranks with different environments cannot issue mismatched collectives.
-  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1) {
+  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1 && P.k <= 16) {  // (finalize's peer reads: k <= 16)
     int p2p_max = 4;
     if (const char *e = std::getenv("KKM_P2P_MAX_RANKS")) p2p_max = std::atoi(e);
     const char *want_env = std::getenv("KKM_P2P");

@@ -29,6 +29,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "gemm_tc.cuh"
 
 namespace kkm {
@@ -40,17 +42,27 @@ constexpr int TS_TB = 1024;            // band height (rows) = SYM_TB
 constexpr int TS_ROWS = 128;           // row tile
 constexpr int TS_CH = 128;             // chunk columns
 constexpr int TS_SLAB_TILES = 4;       // row tiles per unit (512 rows)
-constexpr int TS_STAGES = 5;
 constexpr uint32_t TS_TILE_BYTES = TS_ROWS * TS_CH * 2;  // 32 KB: 2 column halves x [128 rows x 128 B]
-constexpr uint32_t TS_OH_BYTES = 16 * 128 * 2;           // one-hot: 2 halves x [16 labels x 128 B]
 constexpr int TS_THREADS = 7 * 32;
 constexpr int TS_COL_WARP = 6;     // the column-sum MMA issuer
 constexpr int TS_DR_BUF = 3;       // D_row buffers (chunks in flight between the MMA and the drains)
 constexpr int TS_DC_BUF = 4;       // D_col buffers (tiles in flight)
-constexpr int TS_TMEM_COLS = 256;  // D_row 3 x (4 tiles x 16) + D_col 4 x 16
+constexpr int TS_MAX_K = 32;       // labels of one launch: NL = 16 (k <= 16) or 32 (k <= 32)
+
+// Per label count NL: one-hot operand bytes (2 halves x [NL labels x 128 B]), stage ring depth (the
+// one-hots of a unit grow with NL), TMEM columns (D_row 3 x (4 tiles x NL) + D_col 4 x NL).
+template <int NL>
+struct TsCfg {
+  static constexpr uint32_t OH_BYTES = NL * 128 * 2;
+  static constexpr int STAGES = NL == 16 ? 5 : 4;
+  static constexpr int TMEM_COLS = NL == 16 ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * TS_TILE_BYTES + 2 * OH_BYTES +
+                                 2 * TS_SLAB_TILES * OH_BYTES + 512;  // + barriers, units, TMEM slot
+};
 
 struct TsBand {    // a stored piece of band I: rows [I TB + row0, + rows) x columns [I TB, + ldb)
   int64_t koff;    // element offset of the piece in the fp16 K buffer (per plane)
+  int64_t cpoff;   // NL = 32: float offset of its slabs' column partials ([slab][NL][ldb - TB]), else 0
   int32_t band;    // band index I
   int32_t row0;    // first row of the piece within the band (0 or 512)
   int32_t ldb;     // stored columns (row pitch, elements), ceil128(n - I TB)
@@ -61,18 +73,19 @@ struct TsUnit {
   int32_t b, slab, q0, nq;  // owned-band index, 512-row slab, first chunk, chunks
 };
 
-// fp16 one-hot of 128 labels as a K-major, 128-byte-swizzled [16 x 128] UMMA operand (two 64-wide
-// halves of 2 KB): element (c, e) = (lab_e == c). Lane l owns elements 4l .. 4l+3.
+// fp16 one-hot of 128 labels as a K-major, 128-byte-swizzled [NL x 128] UMMA operand (two 64-wide
+// halves of NL x 128 B): element (c, e) = (lab_e == c). Lane l owns elements 4l .. 4l+3.
+template <int NL>
 __device__ __forceinline__ void ts_build_onehot(uint8_t *dst, int4 l4, int lane) {
   const int e = 4 * lane;
   const int h = e >> 6, eh = e & 63;
   const int unit = eh >> 3, sub = (eh & 7) * 2;  // 16-B unit within the 128-B row, byte offset in it
   const uint16_t one = 0x3C00u;                   // fp16 1.0
 #pragma unroll
-  for (int c = 0; c < 16; ++c) {
+  for (int c = 0; c < NL; ++c) {
     const uint32_t lo = (l4.x == c ? one : 0u) | ((l4.y == c ? one : 0u) << 16);
     const uint32_t hi = (l4.z == c ? one : 0u) | ((l4.w == c ? one : 0u) << 16);
-    uint8_t *row = dst + h * 2048 + (c >> 3) * 1024 + (c & 7) * 128;
+    uint8_t *row = dst + h * (NL * 128) + (c >> 3) * 1024 + (c & 7) * 128;
     *reinterpret_cast<uint2 *>(row + ((unit ^ (c & 7)) << 4) + sub) = make_uint2(lo, hi);
   }
 }
@@ -118,9 +131,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   tmem_wait_ld();
 }
 
-// kind::f16, fp16 A and B, fp32 D, M = 128, N = 16; a_mn: A is MN-major.
-constexpr uint32_t ts_idesc(bool a_mn) {
-  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// kind::f16, fp16 A and B, fp32 D, M = 128, N = NL; a_mn: A is MN-major.
+constexpr uint32_t ts_idesc(bool a_mn, int nl) {
+  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((uint32_t)(nl >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
 struct TsSmem {
@@ -133,10 +146,10 @@ struct TsSmem {
   uint32_t *tmem_slot;
 };
 
-constexpr size_t TS_SMEM = 1024 + (size_t)TS_STAGES * TS_TILE_BYTES + 2 * TS_OH_BYTES +
-                           2 * TS_SLAB_TILES * TS_OH_BYTES + 512;  // + barriers, units, TMEM slot
-
+template <int NL>
 __device__ __forceinline__ TsSmem ts_carve(uint8_t *raw) {
+  constexpr int TS_STAGES = TsCfg<NL>::STAGES;
+  constexpr uint32_t TS_OH_BYTES = TsCfg<NL>::OH_BYTES;
   const uint32_t a = smem_u32(raw);
   uint8_t *p = raw + (((a + 1023u) & ~1023u) - a);
   TsSmem s;
@@ -165,13 +178,22 @@ __device__ __forceinline__ TsSmem ts_carve(uint8_t *raw) {
 // maps[b * planes + pl]: fp16 [rows x ldb] view of plane pl (hi, lo) of owned band b, box {64
 // columns, 128 rows}, 128-byte swizzle (global memory, 64-B aligned); both planes of a tile
 // accumulate into the same TMEM sums. work[0], work[1]: zero between launches (reset at the end).
+// NL = 16 (k <= 16): column sums added to Sfix (int64 red.add per column and label);
+// NL = 32 (16 < k <= 32): written to colpart (fp32, [slab][label][column], each entry once) and
+// summed over the slabs by ts_colpart_reduce_kernel -- 2x the labels would double the per-column
+// atomics, while the partials cost ~6 % of the band bytes each way.
+template <int NL>
 __global__ void __launch_bounds__(TS_THREADS, 1)
     spmm_tc_kernel(const CUtensorMap *__restrict__ maps, const TsBand *__restrict__ bands,
                    const TsUnit *__restrict__ units, int nunits, const int32_t *__restrict__ labels, int64_t n,
                    int k, int64_t rows_pad, double fxm, long long *__restrict__ Sfix,
-                   int32_t *__restrict__ work, int planes) {
+                   int32_t *__restrict__ work, int planes, float *__restrict__ colpart) {
+  constexpr int TS_STAGES = TsCfg<NL>::STAGES;
+  constexpr uint32_t TS_OH_BYTES = TsCfg<NL>::OH_BYTES;
+  constexpr int TS_TMEM_COLS = TsCfg<NL>::TMEM_COLS;
+  constexpr uint32_t DR_COLS = TS_SLAB_TILES * NL;  // one D_row buffer: the slab's tiles x NL labels
   extern __shared__ uint8_t smem_raw[];
-  const TsSmem s = ts_carve(smem_raw);
+  const TsSmem s = ts_carve<NL>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < TS_STAGES; ++i) {
@@ -240,7 +262,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         l4.y = r + 1 < n ? labels[r + 1] : -1;
         l4.z = r + 2 < n ? labels[r + 2] : -1;
         l4.w = r + 3 < n ? labels[r + 3] : -1;
-        ts_build_onehot(s.bcol + (ub * TS_SLAB_TILES + t) * TS_OH_BYTES, l4, lane);
+        ts_build_onehot<NL>(s.bcol + (ub * TS_SLAB_TILES + t) * TS_OH_BYTES, l4, lane);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -259,7 +281,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         l4.y = (j + 1 < bd.ldb && g0 + j + 1 < n) ? labels[g0 + j + 1] : -1;
         l4.z = (j + 2 < bd.ldb && g0 + j + 2 < n) ? labels[g0 + j + 2] : -1;
         l4.w = (j + 3 < bd.ldb && g0 + j + 3 < n) ? labels[g0 + j + 3] : -1;
-        ts_build_onehot(s.brow + rb * TS_OH_BYTES, l4, lane);
+        ts_build_onehot<NL>(s.brow + rb * TS_OH_BYTES, l4, lane);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
@@ -296,7 +318,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       int stage = 0;
       uint32_t sphase = 0;
       int64_t chunk_it = 0, dcol_it = 0, drow_it = 0;
-      constexpr uint32_t IROW = ts_idesc(false), ICOL = ts_idesc(true);
+      constexpr uint32_t IROW = ts_idesc(false, NL), ICOL = ts_idesc(true, NL);
       for (int64_t uit = 0;; ++uit) {
         const int ub = (int)(uit & 1);
         const uint32_t uph = (uint32_t)(uit >> 1) & 1u;
@@ -319,7 +341,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
             tc_fence_after();
           }
           const uint64_t brd = umma_desc_sw128(smem_u32(s.brow + rb * TS_OH_BYTES));
-          const uint32_t drow = tmem + (uint32_t)db * 64u;
+          const uint32_t drow = tmem + (uint32_t)db * DR_COLS;
           for (int t = 0; t < ntiles; ++t) {
             const int dc = (int)(dcol_it % TS_DC_BUF);
             const bool cfirst = (t & 1) == 0, clast = (t & 1) == 1 || t == ntiles - 1;
@@ -328,7 +350,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
               mbar_wait(&s.dcolempty[dc], ((uint32_t)(dcol_it / TS_DC_BUF) & 1u) ^ 1u);
               tc_fence_after();
             }
-            const uint32_t dcol = tmem + (uint32_t)(TS_DR_BUF * 64) + (uint32_t)dc * 16u;
+            const uint32_t dcol = tmem + (uint32_t)(TS_DR_BUF * DR_COLS) + (uint32_t)dc * NL;
             const uint64_t bcd = umma_desc_sw128(bcol + (uint32_t)t * TS_OH_BYTES);
             for (int pl = 0; pl < planes; ++pl) {
               mbar_wait(&s.full[stage], sphase);
@@ -341,15 +363,15 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {  // row sums: K-major, k-steps over the 128 columns
                   const uint32_t ko = ((uint32_t)(ks >> 2) * (TS_TILE_BYTES / 2) + (uint32_t)(ks & 3) * 32u) >> 4;
-                  const uint32_t bo = ((uint32_t)(ks >> 2) * 2048u + (uint32_t)(ks & 3) * 32u) >> 4;
-                  ts_mma(drow + (uint32_t)t * 16u, ad + ko, brd + bo, IROW, ks > 0 ? 1u : acc0);
+                  const uint32_t bo = ((uint32_t)(ks >> 2) * (NL * 128u) + (uint32_t)(ks & 3) * 32u) >> 4;
+                  ts_mma(drow + (uint32_t)t * NL, ad + ko, brd + bo, IROW, ks > 0 ? 1u : acc0);
                 }
               } else if (colp) {
                 const uint64_t amn = umma_desc_sw128_mn(a, TS_TILE_BYTES / 2);
                 const uint32_t acc0 = (!cfirst || pl > 0) ? 1u : 0u;
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {  // column sums: A = K^T (MN-major), k-steps over the rows
-                  const uint32_t bo = ((uint32_t)(ks >> 2) * 2048u + (uint32_t)(ks & 3) * 32u) >> 4;
+                  const uint32_t bo = ((uint32_t)(ks >> 2) * (NL * 128u) + (uint32_t)(ks & 3) * 32u) >> 4;
                   ts_mma(dcol, amn + (uint32_t)ks * (2048u >> 4), bcd + bo, ICOL, ks > 0 ? 1u : acc0);
                 }
               }
@@ -387,35 +409,47 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       const int r0 = u.slab * TS_SLAB_TILES * TS_ROWS;
       const int ntiles = min(TS_SLAB_TILES, (bd.rows - r0 + TS_ROWS - 1) / TS_ROWS);
       const int64_t w = (int64_t)bd.ldb - TS_TB;
-      double racc[TS_SLAB_TILES][16];
+      // fp64 for 16 labels; fp32 (RN adds of <= 8 drained chunk-pair sums) for 32, where fp64 would not
+      // fit the registers
+      using RT = typename std::conditional<NL == 16, double, float>::type;
+      RT racc[TS_SLAB_TILES][NL];
 #pragma unroll
       for (int t = 0; t < TS_SLAB_TILES; ++t)
 #pragma unroll
-        for (int c = 0; c < 16; ++c) racc[t][c] = 0.0;
+        for (int c = 0; c < NL; ++c) racc[t][c] = RT(0);
       for (int qi = 0; qi < u.nq; ++qi) {
         const int q = u.q0 + qi;
         if (q * TS_CH >= TS_TB) {  // the column sums of the chunk over the slab's tiles (pairs)
-          double cacc[16];
+          RT cacc[NL];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) cacc[c] = 0.0;
+          for (int c = 0; c < NL; ++c) cacc[c] = RT(0);
           for (int t = 0; t < ntiles; t += 2, ++dcol_it) {
             const int dc = (int)(dcol_it % TS_DC_BUF);
             mbar_wait(&s.dcolfull[dc], (uint32_t)(dcol_it / TS_DC_BUF) & 1u);
             tc_fence_after();
-            float v[16];
-            tmem_ld16(tmem + (uint32_t)(TS_DR_BUF * 64) + (uint32_t)dc * 16u + lq, v);
+#pragma unroll
+            for (int g = 0; g < NL / 16; ++g) {
+              float v[16];
+              tmem_ld16(tmem + (uint32_t)(TS_DR_BUF * DR_COLS) + (uint32_t)dc * NL + 16u * g + lq, v);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) cacc[16 * g + c] += (RT)v[c];
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.dcolempty[dc]);
-#pragma unroll
-            for (int c = 0; c < 16; ++c) cacc[c] += (double)v[c];
           }
           const int64_t jc = (int64_t)q * TS_CH + quarter * 32 + lane - TS_TB;  // off-diagonal column
           if (jc < w) {  // the point g0 + TB + jc of a later band: its column part
-            long long *o = Sfix + g0 + TS_TB + jc;
+            if (NL == 16) {
+              long long *o = Sfix + g0 + TS_TB + jc;
 #pragma unroll
-            for (int c = 0; c < 16; ++c)
-              if (c < k) ts_red_add(o + (int64_t)c * rows_pad, __double2ll_rn(cacc[c] * fxm));
+              for (int c = 0; c < NL; ++c)
+                if (c < k) ts_red_add(o + (int64_t)c * rows_pad, __double2ll_rn((double)cacc[c] * fxm));
+            } else {  // [slab][label][column] partials of this piece's slab (u.slab)
+              float *o = colpart + bd.cpoff + (int64_t)u.slab * NL * w + jc;
+#pragma unroll
+              for (int c = 0; c < NL; ++c) o[(int64_t)c * w] = (float)cacc[c];
+            }
           }
         }
         if ((qi & 1) == 1 || qi == u.nq - 1) {  // the row sums of a chunk pair
@@ -426,10 +460,13 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
 #pragma unroll
           for (int t = 0; t < TS_SLAB_TILES; ++t)
             if (t < ntiles) {
-              float v[16];
-              tmem_ld16(tmem + (uint32_t)db * 64u + (uint32_t)t * 16u + lq, v);
 #pragma unroll
-              for (int c = 0; c < 16; ++c) racc[t][c] += (double)v[c];
+              for (int g = 0; g < NL / 16; ++g) {
+                float v[16];
+                tmem_ld16(tmem + (uint32_t)db * DR_COLS + (uint32_t)t * NL + 16u * g + lq, v);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) racc[t][16 * g + c] += (RT)v[c];
+              }
             }
           tc_fence_before();
           __syncwarp();
@@ -441,8 +478,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         const int64_t row = g0 + bd.row0 + r0 + t * TS_ROWS + quarter * 32 + lane;
         if (t < ntiles && row < n) {  // the row part
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c < k) ts_red_add(Sfix + (int64_t)c * rows_pad + row, __double2ll_rn(racc[t][c] * fxm));
+          for (int c = 0; c < NL; ++c)
+            if (c < k) ts_red_add(Sfix + (int64_t)c * rows_pad + row, __double2ll_rn((double)racc[t][c] * fxm));
         }
       }
       __syncwarp();
@@ -455,6 +492,29 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TS_TMEM_COLS) : "memory");
   }
+}
+
+// NL = 32: the column parts. Slabs of this rank sorted by colstart (= band start + TB): partials
+// colpart[off + c w + (j - colstart)] for the points j >= colstart of later bands. Thread (j, c)
+// sums its slabs in that fixed order (fp64) and adds the total to Sfix[c][j] (int64 fixed point).
+struct TsSlab {
+  int64_t colstart, w, off;
+};
+__global__ void ts_colpart_reduce_kernel(const float *__restrict__ colpart, const TsSlab *__restrict__ slabs,
+                                         int nslab, int64_t n, int k, int64_t rows_pad, double fxm,
+                                         long long *__restrict__ Sfix) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (j >= n || c >= k) return;
+  double s = 0.0;
+  bool any = false;
+  for (int q = 0; q < nslab; ++q) {
+    const TsSlab sl = slabs[q];
+    if (sl.colstart > j) break;
+    s += (double)__ldcs(colpart + sl.off + (int64_t)c * sl.w + (j - sl.colstart));
+    any = true;
+  }
+  if (any) ts_red_add(Sfix + (int64_t)c * rows_pad + j, __double2ll_rn(s * fxm));
 }
 
 // Sfix[c][row] (int64 fixed point, label-major) -> Sout[row][c]: int64 (Sint, for an exact

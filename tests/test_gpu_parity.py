@@ -37,8 +37,8 @@ def _handle(X, k, kind, gamma, coef0, degree, max_iter, precision, **kw):
         if len(precision) >= 3:
             kw["symmetric"] = precision[2]
         if len(precision) == 4:
-            if k > 16 and precision[3] != kkm.KSTORE_FP32:
-                pytest.skip("16-bit K storage needs k <= 16")
+            if k > 32 and precision[3] != kkm.KSTORE_FP32:
+                pytest.skip("16-bit K storage needs k <= 32")
             kw["kstore"] = precision[3]
         precision, kw["path"] = precision[:2]
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
@@ -351,3 +351,15 @@ def test_stream_symmetric_large_k(k):
     X = synth.blobs(9001, 24, k, seed=90 + k, sep=3.0)
     teacher_forced(X, k, oracle.GAUSSIAN, 0.02, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_STREAM))
     teacher_forced(X, k, oracle.POLY, 0.05, 1.0, 2, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_STREAM))
+
+
+@pytest.mark.parametrize("k", [17, 24, 32])
+@pytest.mark.parametrize("kind", [oracle.GAUSSIAN, oracle.POLY])
+def test_tensor_core_bands_32_labels(k, kind):
+    """spmm_tc with 32-label one-hot operands (16 < k <= 32): the column parts go through the
+    [slab][label][column] partials and ts_colpart_reduce_kernel; n = 5001 gives 5 bands (pieces of
+    1024 rows, 2 slabs each) and a ragged last band; teacher-forced against the oracle."""
+    X = synth.blobs(5001, 12, k, seed=70 + k, sep=3.0)
+    args = (kind, 0.05, 0.0, 1) if kind == oracle.GAUSSIAN else (kind, 0.05, 1.0, 2)
+    teacher_forced(X, k, *args, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON,
+                                                      kkm.KSTORE_FP16X2))

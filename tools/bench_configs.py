@@ -26,6 +26,7 @@ ap.add_argument("--points", "--n", dest="n", type=int, default=0, help="override
 ap.add_argument("--grid-rows", type=int, default=1)
 ap.add_argument("--path", default="auto", choices=["auto", "mat", "stream"])
 ap.add_argument("--symmetric", default="auto", choices=["auto", "off", "on"])
+ap.add_argument("--k", type=int, default=0, help="override the cluster count (labelled in the output)")
 ap.add_argument("--kstore", default="auto", choices=["auto", "fp32", "fp16", "fp16x2"],
                 help="materialised band storage (f4: fp16 = low-precision storage)")
 a = ap.parse_args()
@@ -59,6 +60,8 @@ torch.cuda.synchronize()
 
 for name in a.configs.split(","):
     cfg = dict(synth.CONFIGS[name])
+    if a.k:
+        cfg["k"] = a.k
     n = a.n or cfg["n"]
     iters = a.iters or cfg["iters"]
     t0 = time.time()
@@ -89,7 +92,8 @@ for name in a.configs.split(","):
     mat = h.params.path == kkm.PATH_MATERIALIZE or (
         h.params.path == kkm.PATH_AUTO
         and kkm.workspace_size(h.params, n, Xl.shape[1], rank, world) > 0.3 * kfull)
-    sym = (mat and cfg["k"] <= 16 and a.grid_rows <= 1 and h.params.symmetric != kkm.SYM_OFF
+    sym = (mat and (cfg["k"] <= 16 or (cfg["k"] <= 32 and a.kstore != "fp32")) and a.grid_rows <= 1
+           and h.params.symmetric != kkm.SYM_OFF
            and (h.params.symmetric == kkm.SYM_ON or n >= 8192))  # make_plan's rule
     vals = torch.tensor([init_ms, fit_ms, ph["spmm"], ph["cnorm"], ph["assign"], ph["init_gemm"]],
                         dtype=torch.float64, device=dev)

@@ -68,8 +68,10 @@ for name, n, iters, path, g, opt in cases:
         same &= it == it1
         diag = oracle.kernel_diag(X, *args)
         if have_ref:  # the oracle ran: labels identical, J trace within the north_star rule
+            # (kstore FP16 is the documented low-precision storage: its J bound is 3 * 2^-11, DESIGN A27)
+            jt = (lambda b: 3 * 2.0 ** -11 * abs(b)) if opt.get("kstore") == kkm.KSTORE_FP16 else (lambda b: j_tol(b, diag))
             ok &= np.array_equal(lab, ref["labels"]) and it == ref["iters"]
-            ok &= all(abs(a - b) <= j_tol(b, diag) for a, b in zip(J, ref["J_trace"]))
+            ok &= all(abs(a - b) <= jt(b) for a, b in zip(J, ref["J_trace"]))
         else:  # J of the final labels from the points (oracle.objective_X, reading A8)
             Jx = oracle.objective_X(X, lab, cfg["k"], *args)
             ok &= abs(J[-1] - Jx) <= j_tol(Jx, diag)
