@@ -279,6 +279,29 @@ int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   return KKM_OK;
 }
 
+// The 1.5D column-split reduce-scatter over the pr ranks of process column j,
+// as point-to-point exchanges on the world communicator (no split communicator: its creation cost
+// ~3 s of init and a first-use spike): rank (i, j) sends piece i' of its Scol to rank (i', j), receives
+// piece i from every other rank of the column, and sums the pr pieces in rank order (fixed order,
+// so the result is bitwise the same on every run). Collective over the column.
+int column_reduce_scatter(kkm_ctx *h) {
+  const Plan &P = h->P;
+  const size_t bk = (size_t)P.B * P.k;
+  double *rbuf = (double *)(h->ws + P.o_Srecv);
+  CKN(ncclGroupStart());
+  for (int ip = 0; ip < P.pr; ++ip) {
+    if (ip == P.gi) continue;
+    const int peer = ip + P.gj * P.pr;
+    CKN(ncclSend(h->Scol + ip * bk, bk, ncclDouble, peer, h->comm, h->st));
+    CKN(ncclRecv(rbuf + ip * bk, bk, ncclDouble, peer, h->comm, h->st));
+  }
+  CKN(ncclGroupEnd());
+  column_sum_kernel<<<(unsigned)ceil_div((int64_t)bk, 256), 256, 0, h->st>>>(h->Scol, rbuf, P.pr, P.gi, (int64_t)bk,
+                                                                           h->Smine);
+  CKL();
+  return KKM_OK;
+}
+
 // a2 + the 1.5D column-split reduce-scatter: afterwards the S partials of this rank's own 1D
 // block are in s_out[nsplit_out][B][k] (the 1D case reduces nothing: s_out = Spart).
 int launch_spmm(kkm_ctx *h, const int32_t *labels, const double **s_out, int *nsplit_out) {
@@ -301,7 +324,7 @@ int launch_spmm(kkm_ctx *h, const int32_t *labels, const double **s_out, int *ns
                                                                               P.nApad, P.k, h->Scol);
   CKL();
   // P(i, j) keeps piece i of column block j = its own 1D block (column-major ranks)
-  CKN(ncclReduceScatter(h->Scol, h->Smine, (size_t)P.B * P.k, ncclDouble, ncclSum, h->colcomm, h->st));
+  CKR(column_reduce_scatter(h));
   *s_out = h->Smine;
   *nsplit_out = 1;
   return KKM_OK;

@@ -87,7 +87,6 @@ struct kkm_ctx {
   SortedSet dset{};
   bool s_valid = false;  // Sinc holds S of the current labels
   TcStream ts_delta;
-  ncclComm_t colcomm = nullptr;
   int32_t *lab[2], *sizes[2];
   unsigned long long *changed;
   int *bad;

@@ -181,6 +181,17 @@ __global__ void copy_labels_kernel(const int32_t *__restrict__ labels, int64_t n
   if (t < len) labB[t] = t < nB ? labels[t] : -1;
 }
 
+// 1.5D: out[t] = sum over the pr pieces of the column in rank order, piece gi from the own Scol,
+// the others from the received buffer (rbuf[ip * bk + t]).
+__global__ void column_sum_kernel(const double *__restrict__ Scol, const double *__restrict__ rbuf, int pr, int gi,
+                                  int64_t bk, double *__restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= bk) return;
+  double s = 0.0;
+  for (int ip = 0; ip < pr; ++ip) s += ip == gi ? Scol[(int64_t)gi * bk + t] : rbuf[(int64_t)ip * bk + t];
+  out[t] = s;
+}
+
 // Scol[r][c] = sum_s Spart[s][r][c] (fixed order) for r < nA, 0 on [nA, rows_pad).
 __global__ void split_sum_kernel(const double *__restrict__ Spart, int nsplit, int64_t nA, int64_t rows_pad,
                                  int k, double *__restrict__ Scol) {

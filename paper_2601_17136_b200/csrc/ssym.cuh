@@ -91,7 +91,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
   const uint32_t tmem_base = *s.tmem_slot;
 
   if (warp < 2) {
-    ch_producer_mma(sc, s, warp, lane, cr, &t_hi, &t_lo, &t_hi, &t_lo, nkb, nch, idesc, tmem_base);
+    ch_producer_mma(sc, s, warp, lane, cr, &t_hi, &t_lo, &t_hi, &t_lo, nkb, nch, idesc, tmem_base, sc.hint);
   } else {
     const int e = warp - 2;
     const int quarter = warp & 3;
@@ -165,6 +165,8 @@ inline int ssym_launch(TcStream &g, const uint16_t *Shi, const uint16_t *Slo, bo
   T2SymSched sc;
   sc.units = units;
   sc.nitems = nunits;
+  sc.hint = 1;
+  if (const char *e = std::getenv("KKM_SSYM_HINT")) sc.hint = std::atoi(e);  // (A/B runs of the L2 policy)
   const int64_t clusters = nunits < g.num_sms / 2 ? nunits : g.num_sms / 2;
   const unsigned grid = (unsigned)(2 * clusters);
   const float *rs = fp16 ? srscale : nullptr;

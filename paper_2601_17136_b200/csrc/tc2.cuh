@@ -98,8 +98,12 @@ template <class Sched>
 __device__ __forceinline__ void t2_producer(const Sched &sc, const T2Smem &s, const CUtensorMap *a_hi,
                                             const CUtensorMap *a_lo, const CUtensorMap *b_hi,
                                             const CUtensorMap *b_lo, int nkb, uint32_t cr, int hint) {
-  const uint64_t keep = hint ? l2_policy_evict_last() : l2_policy_evict_normal();
-  const uint64_t bpol = keep;  // (evict_normal on the streaming B measured slower)
+  // hint: L2 policy of the A / B operand loads -- 0 normal / normal, 1 evict_last / evict_last,
+  // 2 evict_last / normal, 3 normal / evict_last, 4 evict_last / evict_first
+  const uint64_t keep = (hint == 1 || hint == 2 || hint == 4) ? l2_policy_evict_last() : l2_policy_evict_normal();
+  const uint64_t bpol = (hint == 1 || hint == 3) ? l2_policy_evict_last()
+                        : hint == 4              ? l2_policy_evict_first()
+                                                 : l2_policy_evict_normal();
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   int stage = 0;
   uint32_t phase = 0;
@@ -283,6 +287,7 @@ struct T2StreamSched {
 struct T2SymSched {
   const int4 *units;
   int64_t nitems;
+  int hint;  // L2 policy of the operand loads (t2_producer)
   __device__ __forceinline__ void item(int64_t u, int &ra, int &rb0, int &ntn) const {
     const int4 U = units[u];
     ra = U.x * T2_BM;
