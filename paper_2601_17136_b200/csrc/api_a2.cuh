@@ -254,7 +254,7 @@ int launch_stream_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
   CK(cudaMemsetAsync(h->Sfix, 0, (size_t)P.npad * k * 8, h->st));
   a2_mark(h);
   int rc = ssym_launch(h->ts, h->Shi, h->Slo, P.fp16, P.npad, P.dp, P.n, h->snorms, h->srscale, h->seg, k, h->kp,
-                       h->units, (int64_t)P.units.size(), h->fx_scale, h->Sfix, h->st, &h->launches, h->chain_kb);
+                       h->units, (int64_t)P.units.size(), h->work + 2, h->fx_scale, h->Sfix, h->st, &h->launches, h->chain_kb);
   a2_mark(h);
   if (rc) {
     h->poisoned = true;

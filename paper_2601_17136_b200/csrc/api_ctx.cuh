@@ -56,7 +56,7 @@ struct kkm_ctx {
   SymBand *bands = nullptr;
   float *colpart = nullptr;
   double *colsum = nullptr, *Sfin = nullptr;
-  int32_t *work = nullptr;  // spmm_sym's item scheduler (2 counters, zero between launches)
+  int32_t *work = nullptr;  // item schedulers: [0, 2) spmm_tc, [2, 4) ssym (zero between launches)
   unsigned *a3ctr = nullptr;  // finalize's last-block counter (zero between launches)
   // peer-memory exchange of S (16-bit bands, replicated a3, several ranks): own IPC buffer
   // [2 epochs][k][npad] int64 + flag + peer table; peers' buffers mapped with cudaIpcOpenMemHandle

@@ -240,14 +240,20 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     // G > 0: single-tile units in a supertile raster -- G x G patches of the upper triangle, patch
     // by patch, each patch column by column -- so the ~74 tiles in flight cover a compact patch
     // (~9 row tiles x ~9 column tiles: ~15 MB of operands in L2 instead of 74 row tiles + a block)
-    int64_t G = 0;
+    // (W: column tiles per unit inside a patch)
+    int64_t G = 0, W = 1;
     if (const char *e = std::getenv("KKM_SSYM_G")) G = std::max<int64_t>(0, std::atoll(e));
+    if (const char *e = std::getenv("KKM_SSYM_W")) W = std::max<int64_t>(1, std::atoll(e));
     if (G > 0) {
       for (int64_t I = 0; I * G < Tt; ++I)
-        for (int64_t J = I; J * G < Tt; ++J)
-          for (int64_t tn = J * G; tn < std::min(Tt, (J + 1) * G); ++tn)
-            for (int64_t tm = I * G; tm < std::min(Tt, (I + 1) * G) && tm <= tn; ++tm)
-              all.push_back(make_int4((int)tm, (int)tn, 1, 0));
+        for (int64_t J = I; J * G < Tt; ++J) {
+          const int64_t je = std::min(Tt, (J + 1) * G);
+          for (int64_t t0 = J * G; t0 < je; t0 += W)
+            for (int64_t tm = I * G; tm < std::min(Tt, (I + 1) * G); ++tm) {
+              const int64_t a = std::max(tm, t0), e = std::min(je, t0 + W);
+              if (a < e) all.push_back(make_int4((int)tm, (int)a, (int)(e - a), 0));
+            }
+        }
     } else {
       for (int64_t tm = 0; tm < Tt; ++tm)
         for (int64_t b = tm / BS; b * BS < Tt; ++b) {
@@ -456,6 +462,7 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_Sd = take((size_t)P.B * P.k * 8);   // fp64 S of the moved points' pass
     P.o_Sdx = take((size_t)P.B * P.k * 8);  // its int64 fixed-point sums
   }
+  if (P.sym || P.ssym) P.o_work = take(4 * 4);  // item schedulers: [0, 2) spmm_tc, [2, 4) ssym (zero between launches)
   if (P.sym) {
     P.o_perm_b = take((size_t)P.T * SYM_TB * 4);
     P.o_groups = take((size_t)P.T * P.sym_gmax * sizeof(SymGroup));
@@ -464,7 +471,6 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.o_band_desc = take((size_t)P.T * 4);
     P.o_colpart = take(P.kh ? 4 : std::max<size_t>(cpfloats, 1) * 4);
     P.o_colsum = take(P.kh ? 8 : std::max<size_t>(csdoubles, 1) * 8);
-    P.o_work = take(2 * 4);  // spmm_sym's item scheduler
     P.o_gfirst = take((size_t)P.T * (P.k + 1) * 4);
     P.o_Sfin = take((size_t)P.npad * P.k * 8);
     if (P.tc) {  // one GEMM launch over all owned band pieces: regions + output maps

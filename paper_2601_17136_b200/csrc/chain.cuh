@@ -152,59 +152,65 @@ __device__ __forceinline__ void ch_setup(const ChSmem &s, int warp, uint32_t cem
   tc_fence_after();
 }
 
-// MMA issuer of the chained schedule (warp 1 lane 0 of the leader CTA).
+// MMA issuer body of one work item u (warp 1 lane 0 of the leader CTA): every tile as nch chains.
 template <class Sched>
-__device__ __forceinline__ void ch_mma(const Sched &sc, const ChSmem &s, int nkb, int nch, uint32_t idesc,
-                                             uint32_t tmem_base) {
-  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  int stage = 0;
-  uint32_t phase = 0;
-  int64_t chain = 0;
-  for (int64_t u = cl; u < sc.nitems; u += ncl) {
-    int ra, rb0, ntn;
-    sc.item(u, ra, rb0, ntn);
-    for (int t = 0; t < ntn; ++t) {
-      uint32_t d = tmem_base;
-      int ci = 0, lo = 0, hi = nkb / nch;  // chain ci covers K-blocks [lo, hi) = [ci nkb / nch, (ci+1) nkb / nch)
-      for (int kb = 0; kb < nkb; ++kb) {
-        const bool first = kb == lo;
-        if (first) {
-          const int b = (int)(chain & 1);
-          mbar_wait(&s.cempty[b], ((uint32_t)(chain >> 1) & 1u) ^ 1u);
-          tc_fence_after();
-          d = tmem_base + (uint32_t)b * 256u;
-        }
-        mbar_wait(&s.full[stage], phase);
+__device__ __forceinline__ void ch_mma_item(const Sched &sc, const ChSmem &s, int64_t u, int nkb, int nch,
+                                            uint32_t idesc, uint32_t tmem_base, int &stage, uint32_t &phase,
+                                            int64_t &chain) {
+  int ra, rb0, ntn;
+  sc.item(u, ra, rb0, ntn);
+  for (int t = 0; t < ntn; ++t) {
+    uint32_t d = tmem_base;
+    int ci = 0, lo = 0, hi = nkb / nch;  // chain ci covers K-blocks [lo, hi) = [ci nkb / nch, (ci+1) nkb / nch)
+    for (int kb = 0; kb < nkb; ++kb) {
+      const bool first = kb == lo;
+      if (first) {
+        const int b = (int)(chain & 1);
+        mbar_wait(&s.cempty[b], ((uint32_t)(chain >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t st = smem_u32(s.stages + stage * T2_STAGE_BYTES);
-        const uint32_t a_hi = st, a_lo = st + T2_HALF_BYTES;
-        const uint32_t b_hi = st + 2 * T2_HALF_BYTES, b_lo = st + 3 * T2_HALF_BYTES;
+        d = tmem_base + (uint32_t)b * 256u;
+      }
+      mbar_wait(&s.full[stage], phase);
+      tc_fence_after();
+      const uint32_t st = smem_u32(s.stages + stage * T2_STAGE_BYTES);
+      const uint32_t a_hi = st, a_lo = st + T2_HALF_BYTES;
+      const uint32_t b_hi = st + 2 * T2_HALF_BYTES, b_lo = st + 3 * T2_HALF_BYTES;
 #pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k) {
-          const uint32_t ko = (uint32_t)k * 32u;
-          umma2_f16(d, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_lo + ko), idesc, (first && k == 0) ? 0u : 1u);
-          umma2_f16(d, umma_desc_sw128(a_lo + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
-          umma2_f16(d, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
-        }
-        umma2_commit_both(&s.empty[stage]);
-        if (++stage == T2_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-        if (kb == hi - 1) {
-          ++ci;
-          lo = hi;
-          hi = (int)((int64_t)(ci + 1) * nkb / nch);
-          umma2_commit_both(&s.cfull[chain & 1]);
-          ++chain;
-        }
+      for (int k = 0; k < TC_BK / 16; ++k) {
+        const uint32_t ko = (uint32_t)k * 32u;
+        umma2_f16(d, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_lo + ko), idesc, (first && k == 0) ? 0u : 1u);
+        umma2_f16(d, umma_desc_sw128(a_lo + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
+        umma2_f16(d, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_hi + ko), idesc, 1u);
+      }
+      umma2_commit_both(&s.empty[stage]);
+      if (++stage == T2_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (kb == hi - 1) {
+        ++ci;
+        lo = hi;
+        hi = (int)((int64_t)(ci + 1) * nkb / nch);
+        umma2_commit_both(&s.cfull[chain & 1]);
+        ++chain;
       }
     }
   }
 }
 
+// MMA issuer, static schedule (pair cl takes items cl, cl + ncl, ...).
+template <class Sched>
+__device__ __forceinline__ void ch_mma(const Sched &sc, const ChSmem &s, int nkb, int nch, uint32_t idesc,
+                                       uint32_t tmem_base) {
+  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  int stage = 0;
+  uint32_t phase = 0;
+  int64_t chain = 0;
+  for (int64_t u = cl; u < sc.nitems; u += ncl) ch_mma_item(sc, s, u, nkb, nch, idesc, tmem_base, stage, phase, chain);
+}
+
 __device__ __forceinline__ void ch_wait(const ChSmem &s, int64_t chain) {
-  mbar_wait(&s.cfull[chain & 1], (uint32_t)(chain >> 1) & 1u);
+  mbar_wait_backoff(&s.cfull[chain & 1], (uint32_t)(chain >> 1) & 1u);
   tc_fence_after();
 }
 __device__ __forceinline__ void ch_release(const ChSmem &s, int64_t chain, int lane) {

@@ -162,6 +162,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 #endif
 }
+// Wait with exponential nanosleep backoff (32 ns .. 512 ns) between tests, for waits that are long
+// and not latency-critical (epilogue warps waiting for a chain of ~4 us, the TMA producer waiting for
+// a free stage): a spinning warp re-issues its test every few cycles and burns issue slots and power
+// (ncu at n = 1M: the epilogue's spin loops were over half of the kernel's executed instructions).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
 // L2 eviction-priority policies for .L2::cache_hint operands.
 __device__ __forceinline__ uint64_t l2_policy_evict_normal() {
   uint64_t p;

@@ -197,6 +197,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
                         (float *)(w + P.o_Dr),      (int32_t *)(w + P.o_dperm), (int32_t *)(w + P.o_dpos),
                         (int32_t *)(w + P.o_dseg),  (int32_t *)(w + P.o_dbc),   (int32_t *)(w + P.o_dbo)};
   }
+  if (P.ssym || P.sym) h->work = (int32_t *)(w + P.o_work);
   if (P.ssym) {
     h->units = (int4 *)(w + P.o_units);
     h->Sfix = (long long *)(w + P.o_Sfix);
@@ -213,7 +214,6 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     h->band_desc = (int32_t *)(w + P.o_band_desc);
     h->colpart = (float *)(w + P.o_colpart);
     h->colsum = (double *)(w + P.o_colsum);
-    h->work = (int32_t *)(w + P.o_work);
     if (P.kh) {
       h->tmaps = (CUtensorMap *)(w + P.o_tmaps);
       h->tbands = (TsBand *)(w + P.o_tbands);
@@ -307,6 +307,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     if (!evs.record(h->st)) return fail(KKM_ECUDA, "cudaEventCreate/Record failed");
     // ---- a1: K tile [A set, B set] = kappa(X X^T), materialised once; with
     // symmetric storage (f1) the owned upper-triangle bands, one launch each
+    if (P.ssym) CK(cudaMemsetAsync(h->work, 0, 4 * 4, h->st));
     if (P.ssym && !P.units.empty())
       CK(cudaMemcpyAsync(h->units, P.units.data(), P.units.size() * sizeof(int4), cudaMemcpyHostToDevice, h->st));
     if (P.tc) {  // the fixed-point scale 2^s of the streaming kernels' S (loop, f3 deltas): n max|K| 2^s < 2^61
@@ -328,7 +329,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
         CK(cudaMemcpyAsync(h->bands, P.bands.data(), P.bands.size() * sizeof(SymBand), cudaMemcpyHostToDevice,
                            h->st));
       CK(cudaMemcpyAsync(h->band_desc, P.band_desc.data(), (size_t)P.T * 4, cudaMemcpyHostToDevice, h->st));
-      CK(cudaMemsetAsync(h->work, 0, 2 * 4, h->st));
+      CK(cudaMemsetAsync(h->work, 0, 4 * 4, h->st));
       CK(cudaMemsetAsync(h->a3ctr, 0, 16, h->st));
       if (P.kh) {  // f4: storage scale 2^e with |K| 2^e <= 60000 (|K_ij| <= max_i K_ii, bounded as for ssym)
         max_norm_kernel<<<1, 1024, 0, h->st>>>(h->norms, P.n, h->fxmax);

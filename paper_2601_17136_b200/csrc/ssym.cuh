@@ -21,7 +21,11 @@
 //     converted to int64 directly.
 // Work units (tm, tn0, ntn) cover the upper triangle in aligned blocks of column tiles; the host
 // orders a rank's units block-major, so the ~74 pairs running at once sweep the SAME block of B
-// tiles (L2-resident) with different row tiles.
+// tiles (L2-resident) with different row tiles. The pairs take units in that order DYNAMICALLY (one
+// global counter; the leader CTA's producer fetches the next index and publishes it to both CTAs
+// through a ring of smem slots): with a static round robin the pairs drift apart over a long
+// launch (diagonal units are short) until the units in flight span several blocks and the
+// operands fall out of L2.
 #pragma once
 #include "chain.cuh"
 
@@ -32,7 +36,85 @@ constexpr int SS_THREADS = CH_THREADS;
 constexpr int SS_COLS = CH_COLS;
 constexpr size_t SS_COLC_BYTES = CH_COLC_BYTES;
 constexpr size_t SS_SEG_BYTES = (size_t)(KKM_MAX_K + 1) * 4;
-constexpr size_t SS_EXTRA = SS_EPI_WARPS * SS_COLC_BYTES + (SS_SEG_BYTES + 15) / 16 * 16;
+constexpr int SS_RING = 8;  // unit-index slots in flight per pair (dynamic schedule)
+constexpr size_t SS_RING_OFF = SS_EPI_WARPS * SS_COLC_BYTES + (SS_SEG_BYTES + 15) / 16 * 16;
+constexpr size_t SS_EXTRA = SS_RING_OFF + 2 * SS_RING * 8 + SS_RING * 4;
+// arrivals that free a ring slot (on the leader CTA): per CTA its 16 epilogue warps + the MMA
+// issuer (leader) / the producer (peer CTA)
+constexpr uint32_t SS_RING_CONSUMERS = 2 * (SS_EPI_WARPS + 1);
+
+__device__ __forceinline__ void st_cluster_s32(int32_t *p, uint32_t cta, int32_t v) {
+  asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.s32 [ra], %2;\n\t}" ::"r"(
+                   smem_u32(p)),
+               "r"(cta), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint64_t *bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t parity) {
+  uint32_t ns = 32;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
+// The pair's unit source. Static: pair cl takes units cl, cl + ncl, ... Dynamic: position i of the
+// ring (slot i % SS_RING) carries the i-th unit the pair fetched from the global counter work[0]
+// (-1: none left); the leader producer fetches (one ahead) and publishes, the other roles read.
+// work[1] counts the pairs that saw the end; the last one resets both counters for the next launch.
+struct SsRing {
+  int32_t *slot;
+  uint64_t *full, *empty;  // full: 1 arrival (the leader producer), in both CTAs; empty: leader CTA only
+  bool dyn;
+  int64_t nitems;
+  int32_t *work;
+  __device__ __forceinline__ int64_t static_unit(int64_t i) const {
+    const int64_t u = (int64_t)(blockIdx.x >> 1) + i * (int64_t)(gridDim.x >> 1);
+    return u < nitems ? u : -1;
+  }
+  // leader producer: publish the pair's next unit (nxt: the prefetched counter value)
+  __device__ __forceinline__ int64_t publish(int64_t i, int &nxt) const {
+    if (!dyn) return static_unit(i);
+    const int sl = (int)(i % SS_RING);
+    mbar_wait_acq_cluster(&empty[sl], (uint32_t)((i / SS_RING) & 1) ^ 1u);
+    int u = nxt < nitems ? nxt : -1;
+    if (u >= 0) {
+      nxt = atomicAdd(work, 1);
+    } else if (atomicAdd(work + 1, 1) == (int)(gridDim.x >> 1) - 1) {
+      work[0] = 0;
+      work[1] = 0;
+    }
+    slot[sl] = u;
+    st_cluster_s32(&slot[sl], 1, u);
+    mbar_arrive(&full[sl]);
+    mbar_arrive_cluster_release(&full[sl], 1);
+    return u;
+  }
+  // other roles: the unit at ring position i; `arrive`: this thread frees the slot for its warp
+  __device__ __forceinline__ int64_t take(int64_t i, bool arrive) const {
+    if (!dyn) return static_unit(i);
+    const int sl = (int)(i % SS_RING);
+    mbar_wait_acq_cluster(&full[sl], (uint32_t)((i / SS_RING) & 1));
+    const int u = *reinterpret_cast<volatile int32_t *>(&slot[sl]);
+    __syncwarp(__activemask());
+    if (arrive) mbar_arrive_cluster_release(&empty[sl], 0);
+    return u;
+  }
+};
 constexpr size_t SS_SMEM = (size_t)T2_STAGES * T2_STAGE_BYTES + SS_EXTRA + 1024 + 128;
 
 // One 32-column chunk of a tile (columns p0 .. p0 + 31, this thread's row p): kappa, the row part
@@ -77,30 +159,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
     ssym_kernel(const __grid_constant__ CUtensorMap t_hi, const __grid_constant__ CUtensorMap t_lo,
                       uint32_t idesc, int nkb, int nch, int64_t n, const float *__restrict__ snorms,
                       const float *__restrict__ srscale, const int32_t *__restrict__ seg_g, int k, KappaParams kp,
-                      T2SymSched sc, float fx_scale, long long *__restrict__ Sfix) {
+                      T2SymSched sc, bool dyn, int32_t *__restrict__ work, float fx_scale,
+                      long long *__restrict__ Sfix) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *extra;
   const ChSmem s = ch_carve(smem_raw, (uint32_t)SS_EXTRA, &extra);
   float *colc = reinterpret_cast<float *>(extra);
   int32_t *seg = reinterpret_cast<int32_t *>(extra + SS_EPI_WARPS * SS_COLC_BYTES);
+  SsRing ring;
+  ring.full = reinterpret_cast<uint64_t *>(extra + SS_RING_OFF);
+  ring.empty = ring.full + SS_RING;
+  ring.slot = reinterpret_cast<int32_t *>(ring.empty + SS_RING);
+  ring.dyn = dyn;
+  ring.nitems = sc.nitems;
+  ring.work = work;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cr = cluster_ctarank();
   const bool fp16 = srscale != nullptr;
   for (int c = threadIdx.x; c <= k; c += blockDim.x) seg[c] = seg_g[c];
-  ch_setup(s, warp, 2 * SS_EPI_WARPS);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < SS_RING; ++i) {
+      mbar_init(&ring.full[i], 1);
+      mbar_init(&ring.empty[i], SS_RING_CONSUMERS);
+    }
+  ch_setup(s, warp, 2 * SS_EPI_WARPS);  // (its fence + cluster barrier also publish the ring's init)
   const uint32_t tmem_base = *s.tmem_slot;
 
-  if (warp < 2) {
-    ch_producer_mma(sc, s, warp, lane, cr, &t_hi, &t_lo, &t_hi, &t_lo, nkb, nch, idesc, tmem_base, sc.hint);
+  if (warp == 0) {
+    if (lane == 0) {
+      T2Smem ts;  // the producer only uses the stage ring
+      ts.stages = s.stages;
+      ts.full = s.full;
+      ts.empty = s.empty;
+      const T2Policy pol(sc.hint);
+      int stage = 0;
+      uint32_t phase = 0;
+      int nxt = (dyn && cr == 0) ? atomicAdd(work, 1) : 0;
+      for (int64_t i = 0;; ++i) {
+        const int64_t u = cr == 0 ? ring.publish(i, nxt) : ring.take(i, true);
+        if (u < 0) break;
+        t2_produce_item(sc, ts, u, &t_hi, &t_lo, &t_hi, &t_lo, nkb, cr, pol, stage, phase);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && cr == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t chain = 0;
+      for (int64_t i = 0;; ++i) {
+        const int64_t u = ring.take(i, true);
+        if (u < 0) break;
+        ch_mma_item(sc, s, u, nkb, nch, idesc, tmem_base, stage, phase, chain);
+      }
+    }
   } else {
     const int e = warp - 2;
     const int quarter = warp & 3;
     const int colq = e >> 2;
     float *cn = colc + e * (2 * SS_COLS);
     const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colq * SS_COLS);
-    const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     int64_t chain = 0;
-    for (int64_t u = cl; u < sc.nitems; u += ncl) {
+    for (int64_t i = 0;; ++i) {
+      const int64_t u = ring.take(i, lane == 0);
+      if (u < 0) break;
       const int4 U = sc.units[u];
       const int tm = U.x, tn0 = U.y, tn1 = U.y + U.z;
       const int64_t rw = (int64_t)tm * T2_BM + (int64_t)cr * 128 + quarter * 32;
@@ -136,8 +257,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
 
 inline int ssym_launch(TcStream &g, const uint16_t *Shi, const uint16_t *Slo, bool fp16, int64_t rows, int64_t dp,
                        int64_t n, const float *snorms, const float *srscale, const int32_t *seg, int k,
-                       const KappaParams &kp, const int4 *units, int64_t nunits, double fx_scale, long long *Sfix,
-                       cudaStream_t st, int64_t *launches, int ckb = 0) {  // ckb: K-blocks per chain (0: CH_CKB)
+                       const KappaParams &kp, const int4 *units, int64_t nunits, int32_t *work, double fx_scale,
+                       long long *Sfix, cudaStream_t st, int64_t *launches, int ckb = 0) {
+  // ckb: K-blocks per chain (0: CH_CKB); work: 2 int32 counters, zero between launches (dynamic
+  // schedule; the kernel resets them)
   if (!tc_encode_fn()) {
     TcGemm tmp;
     if (tc_make_maps(tmp, Shi, Slo, fp16, rows, dp)) return 1;
@@ -167,6 +290,7 @@ inline int ssym_launch(TcStream &g, const uint16_t *Shi, const uint16_t *Slo, bo
   sc.nitems = nunits;
   sc.hint = 1;
   if (const char *e = std::getenv("KKM_SSYM_HINT")) sc.hint = std::atoi(e);  // (A/B runs of the L2 policy)
+  const bool dyn = std::getenv("KKM_SSYM_STATIC") == nullptr;  // (A/B runs: the static round robin)
   const int64_t clusters = nunits < g.num_sms / 2 ? nunits : g.num_sms / 2;
   const unsigned grid = (unsigned)(2 * clusters);
   const float *rs = fp16 ? srscale : nullptr;
@@ -176,7 +300,7 @@ inline int ssym_launch(TcStream &g, const uint16_t *Shi, const uint16_t *Slo, bo
     constexpr int KIND = decltype(kind_tag)::value;
     if (ensure_smem_attr((const void *)ssym_kernel<KIND>, SS_SMEM) != cudaSuccess) return 1;
     ssym_kernel<KIND><<<grid, SS_THREADS, SS_SMEM, st>>>(g.a_hi, g.a_lo, t2_idesc(fp16), nkb, nch, n, snorms, rs, seg,
-                                                         k, kp, sc, (float)fx_scale, Sfix);
+                                                         k, kp, sc, dyn, work, (float)fx_scale, Sfix);
     return 0;
   };
   const int rc = ch_dispatch_kind(kp, go);

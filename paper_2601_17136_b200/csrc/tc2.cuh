@@ -92,43 +92,56 @@ __device__ __forceinline__ T2Smem t2_carve(uint8_t *smem_raw, uint32_t extra, ui
   return s;
 }
 
-// Producer (warp 0 lane 0 of both CTAs). Sched::item(u, ra, rb0, ntn): pair-tile A row base,
-// first B row, number of 256-column tiles of work item u (B rows rb0 + t * 256).
+// L2 policy of the operand loads: hint 0 normal / normal, 1 evict_last / evict_last, 2 evict_last /
+// normal, 3 normal / evict_last, 4 evict_last / evict_first (A / B).
+struct T2Policy {
+  uint64_t a, b;
+  __device__ __forceinline__ explicit T2Policy(int hint) {
+    a = (hint == 1 || hint == 2 || hint == 4) ? l2_policy_evict_last() : l2_policy_evict_normal();
+    b = (hint == 1 || hint == 3) ? l2_policy_evict_last() : hint == 4 ? l2_policy_evict_first() : l2_policy_evict_normal();
+  }
+};
+
+// Producer body of one work item u (this CTA's halves of A and B through the stage ring).
+template <class Sched>
+__device__ __forceinline__ void t2_produce_item(const Sched &sc, const T2Smem &s, int64_t u, const CUtensorMap *a_hi,
+                                                const CUtensorMap *a_lo, const CUtensorMap *b_hi,
+                                                const CUtensorMap *b_lo, int nkb, uint32_t cr, const T2Policy &pol,
+                                                int &stage, uint32_t &phase) {
+  int ra, rb0, ntn;
+  sc.item(u, ra, rb0, ntn);
+  for (int t = 0; t < ntn; ++t) {
+    const int rb = rb0 + t * 256;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait_backoff(&s.empty[stage], phase ^ 1);
+      uint8_t *st = s.stages + stage * T2_STAGE_BYTES;
+      if (cr == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * T2_STAGE_BYTES);
+      const int kc = kb * TC_BK;
+      const int ar = ra + (int)cr * 128, br = rb + (int)cr * 128;
+      tma_load_2d_pair(st, a_hi, kc, ar, &s.full[stage], pol.a);
+      tma_load_2d_pair(st + T2_HALF_BYTES, a_lo, kc, ar, &s.full[stage], pol.a);
+      tma_load_2d_pair(st + 2 * T2_HALF_BYTES, b_hi, kc, br, &s.full[stage], pol.b);
+      tma_load_2d_pair(st + 3 * T2_HALF_BYTES, b_lo, kc, br, &s.full[stage], pol.b);
+      if (++stage == T2_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+}
+
+// Producer (warp 0 lane 0 of both CTAs), static schedule: pair cl takes items cl, cl + ncl, ...
+// Sched::item(u, ra, rb0, ntn): pair-tile A row base, first B row, number of 256-column tiles of
+// work item u (B rows rb0 + t * 256).
 template <class Sched>
 __device__ __forceinline__ void t2_producer(const Sched &sc, const T2Smem &s, const CUtensorMap *a_hi,
                                             const CUtensorMap *a_lo, const CUtensorMap *b_hi,
                                             const CUtensorMap *b_lo, int nkb, uint32_t cr, int hint) {
-  // hint: L2 policy of the A / B operand loads -- 0 normal / normal, 1 evict_last / evict_last,
-  // 2 evict_last / normal, 3 normal / evict_last, 4 evict_last / evict_first
-  const uint64_t keep = (hint == 1 || hint == 2 || hint == 4) ? l2_policy_evict_last() : l2_policy_evict_normal();
-  const uint64_t bpol = (hint == 1 || hint == 3) ? l2_policy_evict_last()
-                        : hint == 4              ? l2_policy_evict_first()
-                                                 : l2_policy_evict_normal();
+  const T2Policy pol(hint);
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t u = cl; u < sc.nitems; u += ncl) {
-    int ra, rb0, ntn;
-    sc.item(u, ra, rb0, ntn);
-    for (int t = 0; t < ntn; ++t) {
-      const int rb = rb0 + t * 256;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&s.empty[stage], phase ^ 1);
-        uint8_t *st = s.stages + stage * T2_STAGE_BYTES;
-        if (cr == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * T2_STAGE_BYTES);
-        const int kc = kb * TC_BK;
-        const int ar = ra + (int)cr * 128, br = rb + (int)cr * 128;
-        tma_load_2d_pair(st, a_hi, kc, ar, &s.full[stage], keep);
-        tma_load_2d_pair(st + T2_HALF_BYTES, a_lo, kc, ar, &s.full[stage], keep);
-        tma_load_2d_pair(st + 2 * T2_HALF_BYTES, b_hi, kc, br, &s.full[stage], bpol);
-        tma_load_2d_pair(st + 3 * T2_HALF_BYTES, b_lo, kc, br, &s.full[stage], bpol);
-        if (++stage == T2_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  }
+  for (int64_t u = cl; u < sc.nitems; u += ncl) t2_produce_item(sc, s, u, a_hi, a_lo, b_hi, b_lo, nkb, cr, pol, stage, phase);
 }
 
 

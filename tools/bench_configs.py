@@ -95,11 +95,11 @@ for name in a.configs.split(","):
     sym = (mat and (cfg["k"] <= 16 or (cfg["k"] <= 32 and a.kstore != "fp32")) and a.grid_rows <= 1
            and h.params.symmetric != kkm.SYM_OFF
            and (h.params.symmetric == kkm.SYM_ON or n >= 8192))  # make_plan's rule
-    vals = torch.tensor([init_ms, fit_ms, ph["spmm"], ph["cnorm"], ph["assign"], ph["init_gemm"]],
+    vals = torch.tensor([init_ms, fit_ms, ph["spmm"], ph["cnorm"], ph["assign"], ph["init_gemm"], ph["a2_kernel"]],
                         dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    init_ms, fit_ms, spmm_ms, cn_ms, as_ms, gemm_ms = vals.tolist()
+    init_ms, fit_ms, spmm_ms, cn_ms, as_ms, gemm_ms, a2k_ms = vals.tolist()
     if rank == 0:
         d = Xl.shape[1]
         B = -(-n // world)
@@ -113,8 +113,8 @@ for name in a.configs.split(","):
                         ("streaming (f1 upper triangle)" if cfg["k"] <= 16 and a.grid_rows <= 1
                          else "streaming")),
                "sec_per_iter": loop_ms / 1e3, "total_clustering_s": (init_ms + fit_ms) / 1e3,
-               "init_s": init_ms / 1e3, "phases_ms_per_iter": {"a2": spmm_ms / it, "a3": cn_ms / it,
-                                                             "a4": as_ms / it},
+               "init_s": init_ms / 1e3, "phases_ms_per_iter": {"a2": spmm_ms / it, "a2_kernel": a2k_ms / it,
+                                                             "a3": cn_ms / it, "a4": as_ms / it},
                "final_J": float(J[-1]), "gen_s": round(gen_s, 1)}
         useful = 2.0 * B * n * d
         if mat:

@@ -1,5 +1,5 @@
 """Per-iteration, per-rank phase times (a2 / a3 / a4, CUDA events inside kkm_fit) of one
-config: fit() is called with max_iter = 1 repeatedly and phase_ms() differenced. Launch with
+config (a2 also split into the kernel and the rest): fit() is called with max_iter = 1 repeatedly and phase_ms() differenced. Launch with
 torchrun for N > 1. Diagnoses one-time costs and rank imbalance (e.g. the 1.5D a3 time)."""
 import argparse
 import json
@@ -50,7 +50,7 @@ rows, prev = [], h.phase_ms()
 for t in range(a.iters):
     h.fit()
     cur = h.phase_ms()
-    rows.append([cur[p] - prev[p] for p in ("spmm", "cnorm", "assign")])
+    rows.append([cur[p] - prev[p] for p in ("spmm", "cnorm", "assign", "a2_kernel")])
     prev = cur
 mine = torch.tensor([[init_ms] + [x for r in rows for x in r]], dtype=torch.float64, device=dev)
 if world > 1:
@@ -62,12 +62,14 @@ else:
 if rank == 0:
     for r in range(world):
         v = allr[r]
-        its = v[1:].reshape(a.iters, 3)
+        its = v[1:].reshape(a.iters, 4)
         print(json.dumps({"config": a.config, "grid": f"{a.grid_rows}x{world // a.grid_rows}", "rank": r,
                           "init_ms": round(float(v[0]), 2),
                           "a2_ms": [round(float(x), 3) for x in its[:, 0]],
                           "a3_ms": [round(float(x), 3) for x in its[:, 1]],
-                          "a4_ms": [round(float(x), 3) for x in its[:, 2]]}))
+                          "a4_ms": [round(float(x), 3) for x in its[:, 2]],
+                          # the a2 kernel alone; a2 - a2_kernel = sort / exchange / reduction around it
+                          "a2_kernel_ms": [round(float(x), 3) for x in its[:, 3]]}))
 h.destroy()
 if comm:
     kkm.comm_destroy(comm)
