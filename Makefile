@@ -17,10 +17,16 @@ $(PKG)/libkkm.so: $(SRCS)
 oracle/liboracle.so: oracle/kkm_oracle.c
 	gcc -O2 -fopenmp -fPIC -shared -std=c11 -fno-fast-math -ffp-contract=off $< -o $@ -lm
 
+# A/B experiment builds: make exp NAME=x EXP="-DKKM_EXP_..." -> build/libkkm_x.so (KKM_LIBKKM selects it)
+exp: $(SRCS)
+	mkdir -p build
+	$(NVCC) $(NVFLAGS) $(EXP) $(PKG)/csrc/kkm_api.cu -o build/libkkm_$(NAME).so -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath=$(NCCL_DIR)/lib
+
 sass: $(PKG)/libkkm.so
 	cuobjdump -sass $(PKG)/libkkm.so > build_sass.txt
 
 clean:
 	rm -f $(PKG)/libkkm.so oracle/liboracle.so
 
-.PHONY: all clean sass
+.PHONY: all clean sass exp

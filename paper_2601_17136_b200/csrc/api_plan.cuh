@@ -223,27 +223,26 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.chunks_per_split = 0;
   }
   P.sym = P.materialize && sym_ok;
-  // f1 on the streaming path: upper-triangle pair tiles of the label-sorted K, work units
-  // (row tile, first column tile, count) of <= 512 tiles, spread over the ranks largest first
+  // f1 on the streaming path: upper-triangle pair tiles of the label-sorted K as work units
+  // (row tile, first column tile, count), in an L2-friendly order; each rank takes a contiguous
+  // run of that order holding ~1/P of the tiles, and its pairs take the run's units dynamically
+  // (ssym.cuh), so the units in flight on a GPU stay consecutive in the order
   P.ssym = !P.materialize && ssym_elig && P.tc;
   P.units.clear();
   if (P.ssym) {
     const int64_t Tt = ceil_div(n, 256);
     std::vector<int4> all;
-    // units = (row tile, globally aligned block of <= BS column tiles); a rank's units run
-    // block-major (below), so the ~74 pairs running at once sweep the same block of B tiles
-    // with different row tiles: the block (BS x 256 rows of the split operand) and the pairs'
-    // A tiles stay L2-resident
-    int64_t BS = 16;  // measured at n = 200k: 8 / 16 / 32 tiles -> 67.2 / 68.1 / 70.4 ms, DRAM 134 vs 205 GB (16 vs 32)
-    if (const char *e = std::getenv("KKM_SSYM_BS")) BS = std::max<int64_t>(1, std::atoll(e));
-    const bool tile_major = std::getenv("KKM_SSYM_TILE_MAJOR") != nullptr;  // (the round-1 order, A/B only)
-    // G > 0: single-tile units in a supertile raster -- G x G patches of the upper triangle, patch
-    // by patch, each patch column by column -- so the ~74 tiles in flight cover a compact patch
-    // (~9 row tiles x ~9 column tiles: ~15 MB of operands in L2 instead of 74 row tiles + a block)
-    // (W: column tiles per unit inside a patch)
-    int64_t G = 0, W = 1;
+    // Default: a G x G supertile raster -- patches of G row tiles x G column tiles of the upper
+    // triangle, patch row by patch row, inside a patch W column tiles at a time across its G row
+    // tiles; a unit = (row tile, W column tiles). The ~74 units in flight cover ~G row tiles x a
+    // few W-groups of columns: ~30 MB of split operands in L2, each B tile read by G units in a
+    // row. Measured at n = 1M (dynamic schedule): G x W = 32 x 16 1.50-1.52 s, DRAM 258 GB, L2 hit
+    // 94 %; 16 x 4 1.56 s; the block-major order (G = 0: units = (row tile, aligned block of BS
+    // column tiles), block by block) 1.55 s, DRAM 959 GB. KKM_SSYM_G / _W / _BS: A/B runs.
+    int64_t G = 32, W = 16, BS = 16;
     if (const char *e = std::getenv("KKM_SSYM_G")) G = std::max<int64_t>(0, std::atoll(e));
     if (const char *e = std::getenv("KKM_SSYM_W")) W = std::max<int64_t>(1, std::atoll(e));
+    if (const char *e = std::getenv("KKM_SSYM_BS")) BS = std::max<int64_t>(1, std::atoll(e));
     if (G > 0) {
       for (int64_t I = 0; I * G < Tt; ++I)
         for (int64_t J = I; J * G < Tt; ++J) {
@@ -255,31 +254,22 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
             }
         }
     } else {
-      for (int64_t tm = 0; tm < Tt; ++tm)
-        for (int64_t b = tm / BS; b * BS < Tt; ++b) {
+      for (int64_t b = 0; b * BS < Tt; ++b)
+        for (int64_t tm = 0; tm < std::min(Tt, (b + 1) * BS); ++tm) {
           const int64_t a = std::max(tm, b * BS), e = std::min(Tt, (b + 1) * BS);
           all.push_back(make_int4((int)tm, (int)a, (int)(e - a), 0));
         }
     }
-    std::vector<int64_t> load(nranks, 0);
-    std::vector<int> order(all.size());
-    for (size_t i = 0; i < all.size(); ++i) order[i] = (int)i;
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return all[x].z > all[y].z; });
-    std::vector<char> mine(all.size(), 0);
-    for (int i : order) {
-      int r = 0;
-      for (int q = 1; q < nranks; ++q)
-        if (load[q] < load[r]) r = q;
-      load[r] += all[i].z;
-      if (r == rank) mine[i] = 1;
+    // contiguous runs by cumulative tile count: rank r takes the units whose first tile falls in
+    // [r total / P, (r + 1) total / P) of the running count (imbalance <= one unit)
+    int64_t total = 0;
+    for (const int4 &u : all) total += u.z;
+    int64_t cum = 0;
+    for (const int4 &u : all) {
+      const int64_t owner = std::min<int64_t>(nranks - 1, cum * nranks / std::max<int64_t>(total, 1));
+      if (owner == rank) P.units.push_back(u);
+      cum += u.z;
     }
-    for (size_t i = 0; i < all.size(); ++i)
-      if (mine[i]) P.units.push_back(all[i]);
-    if (!tile_major && G == 0)  // block-major order on the rank: (column block, row tile)
-      std::stable_sort(P.units.begin(), P.units.end(), [&](const int4 &x, const int4 &y) {
-        const int64_t bx = x.y / BS, by = y.y / BS;
-        return bx != by ? bx < by : x.x < y.x;
-      });
     P.nsplit = 1;
   }
   P.tbands.clear();

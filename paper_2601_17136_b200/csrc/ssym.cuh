@@ -146,7 +146,11 @@ __device__ __forceinline__ void ss_chunk(float (&x)[32], int64_t p0, const float
   // column part: column p0 + l gets the sum over the warp's rows of each row label
   if (r0 == r1) {  // one label (almost always): the butterfly consumes x
     const float cs = lane_column_sum(x, lane);
+#ifdef KKM_EXP_NO_COLPART  // (A/B experiment builds only: the column-part atomics removed)
+    if (p0 + lane < n && cs == -1.2345e-30f) red_add_s64(Sfix + (p0 + lane) * k + r0, ch_fix(cs, fx_scale));
+#else
     if (p0 + lane < n) red_add_s64(Sfix + (p0 + lane) * k + r0, ch_fix(cs, fx_scale));
+#endif
   } else if (row_ok) {  // the rows straddle a segment boundary: element by element
 #pragma unroll
     for (int q = 0; q < 32; ++q)
@@ -243,6 +247,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
         ch_stage_columns(cn, snorms, fp16 ? srscale : nullptr, pbase, n, kp.kind == 2, lane);
         float va[32], vb[32];
         ch_drain(s, tq, nch, chain, va, vb, lane);
+#ifdef KKM_EXP_NO_EPI  // (A/B experiment builds only: drain, no epilogue arithmetic)
+        if (va[0] == -1.2345e-30f && vb[31] == 1.f) Sfix[p] = 1;
+        continue;
+#endif
         if (rw >= n) continue;
         ss_chunk<KIND>(va, pbase, cn, kp, rk, diag, p, row_ok, n, seg, k, cseg, cur, run, r0, r1, mylab, lane, fx_scale,
                  Sfix);

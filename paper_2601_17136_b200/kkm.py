@@ -9,7 +9,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libkkm.so")
+# KKM_LIBKKM: an alternative build of the same library (`make exp`, A/B experiments only)
+_LIB_PATH = os.environ.get("KKM_LIBKKM") or os.path.join(_HERE, "libkkm.so")
 
 OK, EINVAL, ELABEL, ENOMEM, EUNSUP, ECUDA, ENCCL, ESTATE = range(8)
 _NAMES = {1: "KKM_EINVAL", 2: "KKM_ELABEL", 3: "KKM_ENOMEM", 4: "KKM_EUNSUP", 5: "KKM_ECUDA",

@@ -132,3 +132,20 @@ def test_virtual_ranks_iteration_equals_oracle(case, P):
     assert abs(J - ref["J"]) <= 1e-12 * abs(ref["J"])
     assert np.array_equal(new, ref["new_labels"])
     assert np.allclose(D, ref["Dfull"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sym_stream_ranks_balanced_at_config4_size(P):
+    """Streaming f1 at the config-4 size (n = 1M): each rank's contiguous run of the unit order
+    holds 1/P of the upper-triangle tiles to within one unit (16 tiles), and the runs together
+    are the whole triangle."""
+    n = 1_000_000
+    T = -(-n // 256)
+    tiles = []
+    for r in range(P):
+        info, pc = kkm.plan_query(params(10, kkm.PATH_STREAM, kkm.SYM_AUTO, kkm.KSTORE_AUTO, 1), n, 784, rank=r,
+                                  nranks=P)
+        assert info.layout == kkm.LAYOUT_SYM_STREAM
+        tiles.append(int(np.sum(-(-pc[:, 3] // 256))))   # column tiles of each unit
+    assert sum(tiles) == T * (T + 1) // 2
+    assert max(tiles) - min(tiles) <= 2 * 16, tiles
