@@ -132,6 +132,8 @@ def test_workspace_size_and_errors():
         with pytest.raises(kkm.KKMError, match="EUNSUP"):
             kkm.workspace_size(q, 60000, 784, rank=0, nranks=2 if field == "grid_rows" else 1)
     q = kkm.default_params()
-    q.kstore, q.k = kkm.KSTORE_FP16, 17
+    q.kstore, q.k = kkm.KSTORE_FP16, 32  # 16-bit bands: 16- or 32-label one-hots (spmm_tc_kernel<NL>)
+    assert kkm.workspace_size(q, 60000, 784) > 0
+    q.k = 33
     with pytest.raises(kkm.KKMError, match="EUNSUP"):
         kkm.workspace_size(q, 60000, 784)

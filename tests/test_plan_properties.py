@@ -40,7 +40,7 @@ def test_workspace_plan(n, d, k, nranks, grid_rows, path, prec, sym, inc, kind, 
     if path == kkm.PATH_STREAM:
         assert prec != kkm.PREC_FP32_SIMT
     if kstore in (kkm.KSTORE_FP16, kkm.KSTORE_FP16X2):  # 16-bit bands: materialised 1D f1 only
-        assert prec != kkm.PREC_FP32_SIMT and k <= 16 and grid_rows <= 1 and sym != kkm.SYM_OFF
+        assert prec != kkm.PREC_FP32_SIMT and k <= 32 and grid_rows <= 1 and sym != kkm.SYM_OFF  # NL = 16 or 32
         assert path != kkm.PATH_STREAM
         # the bands (about n^2 / 2 values over the ranks) at 2 or 4 bytes per value
         tot = sum(sizes)
