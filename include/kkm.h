@@ -98,8 +98,10 @@ extern "C" {
 #define KKM_PH_INIT_PREP 0  /* X copy/gather, norms, bf16 split, diag           */
 #define KKM_PH_INIT_GEMM 1  /* a1: K = kappa(X X^T) materialisation             */
 #define KKM_PH_SPMM 2       /* a2 per fit (sum over iterations)                 */
-#define KKM_PH_CNORM 3      /* a3 incl. its collective                          */
-#define KKM_PH_ASSIGN 4     /* a4 incl. the labels allgather                    */
+#define KKM_PH_CNORM 3      /* a3 incl. its collective; where a3 and a4 run as ONE
+                               launch (single-CTA small n; the grid-wide update of
+                               the 16-bit band paths, k <= 64) it includes a4      */
+#define KKM_PH_ASSIGN 4     /* a4 incl. the labels allgather (0 when fused into a3) */
 #define KKM_PH_A2_KERNEL 5  /* the dominant a2 kernel alone (spmm_tc over the 16-bit bands /
                                spmm_sym / spmm_onehot / spmm_group / the streaming kernels),
                                summed over the loop's launches */

@@ -172,7 +172,7 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
             P.kplanes, cpart);
       CKL();
       if (nl32 && !P.tslabs.empty()) {  // the column parts, summed over this rank's slabs
-        ts_colpart_reduce_kernel<<<dim3((unsigned)ceil_div(P.n, 256), (unsigned)k), 256, 0, h->st>>>(
+        ts_colpart_reduce_kernel<<<dim3((unsigned)ceil_div(P.n, 4 * 256), (unsigned)k), 256, 0, h->st>>>(
             cpart, (const TsSlab *)(h->ws + P.o_tslabs), (int)P.tslabs.size(), P.n, k, P.npad, h->tfxm, Sx);
         CKL();
       }

@@ -43,6 +43,28 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
   return KKM_OK;
 }
 
+// a3 + a4 in one cooperative launch (update_grid_kernel): the int64 S of the one-rank / replicated
+// f1 paths, k <= UG_MAX_K, no peer exchange. New labels into lab[cur^1], sizes into sizes[cur^1].
+bool use_update_grid(const kkm_ctx *h) { return h->ug_grid > 0 && !h->p2p; }
+int run_update_grid(kkm_ctx *h, double *J_out, unsigned long long *changed_out) {
+  const Plan &P = h->P;
+  const int nx = h->cur ^ 1;
+  const long long *Sfix = h->tSfix;
+  int64_t rows_pad = P.npad, nrows = P.a_n;
+  int k = P.k;
+  double inv = h->tfx_inv;
+  const int32_t *sizes = h->sizes[h->cur], *cl = h->lab[h->cur] + P.a_row0;
+  const double *diag = h->diag;
+  double *E = h->E, *bp = h->blockpart, *cn = h->cnorm;
+  unsigned *bar = h->a3ctr;
+  int32_t *cl_new = h->lab[nx] + P.a_row0, *sz_next = h->sizes[nx];
+  void *args[] = {&Sfix, &rows_pad, &nrows, &k, &inv, &sizes, &cl, &diag, &E, &bp, &bar, &cn, &J_out, &cl_new,
+                  &sz_next, &changed_out};
+  const unsigned grid = (unsigned)std::min<int64_t>({ceil_div(P.a_n, UG_THREADS), (int64_t)h->ug_grid, (int64_t)P.nfin});
+  CK(cudaLaunchCooperativeKernel((const void *)update_grid_kernel, grid, UG_THREADS, args, 0, h->st));
+  return KKM_OK;
+}
+
 // a4 + the V update: new labels into lab[cur^1], sizes into sizes[cur^1], allgather.
 int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
   const Plan &P = h->P;
@@ -51,7 +73,7 @@ int run_assign(kkm_ctx *h, unsigned long long *changed_out) {
     const int th = 256;
     assign_kernel<<<(unsigned)ceil_div(P.a_n, th), th, (size_t)P.k * 4, h->st>>>(
         h->E, P.a_n, P.k, h->cnorm, h->diag, h->lab[h->cur] + P.a_row0, h->lab[nx] + P.a_row0,
-        h->sizes[nx], changed_out, h->Dfull);
+        h->sizes[nx], changed_out, nullptr);  // (Dfull: formed on demand by kkm_debug_read)
     CKL();
   }
   if (P.nranks > 1 && !P.repl) {  // the changed count is global too: every rank takes the same control path

@@ -34,6 +34,7 @@ struct kkm_ctx {
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   int num_sms = 148;
+  int ug_grid = 0;  // co-resident blocks of update_grid_kernel (0: not used by this plan)
   uint8_t *ws = nullptr;
   float *Xf = nullptr, *norms = nullptr, *K = nullptr;
   float *mean = nullptr;  // Gaussian: the column means X was centered on (0 otherwise)

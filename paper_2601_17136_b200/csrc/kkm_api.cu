@@ -448,6 +448,14 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     rc = agree_min(h, &want);
     if (rc == KKM_OK && want) rc = setup_p2p(h);
   }
+  if (rc == KKM_OK && P.a3fix && P.k <= UG_MAX_K && P.a_n > 0) {  // a3 + a4 as one cooperative launch
+    int coop = 0, per_sm = 0, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, update_grid_kernel, UG_THREADS, 0) == cudaSuccess)
+      h->ug_grid = per_sm * h->num_sms;
+    cudaGetLastError();
+  }
   if (rc) {
     delete h;
     return rc;
@@ -496,6 +504,9 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
           S, ns, P.n, rows_pad, P.k, h->sizes[h->cur], h->lab[h->cur], h->diag, h->E, h->cnorm, h->J + t, 1,
           h->lab[h->cur ^ 1], h->sizes[h->cur ^ 1], h->changed + t, h->Dfull);
       CKL();
+      if (timing) CKR(rec(ev));
+    } else if (use_update_grid(h)) {  // a3 + a4 in one launch (reported as a3)
+      CKR(run_update_grid(h, h->J + t, h->changed + t));
       if (timing) CKR(rec(ev));
     } else {
       CKR(run_cnorm(h, S, ns, rows_pad, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
@@ -722,7 +733,12 @@ int kkm_debug_read(kkm_handle h, int32_t what, void *dst) {
       CKR(copy_any(h, dst, h->sizes[h->have_last ? prev : h->cur], (size_t)P.k * 4));
       break;
     case KKM_DBG_DIAG: CKR(copy_any(h, dst, h->diag + (P.row0 - P.a_row0), (size_t)P.nloc * 8)); break;
-    case KKM_DBG_DFULL:
+    case KKM_DBG_DFULL:  // formed from the last iteration's E and c (the expression of a4)
+      if (P.a_n > 0) {
+        dfull_kernel<<<(unsigned)ceil_div(P.a_n * P.k, 256), 256, 0, h->st>>>(h->E, P.a_n, P.k, h->cnorm, h->diag,
+                                                                            h->Dfull);
+        CKL();
+      }
       CKR(copy_any(h, dst, h->Dfull + (P.row0 - P.a_row0) * P.k, (size_t)P.nloc * P.k * 8));
       break;
     case KKM_DBG_LABELS_PREV:

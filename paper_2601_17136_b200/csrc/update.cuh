@@ -347,6 +347,183 @@ __global__ void moved_key_kernel(const int32_t *__restrict__ cl_old, const int32
   key[i] = v;
 }
 
+// ---- a3 + a4 in ONE grid-wide launch over the int64 fixed-point S (the 16-bit band / f1 paths on
+// one rank or replicated, k <= UG_MAX_K): a cooperative launch (all blocks co-resident) with one
+// grid barrier. Phase 1: z_i = E(i, cl_i) = (S(i, cl_i) 2^-s) / |L_cl_i| (Eq. z) -- ONE S value per
+// row -- and per-cluster sums of z plus sum_i (K_ii - z_i), reduced per warp by a 31-shuffle
+// reduce-scatter butterfly (lane l ends with cluster l's sum) and per block over warps in order,
+// into blockpart. Barrier. Every block sums blockpart over the blocks in the same fixed order
+// (so every block holds the same c and J, Eqs. c, and A8) -- no second launch. Phase 2: per row
+// all k S values, E = S 2^-s / |L_c| (bitwise the value finalize stores), D = -2E + c, the lowest-
+// index argmin (A6), new labels, the exact integer size histogram and the changed count. The E
+// rows are stored (debug reads); the full distances are formed on demand (dfull_kernel).
+// Replaces finalize + assign (two launches, an E round trip and a serial last-block tail: 31 us
+// at config 2, k = 10; 81 us at k = 32).
+constexpr int UG_THREADS = 256;
+constexpr int UG_MAX_K = 64;
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {  // bar[0]: arrivals, bar[1]: generation
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = *reinterpret_cast<volatile unsigned *>(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned *>(bar) = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      uint32_t ns = 32;
+      while (*reinterpret_cast<volatile unsigned *>(bar + 1) == gen) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
+    const long long *__restrict__ Sfix, int64_t rows_pad, int64_t nrows, int k, double inv,
+    const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl, const double *__restrict__ diag,
+    double *__restrict__ E, double *__restrict__ blockpart, unsigned *__restrict__ bar, double *__restrict__ cnorm_out,
+    double *__restrict__ J_out, int32_t *__restrict__ cl_new, int32_t *__restrict__ sizes_next,
+    unsigned long long *__restrict__ changed_out) {
+  __shared__ double wpart[UG_THREADS / 32][UG_MAX_K + 1];
+  __shared__ double cn[UG_MAX_K];
+  __shared__ int hist[UG_MAX_K];
+  __shared__ unsigned long long nchg;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = UG_THREADS / 32;
+  const int64_t stride = (int64_t)gridDim.x * UG_THREADS;
+  if (blockIdx.x == 0) {  // zeroed before the barrier, accumulated after it
+    for (int c = t; c < k; c += UG_THREADS) sizes_next[c] = 0;
+    if (t == 0) *changed_out = 0ull;
+  }
+  // ---- phase 1: per-cluster sums of z and sum (K_ii - z_i)
+  double acc0 = 0.0, acc1 = 0.0, accJ = 0.0;  // lane l: clusters l and l + 32
+  for (int64_t base = (int64_t)blockIdx.x * UG_THREADS + (t & ~31); base < nrows; base += stride) {
+    const int64_t i = base + lane;
+    int li = -1;
+    double zi = 0.0, ji = 0.0;
+    if (i < nrows) {
+      li = cl[i];
+      const int32_t sz = sizes[li];
+      const double sv = 0.0 + (double)Sfix[(int64_t)li * rows_pad + i] * inv;
+      zi = sz > 0 ? sv / (double)sz : 0.0;
+      ji = diag[i] - zi;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h * 32 >= k) break;
+      double v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = (li == h * 32 + q) ? zi : 0.0;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {  // reduce-scatter butterfly: lane l keeps the sum of v[l]
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int q = 0; q < o; ++q) {
+          const double send = up ? v[q] : v[q + o];
+          const double keep = up ? v[q + o] : v[q];
+          v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (h == 0) acc0 += v[0];
+      else acc1 += v[0];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ji += __shfl_xor_sync(0xffffffffu, ji, o);
+    accJ += ji;
+  }
+  // lane l of every warp: its clusters' partials; the butterfly leaves cluster l on lane
+  // bitreverse-free position l (each level keeps the half selected by the lane bit)
+  if (lane < k) wpart[w][lane] = acc0;
+  if (lane + 32 < k) wpart[w][lane + 32] = acc1;
+  if (lane == 0) wpart[w][k] = accJ;
+  __syncthreads();
+  for (int c = t; c <= k; c += UG_THREADS) {
+    double sum = 0.0;
+    for (int q = 0; q < nw; ++q) sum += wpart[q][c];
+    blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sum;
+  }
+  grid_barrier(bar);
+  // ---- c and J: every block sums the block partials in the same fixed order
+  for (int c = w; c <= k; c += nw) {
+    double sum = 0.0;
+    int b = lane;
+    for (; b + 32 * 7 < (int)gridDim.x; b += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(blockpart + (int64_t)(b + 32 * u) * (k + 1) + c);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; b < (int)gridDim.x; b += 32) sum += __ldcg(blockpart + (int64_t)b * (k + 1) + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+      if (c < k) {
+        const int32_t sz = sizes[c];
+        const double v = sz > 0 ? sum / (double)sz : __longlong_as_double(0x7ff0000000000000LL);  // +inf (A7)
+        cn[c] = v;
+        if (blockIdx.x == 0) cnorm_out[c] = v;
+      } else if (blockIdx.x == 0) {
+        *J_out = sum;  // sum_i (K_ii - z_i) = tr K - sum_c |L_c| c(c) (A8)
+      }
+    }
+  }
+  for (int c = t; c < k; c += UG_THREADS) hist[c] = 0;
+  if (t == 0) nchg = 0ull;
+  __syncthreads();
+  // ---- phase 2: E, D, argmin, sizes, changed
+  unsigned changed = 0;
+  for (int64_t i = (int64_t)blockIdx.x * UG_THREADS + t; i < nrows; i += stride) {
+    int best = 0;
+    double bd = __longlong_as_double(0x7ff0000000000000LL);
+    for (int c0 = 0; c0 < k; c0 += 16) {
+      long long sv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) sv[q] = c0 + q < k ? Sfix[(int64_t)(c0 + q) * rows_pad + i] : 0ll;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int c = c0 + q;
+        if (c < k) {
+          const double s = 0.0 + (double)sv[q] * inv;
+          const int32_t sz = sizes[c];
+          const double e = sz > 0 ? s / (double)sz : 0.0;
+          if (E) E[i * k + c] = e;
+          const double cv = cn[c];
+          const double dsh = isinf(cv) ? cv : fma(-2.0, e, cv);
+          if (dsh < bd) {
+            bd = dsh;
+            best = c;
+          }
+        }
+      }
+    }
+    cl_new[i] = best;
+    changed += best != cl[i];
+    atomicAdd(&hist[best], 1);
+  }
+  const unsigned wc = __reduce_add_sync(0xffffffffu, changed);
+  if (lane == 0 && wc) atomicAdd(&nchg, (unsigned long long)wc);
+  __syncthreads();
+  for (int c = t; c < k; c += UG_THREADS)
+    if (hist[c]) atomicAdd(&sizes_next[c], hist[c]);
+  if (t == 0 && nchg) atomicAdd(changed_out, nchg);
+}
+
+// Dfull(i, c) = K_ii + D(i, c) from the stored E and c (debug reads; the same expression as assign).
+__global__ void dfull_kernel(const double *__restrict__ E, int64_t nrows, int k, const double *__restrict__ cnorm,
+                             const double *__restrict__ diag, double *__restrict__ Dfull) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows * k) return;
+  const int64_t i = t / k;
+  const int c = (int)(t % k);
+  const double cn = cnorm[c];
+  Dfull[t] = diag[i] + (isinf(cn) ? cn : fma(-2.0, E[t], cn));
+}
+
 }  // namespace kkm
 
 namespace kkm {

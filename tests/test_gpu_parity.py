@@ -99,16 +99,25 @@ def test_har_like_gaussian_teacher_forced(precision):
 
 @pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
 def test_many_clusters_multipass(precision):
-    """k = 21 > 16: the label-sorted-group SpMM (v2); streaming: 2 launches of <= 16 clusters."""
+    """k = 21 > 16: the label-sorted-group SpMM (v2); streaming: one launch (running sums per segment)."""
     X = synth.blobs(1500, 16, 21, seed=3, sep=4.0)
     teacher_forced(X, 21, oracle.LINEAR, iters=3, precision=precision)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
 def test_very_many_clusters(precision):
-    """k = 70 > 64: the one-hot SpMM in ceil(k/16) passes; streaming: 5 cluster-group launches."""
+    """k = 70 > 64: the one-hot SpMM in ceil(k/16) passes; streaming: one launch."""
     X = synth.blobs(600, 8, 70, seed=6, sep=3.0)
     teacher_forced(X, 70, oracle.POLY, 0.2, 1.0, 2, iters=2, precision=precision)
+
+
+@pytest.mark.parametrize("k", [256, 900])
+@pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)
+def test_huge_k(k, precision):
+    """k >= 192: a3's per-cluster partials need > 48 KB of dynamic smem (opt-in per device); k = 900
+    is KKM_MAX_K (the streaming kernels' segment table in smem). Teacher-forced against the oracle."""
+    X = synth.blobs(2 * k + 300, 8, k, seed=k, sep=3.0)
+    teacher_forced(X, k, oracle.GAUSSIAN, 0.5, iters=2, precision=precision)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS, ids=PREC_IDS)

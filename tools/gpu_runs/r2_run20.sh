@@ -9,3 +9,7 @@ for c in har200k mnist1m; do
   done
 done
 timeout 1800 python -m pytest tests/test_multi_gpu.py -m gpu -q -rs > gpurun_out/r2_20_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2_20_pytest.log
+for c in mnist1m mnist8m; do
+  it=5; [ $c = mnist8m ] && it=2
+  timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29620 tools/bench_configs.py --configs $c --iters $it > gpurun_out/r2_20_cfg_$c.log 2>&1; echo "$c 1x4 rc=$?"; tail -1 gpurun_out/r2_20_cfg_$c.log | cut -c1-420
+done
