@@ -167,7 +167,11 @@ typedef struct kkm_ctx *kkm_handle;
 #define KKM_LAYOUT_SYM_STREAM 4   /* f1: upper-triangle tiles of the label-sorted K, recomputed (ssym) */
 #define KKM_XCHG_NONE 0           /* one rank                                                           */
 #define KKM_XCHG_PARTIALS 1       /* per iteration: allgather of (k+1) partials, labels, sizes (1D/1.5D) */
-#define KKM_XCHG_S_ALLREDUCE 2    /* per iteration: one allreduce of S (n x k), a3/a4 replicated        */
+#define KKM_XCHG_S_ALLREDUCE 2    /* per iteration: one allreduce of S (n x k), a3/a4 replicated; opt-in
+                                     KKM_LSA=1 (16-bit bands, k <= 64, <= 8 ranks on one NVLink
+                                     domain): no allreduce -- the fused a3/a4 kernel reads every
+                                     rank's S from NCCL symmetric windows and splits the rows over
+                                     the ranks                                     */
 #define KKM_XCHG_S_REDUCE_SCATTER 3 /* per iteration: reduce-scatter of S to the 1D blocks + partials   */
 typedef struct kkm_plan_info {
   int32_t path;          /* effective KKM_PATH_MATERIALIZE or KKM_PATH_STREAM                    */
@@ -322,7 +326,9 @@ int kkm_phase_ms(kkm_handle h, float *ms);
  * init (for bench.py's gpu_launches). */
 int kkm_launch_count(kkm_handle h, int64_t *count);
 
-/* Frees the handle (workspace and communicator stay the caller's). */
+/* Frees the handle (workspace and communicator stay the caller's). With the opt-in peer-memory
+ * update (KKM_LSA=1, see KKM_XCHG_S_ALLREDUCE) it also deregisters the NCCL symmetric window,
+ * which is collective: every rank destroys its handle, before kkm_comm_destroy. */
 int kkm_destroy(kkm_handle h);
 
 /* Thread-local message for the last non-zero status of this thread. */

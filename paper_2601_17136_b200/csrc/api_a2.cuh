@@ -156,6 +156,10 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
     if (h->p2p) {  // this epoch's half of the own exchange buffer (the other half may still be read)
       ++h->epoch;
       Sx = (long long *)(h->xbuf + (h->epoch & 1) * (size_t)P.npad * k * 8);
+    } else if (h->lsa) {  // alternate parities of the symmetric window: a peer may still read the
+      h->ls_par ^= 1;     // other one (its reads end before it reaches the next cross-rank barrier)
+      Sx = (long long *)(h->lsbuf + (size_t)h->ls_par * h->ls_sb);
+      h->tSfix = Sx;
     }
     CK(cudaMemsetAsync(Sx, 0, (size_t)P.npad * k * 8, h->st));
     a2_mark(h);
@@ -182,6 +186,10 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
       peer_signal_kernel<<<1, 1, 0, h->st>>>(
           (unsigned long long *)(h->xbuf + 2 * (size_t)P.npad * k * 8), h->epoch);
       CKL();
+      *s_out = nullptr;
+      return KKM_OK;
+    }
+    if (h->lsa && h->ls_fused_next) {  // update_grid_kernel<true> sums the ranks' S itself
       *s_out = nullptr;
       return KKM_OK;
     }

@@ -45,6 +45,9 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
 
 // a3 + a4 in one cooperative launch (update_grid_kernel): the int64 S of the one-rank / replicated
 // f1 paths, k <= UG_MAX_K, no peer exchange. New labels into lab[cur^1], sizes into sizes[cur^1].
+// With the NVLink peer-memory window (h->lsa, in the fit loop) the launch is the distributed
+// variant: own rows only, S summed over the ranks while read, labels / sizes / changed stored into
+// every rank's copies, three cross-rank arrivals.
 bool use_update_grid(const kkm_ctx *h) { return h->ug_grid > 0 && !h->p2p; }
 int run_update_grid(kkm_ctx *h, double *J_out, unsigned long long *changed_out) {
   const Plan &P = h->P;
@@ -58,10 +61,27 @@ int run_update_grid(kkm_ctx *h, double *J_out, unsigned long long *changed_out) 
   double *E = h->E, *bp = h->blockpart, *cn = h->cnorm;
   unsigned *bar = h->a3ctr;
   int32_t *cl_new = h->lab[nx] + P.a_row0, *sz_next = h->sizes[nx];
+  const bool lsa = h->lsa && h->ls_fused_next;
+  LsaArgs L = h->lsargs;
+  if (lsa) {
+    nrows = P.nloc;
+    L.row0 = P.row0;
+    L.off_S = (size_t)h->ls_par * h->ls_sb;
+    L.off_lab_next = h->ls_off_lab + (size_t)nx * h->ls_lb;
+    L.off_sizes_next = h->ls_off_sizes + (size_t)nx * 4096;
+    L.off_changed = (size_t)((uint8_t *)changed_out - h->lsbuf);
+    L.target = (h->ls_epoch + 1) * (unsigned)P.nranks;
+    L.Sred = (long long *)(h->ws + P.o_tSfix);  // (the workspace S is free: S lives in the window)
+    h->ls_epoch += 3;
+  }
   void *args[] = {&Sfix, &rows_pad, &nrows, &k, &inv, &sizes, &cl, &diag, &E, &bp, &bar, &cn, &J_out, &cl_new,
-                  &sz_next, &changed_out};
-  const unsigned grid = (unsigned)std::min<int64_t>({ceil_div(P.a_n, UG_THREADS), (int64_t)h->ug_grid, (int64_t)P.nfin});
-  CK(cudaLaunchCooperativeKernel((const void *)update_grid_kernel, grid, UG_THREADS, args, 0, h->st));
+                  &sz_next, &changed_out, &L};
+  // (the distributed variant takes every co-resident block: its phase 0 is a latency-bound
+  // NVLink read of P copies, more threads = more loads in flight)
+  const int64_t need = lsa ? (int64_t)h->ug_grid : std::max<int64_t>(1, ceil_div(nrows, UG_THREADS));
+  const unsigned grid = (unsigned)std::min<int64_t>({need, (int64_t)h->ug_grid, (int64_t)P.nfin});
+  if (lsa) CK(cudaLaunchCooperativeKernel((const void *)update_grid_kernel<true>, grid, UG_THREADS, args, 0, h->st));
+  else CK(cudaLaunchCooperativeKernel((const void *)update_grid_kernel<false>, grid, UG_THREADS, args, 0, h->st));
   return KKM_OK;
 }
 

@@ -69,6 +69,20 @@ struct kkm_ctx {
                                      // (+64: this rank's timed-out word, checked by check_p2p)
   unsigned long long epoch = 0;
   unsigned long long p2p_timeout_ns = 0;
+  // Distributed a3/a4 over NVLink peer memory (16-bit bands, replicated plan, several ranks;
+  // api_exchange.cuh setup_lsa): an NCCL symmetric window per rank [2 parities of k x npad int64 S |
+  // 2 label buffers | 2 size histograms | changed counters | rank partials | flag page], mapped by
+  // every rank; S is summed by the fused a3/a4 kernel while it reads it (no allreduce)
+  bool lsa = false;
+  uint8_t *lsbuf = nullptr;            // own window (ncclMemAlloc)
+  ncclWindow_t lswin = nullptr;
+  ncclDevComm lsdev{};
+  LsaArgs lsargs{};                    // peer bases + section offsets (off_S etc. set per launch)
+  size_t ls_sb = 0, ls_off_lab = 0, ls_lb = 0, ls_off_sizes = 0, ls_off_changed = 0, ls_off_rankpart = 0,
+         ls_off_flag = 0;
+  int ls_par = 0;                      // parity of the S buffer the latest a2 wrote
+  bool ls_fused_next = false;          // the next a2's consumer sums S itself (no allreduce)
+  uint32_t ls_epoch = 0;               // cross-rank arrivals per rank so far
   // f4 fp16 K storage
   CUtensorMap *tmaps = nullptr;
   TsBand *tbands = nullptr;

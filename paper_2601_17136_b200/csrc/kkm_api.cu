@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <cmath>
@@ -452,9 +453,24 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
     int coop = 0, per_sm = 0, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, update_grid_kernel, UG_THREADS, 0) == cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, update_grid_kernel<true>, UG_THREADS, 0) == cudaSuccess)
       h->ug_grid = per_sm * h->num_sms;
     cudaGetLastError();
+  }
+  // Opt-in (KKM_LSA=1): a3/a4 distributed over the ranks inside the fused update, reading S from
+  // every rank's NCCL symmetric window over NVLink instead of an NCCL allreduce per iteration.
+  // Measured on 4 B200: the same per-iteration time as the allreduce + replicated
+  // update (0.398 vs 0.404 ms at config 2; three cross-rank arrivals cost what the allreduce did)
+  // and +50 ms of window registration per handle, so the default stays on NCCL. Every rank
+  // evaluates the same condition (same plan, env) and agrees before the collective setup.
+  if (rc == KKM_OK && P.repl && P.nranks > 1 && P.nranks <= LSA_MAX_RANKS && !h->p2p && P.a3fix &&
+      P.k <= UG_MAX_K) {
+    int want = 0;
+    if (const char *e = std::getenv("KKM_LSA")) want = h->ug_grid > 0 && std::atoi(e) == 1;
+    if (std::getenv("KKM_LSA_DEBUG"))
+      std::fprintf(stderr, "[kkm rank %d] lsa wish %d (ug_grid %d)\n", P.rank, want, h->ug_grid);
+    rc = agree_min(h, &want);
+    if (rc == KKM_OK && want) rc = setup_lsa(h);
   }
   if (rc) {
     delete h;
@@ -491,7 +507,12 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
       ns = 1;
       rows_pad = P.B;
     } else {
-      CKR(launch_spmm(h, h->lab[h->cur], &S, &ns));  // a2 (+ 1.5D reduce-scatter)
+      h->ls_fused_next = h->lsa && use_update_grid(h);  // (peer-memory window: no allreduce, run_update_grid)
+      const int arc = launch_spmm(h, h->lab[h->cur], &S, &ns);  // a2 (+ 1.5D reduce-scatter)
+      if (arc != KKM_OK) {
+        h->ls_fused_next = false;
+        return arc;
+      }
       if (P.inc && P.nloc > 0) {
         sinc_set_kernel<<<(unsigned)ceil_div(P.nloc * P.k, 256), 256, 0, h->st>>>(S, ns, rows_pad, P.nloc, P.k,
                                                                                    h->Sinc);
@@ -506,7 +527,9 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
       CKL();
       if (timing) CKR(rec(ev));
     } else if (use_update_grid(h)) {  // a3 + a4 in one launch (reported as a3)
-      CKR(run_update_grid(h, h->J + t, h->changed + t));
+      const int urc = run_update_grid(h, h->J + t, h->changed + t);
+      h->ls_fused_next = false;
+      CKR(urc);
       if (timing) CKR(rec(ev));
     } else {
       CKR(run_cnorm(h, S, ns, rows_pad, h->E, h->cnorm, h->J + t, h->sizes[h->cur ^ 1], h->changed + t));  // a3
@@ -557,6 +580,17 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
   CKR(sync_stream(h));
   CKR(check_p2p(h));
+  CKR(check_lsa(h));
+#ifdef KKM_EXP_LSA_STAMPS
+  if (h->lsa) {
+    unsigned long long st[10];
+    CK(cudaMemcpy(st, h->lsbuf + h->ls_off_flag + 32 * 8, sizeof(st), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[kkm rank %d] last update (us): wait1 %.1f ph0 %.1f ph1 %.1f gridbar %.1f sums %.1f wait2 %.1f ph2 %.1f "
+                 "gridbar %.1f wait3 %.1f\n", h->P.rank, (st[1] - st[0]) * 1e-3, (st[9] - st[1]) * 1e-3, (st[2] - st[9]) * 1e-3,
+                 (st[3] - st[2]) * 1e-3, (st[4] - st[3]) * 1e-3, (st[5] - st[4]) * 1e-3, (st[6] - st[5]) * 1e-3,
+                 (st[7] - st[6]) * 1e-3, (st[8] - st[7]) * 1e-3);
+  }
+#endif
   if (timing) {
     const std::vector<cudaEvent_t> &e5 = ev.v;
     for (size_t i = 0; i + 4 < e5.size(); i += 5) {  // the a2 phase includes the f3 S update
@@ -831,6 +865,12 @@ int kkm_launch_count(kkm_handle h, int64_t *count) {
 int kkm_destroy(kkm_handle h) {
   if (!h) return KKM_OK;
   cudaStreamSynchronize(h->st);
+  if (h->lsa) {  // collective: every rank destroys its handle before the communicator
+    ncclDevCommDestroy(h->comm, &h->lsdev);
+    ncclCommWindowDeregister(h->comm, h->lswin);
+    ncclMemFree(h->lsbuf);
+    cudaGetLastError();
+  }
   if (h->xbuf) {
     // no rank frees its exchange buffer while a peer may still read it: raise the own flag to
     // DONE (after the stream is idle) and wait, bounded, for every peer's DONE -- no NCCL here, so

@@ -348,19 +348,37 @@ __global__ void moved_key_kernel(const int32_t *__restrict__ cl_old, const int32
 }
 
 // ---- a3 + a4 in ONE grid-wide launch over the int64 fixed-point S (the 16-bit band / f1 paths on
-// one rank or replicated, k <= UG_MAX_K): a cooperative launch (all blocks co-resident) with one
-// grid barrier. Phase 1: z_i = E(i, cl_i) = (S(i, cl_i) 2^-s) / |L_cl_i| (Eq. z) -- ONE S value per
-// row -- and per-cluster sums of z plus sum_i (K_ii - z_i), reduced per warp by a 31-shuffle
-// reduce-scatter butterfly (lane l ends with cluster l's sum) and per block over warps in order,
-// into blockpart. Barrier. Every block sums blockpart over the blocks in the same fixed order
-// (so every block holds the same c and J, Eqs. c, and A8) -- no second launch. Phase 2: per row
-// all k S values, E = S 2^-s / |L_c| (bitwise the value finalize stores), D = -2E + c, the lowest-
-// index argmin (A6), new labels, the exact integer size histogram and the changed count. The E
-// rows are stored (debug reads); the full distances are formed on demand (dfull_kernel).
-// Replaces finalize + assign (two launches, an E round trip and a serial last-block tail: 31 us
-// at config 2, k = 10; 81 us at k = 32).
+// one rank or replicated, k <= UG_MAX_K): a cooperative launch (all blocks co-resident) with a grid
+// barrier. Phase 1: z_i = E(i, cl_i) = (S(i, cl_i) 2^-s) / |L_cl_i| (Eq. z) -- ONE S value per row
+// -- and per-cluster sums of z plus sum_i (K_ii - z_i), reduced per warp by a 31-shuffle
+// reduce-scatter butterfly (lane l ends with cluster l's sum) and per block over its warps in
+// order, into blockpart. Grid barrier. Every block sums blockpart over the blocks in the same
+// fixed order, so every block holds the same c and J (Eqs. c, A8) -- no second launch. Phase 2:
+// per row all k S values, E = S 2^-s / |L_c| (bitwise the value finalize stores), D = -2E + c, the
+// lowest-index argmin (A6), new labels, the exact integer size histogram and the changed count.
+// The E rows are stored (debug reads); the full distances are formed on demand (dfull_kernel).
+//
+// LSA = true (several ranks on one NVLink domain): the a2 all-reduce of S is fused in
+// and the update is DISTRIBUTED instead of replicated. Every rank's S lives in an NCCL symmetric
+// window mapped by all ranks (peer pointers, load/store over NVLink); a rank handles only its own
+// 1D block of rows: S(i, c) = the sum of the P ranks' S(i, c) read in rank order (exact integers),
+// its per-cluster partials go to every rank's table (peer stores), and after a cross-rank barrier
+// every rank sums the P partials in rank order (the same c and J everywhere); the new labels, the
+// size histogram and the changed count are stored / added into every rank's copies. Three
+// cross-rank arrivals per launch (S complete; partials published; labels landed), each one
+// red.release.sys per peer on the peers' flag words and an acquire spin on the own one.
 constexpr int UG_THREADS = 256;
 constexpr int UG_MAX_K = 64;
+constexpr int LSA_MAX_RANKS = 8;
+
+struct LsaArgs {
+  uint8_t *base[LSA_MAX_RANKS];  // every rank's window, as mapped in this process (base[rank]: own)
+  int nranks, rank;
+  int64_t row0;                  // this rank's rows [row0, row0 + nrows)
+  size_t off_S, off_lab_next, off_sizes_next, off_changed, off_rankpart, off_flag;
+  unsigned target;               // arrivals the first cross-rank wait needs (then + nranks, + 2 nranks)
+  long long *Sred;               // [k][rows_pad] (own rows used): the ranks' S summed (phase 0)
+};
 
 __device__ __forceinline__ void grid_barrier(unsigned *bar) {  // bar[0]: arrivals, bar[1]: generation
   __syncthreads();
@@ -383,32 +401,127 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {  // bar[0]: arriva
   __syncthreads();
 }
 
+// Cross-rank arrival (block 0, after a system-scope fence: its own and -- through the preceding
+// grid barrier -- the grid's peer stores are visible first) and wait (every block, or only block
+// 0 with all_wait = false) until the own flag reaches `target`. A rank that never arrives is
+// bounded by ~600 s of %globaltimer: the own flag page's word 16 is set (the host reports
+// KKM_ENCCL) and the kernel finishes on whatever it reads.
+__device__ __forceinline__ void lsa_arrive_wait(const LsaArgs &L, unsigned target, bool all_wait) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      __threadfence_system();
+      for (int p = 0; p < L.nranks; ++p)
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(L.base[p] + L.off_flag) : "memory");
+    }
+    if (all_wait || blockIdx.x == 0) {
+      const unsigned *flag = reinterpret_cast<const unsigned *>(L.base[L.rank] + L.off_flag);
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (uint32_t ns = 32;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if ((int)(v - target) >= 0) break;
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 600ull * 1000000000ull) {
+          atomicExch(reinterpret_cast<unsigned *>(L.base[L.rank] + L.off_flag) + 16, 1u);
+          break;
+        }
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// S(i, c): this rank's (LSA = false) or the ranks' sum of the own rows (phase 0's local copy).
+template <bool LSA>
+__device__ __forceinline__ long long s_load(const long long *__restrict__ Sfix, const LsaArgs &L, int64_t idx) {
+  return LSA ? __ldcg(L.Sred + idx) : Sfix[idx];
+}
+
+// Phase 0 of the distributed update: Sred[c][i] = sum over the ranks (rank order; exact integers)
+// of their S[c][i] for the own rows i, every c -- the reduce-scatter of S done by the kernel with
+// all P (P - 1 of them remote, over NVLink) loads of two elements in flight per thread.
+__device__ __forceinline__ void lsa_reduce_own(const LsaArgs &L, int64_t rows_pad, int64_t nrows, int k) {
+  constexpr int U = 4;  // elements per thread and pass: U x P loads in flight
+  const int64_t total = nrows * k, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += U * stride) {
+    int64_t x[U];
+    long long v[U][LSA_MAX_RANKS];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      x[u] = e < total ? (e / nrows) * rows_pad + L.row0 + e % nrows : -1;
+    }
+#pragma unroll
+    for (int p = 0; p < LSA_MAX_RANKS; ++p)
+      if (p < L.nranks) {
+        const long long *S = reinterpret_cast<const long long *>(L.base[p] + L.off_S);
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u][p] = x[u] >= 0 ? __ldcv(S + x[u]) : 0ll;
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long sum = 0;
+#pragma unroll
+      for (int p = 0; p < LSA_MAX_RANKS; ++p)
+        if (p < L.nranks) sum += v[u][p];
+      if (x[u] >= 0) L.Sred[x[u]] = sum;
+    }
+  }
+}
+
+#ifdef KKM_EXP_LSA_STAMPS  // (A/B experiment builds only: block 0's phase timestamps into the flag page)
+#define LSA_STAMP(j)                                                                                      \
+  if (LSA && blockIdx.x == 0 && threadIdx.x == 0) {                                                      \
+    unsigned long long ts_;                                                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_));                                              \
+    reinterpret_cast<unsigned long long *>(L.base[L.rank] + L.off_flag)[32 + (j)] = ts_;                 \
+  }
+#else
+#define LSA_STAMP(j)
+#endif
+
+template <bool LSA>
 __global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
     const long long *__restrict__ Sfix, int64_t rows_pad, int64_t nrows, int k, double inv,
     const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl, const double *__restrict__ diag,
     double *__restrict__ E, double *__restrict__ blockpart, unsigned *__restrict__ bar, double *__restrict__ cnorm_out,
     double *__restrict__ J_out, int32_t *__restrict__ cl_new, int32_t *__restrict__ sizes_next,
-    unsigned long long *__restrict__ changed_out) {
+    unsigned long long *__restrict__ changed_out, LsaArgs L) {
   __shared__ double wpart[UG_THREADS / 32][UG_MAX_K + 1];
   __shared__ double cn[UG_MAX_K];
   __shared__ int hist[UG_MAX_K];
   __shared__ unsigned long long nchg;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = UG_THREADS / 32;
   const int64_t stride = (int64_t)gridDim.x * UG_THREADS;
-  if (blockIdx.x == 0) {  // zeroed before the barrier, accumulated after it
+  const int64_t r0 = LSA ? L.row0 : 0;  // rows r0 + [0, nrows)
+  if (blockIdx.x == 0) {  // zeroed before the barrier (LSA: before this rank's second arrival), accumulated after
     for (int c = t; c < k; c += UG_THREADS) sizes_next[c] = 0;
     if (t == 0) *changed_out = 0ull;
   }
+  LSA_STAMP(0)
+  if (LSA) {
+    lsa_arrive_wait(L, L.target, true);  // every rank's S is complete
+    LSA_STAMP(1)
+    lsa_reduce_own(L, rows_pad, nrows, k);
+    __threadfence();
+    grid_barrier(bar);
+  }
+  LSA_STAMP(9)
   // ---- phase 1: per-cluster sums of z and sum (K_ii - z_i)
   double acc0 = 0.0, acc1 = 0.0, accJ = 0.0;  // lane l: clusters l and l + 32
   for (int64_t base = (int64_t)blockIdx.x * UG_THREADS + (t & ~31); base < nrows; base += stride) {
-    const int64_t i = base + lane;
+    const int64_t i = r0 + base + lane;
     int li = -1;
     double zi = 0.0, ji = 0.0;
-    if (i < nrows) {
+    if (base + lane < nrows) {
       li = cl[i];
       const int32_t sz = sizes[li];
-      const double sv = 0.0 + (double)Sfix[(int64_t)li * rows_pad + i] * inv;
+      const double sv = 0.0 + (double)s_load<LSA>(Sfix, L, (int64_t)li * rows_pad + i) * inv;
       zi = sz > 0 ? sv / (double)sz : 0.0;
       ji = diag[i] - zi;
     }
@@ -435,8 +548,6 @@ __global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
     for (int o = 16; o >= 1; o >>= 1) ji += __shfl_xor_sync(0xffffffffu, ji, o);
     accJ += ji;
   }
-  // lane l of every warp: its clusters' partials; the butterfly leaves cluster l on lane
-  // bitreverse-free position l (each level keeps the half selected by the lane bit)
   if (lane < k) wpart[w][lane] = acc0;
   if (lane + 32 < k) wpart[w][lane + 32] = acc1;
   if (lane == 0) wpart[w][k] = accJ;
@@ -446,8 +557,10 @@ __global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
     for (int q = 0; q < nw; ++q) sum += wpart[q][c];
     blockpart[(int64_t)blockIdx.x * (k + 1) + c] = sum;
   }
+  LSA_STAMP(2)
   grid_barrier(bar);
-  // ---- c and J: every block sums the block partials in the same fixed order
+  LSA_STAMP(3)
+  // ---- the grid's (k + 1) sums, by every block in the same fixed order
   for (int c = w; c <= k; c += nw) {
     double sum = 0.0;
     int b = lane;
@@ -462,7 +575,11 @@ __global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0) {
-      if (c < k) {
+      if (LSA) {  // this rank's partial -> every rank's table (block 0), then summed over the ranks below
+        if (blockIdx.x == 0)
+          for (int p = 0; p < L.nranks; ++p)
+            reinterpret_cast<double *>(L.base[p] + L.off_rankpart)[L.rank * (k + 1) + c] = sum;
+      } else if (c < k) {
         const int32_t sz = sizes[c];
         const double v = sz > 0 ? sum / (double)sz : __longlong_as_double(0x7ff0000000000000LL);  // +inf (A7)
         cn[c] = v;
@@ -472,18 +589,37 @@ __global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
       }
     }
   }
+  if (LSA) {
+    LSA_STAMP(4)
+    lsa_arrive_wait(L, L.target + L.nranks, true);  // every rank's partials published
+    LSA_STAMP(5)
+    const double *rp = reinterpret_cast<const double *>(L.base[L.rank] + L.off_rankpart);
+    for (int c = t; c <= k; c += UG_THREADS) {
+      double sum = 0.0;
+      for (int p = 0; p < L.nranks; ++p) sum += __ldcv(rp + p * (k + 1) + c);
+      if (c < k) {
+        const int32_t sz = sizes[c];
+        const double v = sz > 0 ? sum / (double)sz : __longlong_as_double(0x7ff0000000000000LL);
+        cn[c] = v;
+        if (blockIdx.x == 0) cnorm_out[c] = v;
+      } else if (blockIdx.x == 0) {
+        *J_out = sum;
+      }
+    }
+  }
   for (int c = t; c < k; c += UG_THREADS) hist[c] = 0;
   if (t == 0) nchg = 0ull;
   __syncthreads();
   // ---- phase 2: E, D, argmin, sizes, changed
   unsigned changed = 0;
-  for (int64_t i = (int64_t)blockIdx.x * UG_THREADS + t; i < nrows; i += stride) {
+  for (int64_t li0 = (int64_t)blockIdx.x * UG_THREADS + t; li0 < nrows; li0 += stride) {
+    const int64_t i = r0 + li0;
     int best = 0;
     double bd = __longlong_as_double(0x7ff0000000000000LL);
     for (int c0 = 0; c0 < k; c0 += 16) {
       long long sv[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) sv[q] = c0 + q < k ? Sfix[(int64_t)(c0 + q) * rows_pad + i] : 0ll;
+      for (int q = 0; q < 16; ++q) sv[q] = c0 + q < k ? s_load<LSA>(Sfix, L, (int64_t)(c0 + q) * rows_pad + i) : 0ll;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int c = c0 + q;
@@ -501,16 +637,36 @@ __global__ void __launch_bounds__(UG_THREADS) update_grid_kernel(
         }
       }
     }
-    cl_new[i] = best;
+    if (LSA) {
+      for (int p = 0; p < L.nranks; ++p) reinterpret_cast<int32_t *>(L.base[p] + L.off_lab_next)[i] = best;
+    } else {
+      cl_new[i] = best;
+    }
     changed += best != cl[i];
     atomicAdd(&hist[best], 1);
   }
   const unsigned wc = __reduce_add_sync(0xffffffffu, changed);
   if (lane == 0 && wc) atomicAdd(&nchg, (unsigned long long)wc);
   __syncthreads();
-  for (int c = t; c < k; c += UG_THREADS)
-    if (hist[c]) atomicAdd(&sizes_next[c], hist[c]);
-  if (t == 0 && nchg) atomicAdd(changed_out, nchg);
+  if (LSA) {
+    for (int c = t; c < k; c += UG_THREADS)
+      if (hist[c])
+        for (int p = 0; p < L.nranks; ++p)
+          atomicAdd(reinterpret_cast<int32_t *>(L.base[p] + L.off_sizes_next) + c, hist[c]);
+    if (t == 0 && nchg)
+      for (int p = 0; p < L.nranks; ++p)
+        atomicAdd(reinterpret_cast<unsigned long long *>(L.base[p] + L.off_changed), nchg);
+    LSA_STAMP(6)
+    __threadfence_system();
+    grid_barrier(bar);  // every block's peer stores issued and fenced
+    LSA_STAMP(7)
+    lsa_arrive_wait(L, L.target + 2 * L.nranks, false);  // block 0: every rank's labels landed here
+    LSA_STAMP(8)
+  } else {
+    for (int c = t; c < k; c += UG_THREADS)
+      if (hist[c]) atomicAdd(&sizes_next[c], hist[c]);
+    if (t == 0 && nchg) atomicAdd(changed_out, nchg);
+  }
 }
 
 // Dfull(i, c) = K_ii + D(i, c) from the stored E and c (debug reads; the same expression as assign).
