@@ -241,3 +241,96 @@ def test_15d_schedule_matches_oracle(n, pr, pc):
         assert np.array_equal(lab, ref["new_labels"])
         assert np.allclose(cn, ref["cnorm"], rtol=1e-12)
         assert abs(J - ref["J"]) <= 1e-10 * max(1.0, abs(ref["J"]))
+
+
+# ---- the default 1D f1 exchange: each rank's S contributions from the library's own
+# plan (kkm_plan_query pieces: row parts + mirrored column parts), summed over the ranks as int64
+# fixed point by a real allreduce (gloo), then a3/a4 replicated on every rank -- and the opt-in
+# distributed variant (KKM_LSA=1): each rank finishes only its own rows, exchanges its (k + 1)
+# partials, and the labels are gathered. The arithmetic per rank is the oracle's.
+FX = 2.0 ** 40  # fixed-point scale (|S| * 2^40 << 2^63 at these sizes)
+
+
+def f1_contrib(pcs, K, labels, k):
+    n = K.shape[0]
+    V = np.zeros((n, k))
+    V[np.arange(n), labels] = 1.0
+    Sr = np.zeros((n, k))
+    for r0, nr, c0, nc, cd in pcs:
+        Sr[r0:r0 + nr] += K[r0:r0 + nr, c0:c0 + nc] @ V[c0:c0 + nc]
+        if cd < c0 + nc:
+            a = max(cd, c0)
+            Sr[a:c0 + nc] += K[r0:r0 + nr, a:c0 + nc].T @ V[r0:r0 + nr]
+    return np.rint(Sr * FX).astype(np.int64)
+
+
+def _worker_f1(rank, P, port, n, k, distributed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    import paper_2601_17136_b200 as kkm
+    X, cfg = synth.make_config("har200k", n=n)
+    args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
+    K = oracle.kernel_matrix(X, *args)
+    diag = np.diag(K).copy()
+    p = kkm.default_params()
+    p.k, p.kind, p.path, p.symmetric, p.kstore = k, kkm.KERNEL_GAUSSIAN, kkm.PATH_MATERIALIZE, kkm.SYM_ON, kkm.KSTORE_FP16X2
+    info, pcs = kkm.plan_query(p, n, X.shape[1], rank=rank, nranks=P)
+    assert info.exchange == kkm.XCHG_S_ALLREDUCE
+    labels = oracle.round_robin(n, k)
+    res = []
+    for _ in range(3):
+        S = torch.from_numpy(f1_contrib(pcs, K, labels, k))
+        dist.all_reduce(S)  # exact integer sum: the same bits on every rank, any order
+        sizes = np.bincount(labels, minlength=k)
+        E = (S.numpy().astype(np.float64) / FX) / np.maximum(sizes, 1)
+        if not distributed:  # replicated a3/a4 over all points
+            cn = oracle.cnorm(E, labels, k)
+            J = oracle.objective(diag, labels, k, cn)
+            labels, _ = oracle.assign(E, diag, cn)
+        else:  # own rows only; (k + 1) partials gathered and summed in rank order; labels gathered
+            r0, r1 = shard_begin(n, rank, P), shard_begin(n, rank + 1, P)
+            part = np.zeros(k + 1)
+            for i in range(r0, r1):
+                part[labels[i]] += E[i, labels[i]]
+                part[k] += diag[i] - E[i, labels[i]]
+            allp = [torch.zeros(k + 1, dtype=torch.float64) for _ in range(P)]
+            dist.all_gather(allp, torch.from_numpy(part))
+            tot = np.zeros(k + 1)
+            for r in range(P):
+                tot += allp[r].numpy()
+            cn = np.where(sizes > 0, tot[:k] / np.maximum(sizes, 1), np.inf)
+            J = tot[k]
+            mine, _ = oracle.assign(E[r0:r1], diag[r0:r1], cn)
+            B = -(-n // P)
+            send = torch.full((B,), -1, dtype=torch.int32)
+            send[:mine.size] = torch.from_numpy(mine.astype(np.int32))
+            out = [torch.empty(B, dtype=torch.int32) for _ in range(P)]
+            dist.all_gather(out, send)
+            labels = torch.cat(out).numpy()[:n]
+        res.append((np.asarray(labels).copy(), np.asarray(cn), float(J)))
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("distributed", [False, True], ids=["replicated", "distributed"])
+def test_gloo_world2_f1_exchange_matches_oracle(distributed):
+    P, k, n = 2, 6, 3001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_f1, args=(r, P, port, n, k, distributed, q)) for r in range(P)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(P))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    X, cfg = synth.make_config("har200k", n=n)
+    ref = oracle.fit(X, k, cfg["kind"], cfg["gamma"], max_iter=3, keep_trace=True)
+    for t in range(3):
+        lab0, cn0, J0 = out[0][t]
+        lab1, cn1, J1 = out[1][t]
+        assert np.array_equal(lab0, lab1)
+        assert np.array_equal(cn0, cn1) and J0 == J1  # bitwise the same on both ranks
+        assert np.array_equal(lab0, ref["label_trace"][t + 1])
+        assert abs(J0 - ref["J_trace"][t]) <= 1e-9 * abs(ref["J_trace"][t])
