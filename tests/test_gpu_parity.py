@@ -372,3 +372,29 @@ def test_tensor_core_bands_32_labels(k, kind):
     args = (kind, 0.05, 0.0, 1) if kind == oracle.GAUSSIAN else (kind, 0.05, 1.0, 2)
     teacher_forced(X, k, *args, iters=2, precision=(kkm.PREC_FP16X3, kkm.PATH_MATERIALIZE, kkm.SYM_ON,
                                                       kkm.KSTORE_FP16X2))
+
+
+@pytest.mark.parametrize("order", [{"KKM_SSYM_STATIC": "1"}, {"KKM_SSYM_G": "0"}, {"KKM_SSYM_G": "8", "KKM_SSYM_W": "3"}],
+                         ids=["static", "block-major", "supertile-8x3"])
+def test_stream_symmetric_schedule_invariance(order, monkeypatch):
+    """The streaming f1 kernel's S is int64 fixed point added with red.add (associative), so the
+    order in which the CTA pairs take the units -- dynamic (default) or the static round robin,
+    supertile or block-major unit order -- must give bitwise the same E, c, J and labels
+    (ssym.cuh). The unit order is read when the plan is made (kkm_init); the
+    schedule when each kernel launches."""
+    X = synth.blobs(20001, 16, 7, seed=5, sep=3.0)
+
+    def run():
+        h = _handle(X, 7, oracle.GAUSSIAN, 0.05, 0.0, 1, 3, (kkm.PREC_FP16X3, kkm.PATH_STREAM))
+        it, J, ch = h.fit()
+        out = (h.assign().cpu().numpy(), h.debug_read(kkm.DBG_E), h.debug_read(kkm.DBG_CNORM), J)
+        h.destroy()
+        return out
+
+    ref = run()
+    for key, val in order.items():
+        monkeypatch.setenv(key, val)
+    alt = run()
+    assert np.array_equal(ref[0], alt[0])
+    for a, b in zip(ref[1:], alt[1:]):
+        assert np.array_equal(a, b)
