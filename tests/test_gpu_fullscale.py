@@ -86,9 +86,9 @@ def _handle(X, k, args, **kw):
 
 def test_config4_recipe_streaming_symmetric_sampled():
     """BASELINE configs[3] recipe (n = 1,000,000, d = 784, k = 10, Gaussian, median gamma): K
-    (4 TB) cannot be stored, so AUTO streams it with the upper-triangle kernel
-    (tc2_stream_sym_kernel: 3907 row tiles, units of <= 64 aligned column tiles, int64 fixed-point
-    S at n max K_ii 2^s < 2^61). Two injected labelings."""
+    (4 TB) cannot be stored, so AUTO streams it with the upper-triangle kernel (ssym_kernel:
+    3907 row tiles in 32 x 32 supertiles, units of 16 column tiles taken dynamically, int64
+    fixed-point S at n max K_ii 2^s < 2^61). Two injected labelings."""
     name = "mnist1m"
     n = synth.CONFIGS[name]["n"]
     X, truth = synth.mnist_like(n, synth.CONFIGS[name]["seed"], return_truth=True)
@@ -103,11 +103,28 @@ def test_config4_recipe_streaming_symmetric_sampled():
     h.destroy()
 
 
+def test_config5_recipe_streaming_symmetric_sampled():
+    """BASELINE configs[4] recipe (MNIST8m-shaped: n = 8,100,000, d = 784, k = 10, poly(1,1,2)) on
+    ONE GPU: the streaming f1 kernel over 31641 row tiles (~5e8 pair tiles, ~100 s), the int64
+    fixed-point S at n = 8.1M. One injected labeling, 64 sampled rows (8.1M exact kernel
+    evaluations each)."""
+    name = "mnist8m"
+    n = synth.CONFIGS[name]["n"]
+    X, truth = synth.mnist_like(n, synth.CONFIGS[name]["seed"], return_truth=True)
+    cfg = synth.CONFIGS[name]
+    args = (cfg["kind"], cfg.get("gamma") or 1.0, cfg.get("coef0", 1.0), cfg.get("degree", 2))
+    k = cfg["k"]
+    h = _handle(X, k, args)
+    rows = sample_rows(n, 64, seed=8)
+    sampled_iteration(h, X, noisy_truth(truth, k, seed=8), k, args, rows)
+    h.destroy()
+
+
 @pytest.mark.parametrize("k", [10, 21])
 def test_streaming_full_kernel_300k_sampled(k):
     """The full (non-symmetric) streaming kernel at n = 300,000 (MNIST recipe, poly(1,1,2)):
-    1172 column tiles -> several splits of <= 512 tiles per work unit, fp64 split partials;
-    k = 21: two cluster-group launches over the label-sorted operand."""
+    1172 column tiles split over the work units (tc3_stream_kernel, int64 fixed-point S, any k in
+    one launch: k = 21 has 20 segment boundaries inside the units)."""
     n = 300000
     X, truth = synth.mnist_like(n, 4, return_truth=True)
     args = (oracle.POLY, 1.0, 1.0, 2)
