@@ -48,13 +48,13 @@ struct StreamA {
 // A and B are disjoint): sorted position of A row i for b0 <= i < b0 + npos (the Gaussian
 // diagonal). fx = 2^s with nB max|K| 2^s < 2^61.
 int stream_pass(kkm_ctx *h, TcStream &ts, const StreamA &A, const SortedSet &B, int64_t brows, int64_t nB,
-                int64_t b0, const int32_t *pos, int64_t npos, int splits, double fx, long long *Sx, double *S) {
+                int64_t b0, const int32_t *pos, int64_t npos, double fx, long long *Sx, double *S) {
   const Plan &P = h->P;
   const int k = P.k;
   if (A.nA == 0) return KKM_OK;
   CK(cudaMemsetAsync(Sx, 0, (size_t)A.rows_pad * k * 8, h->st));
   if (tc3_stream_launch(ts, A.hi, A.lo, B.hi, B.lo, P.fp16, A.arows, brows, P.dp, nB, b0, A.row0, A.nA, A.norms,
-                        A.rscale, B.norms, B.rscale, pos, npos, B.seg, k, h->kp, splits, fx, Sx, h->st, &h->launches,
+                        A.rscale, B.norms, B.rscale, pos, npos, B.seg, k, h->kp, fx, Sx, h->st, &h->launches,
                         h->chain_kb)) {
     h->poisoned = true;
     return fail(KKM_ECUDA, "streaming kernel launch failed: %s", tc_gemm_error());
@@ -72,7 +72,7 @@ int launch_stream(kkm_ctx *h, const int32_t *labels) {
   CKR(sort_gather(h, labels + P.b0, P.b0, P.nB, P.npad, B));
   const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.a0, P.nA, P.nApad};
   a2_mark(h);
-  const int rc = stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, P.stream_splits, h->fx_scale,
+  const int rc = stream_pass(h, h->ts, A, B, P.npad, P.nB, P.b0, h->pos, P.nB, h->fx_scale,
                             (long long *)(h->ws + P.o_Sx), h->Spart);
   a2_mark(h);
   return rc;

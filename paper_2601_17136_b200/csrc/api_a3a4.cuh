@@ -136,7 +136,6 @@ int delta_update(kkm_ctx *h, int64_t m) {
   const int32_t *cl_old = h->lab[h->cur], *cl_new = h->lab[h->cur ^ 1];
   const int nblk = (int)ceil_div(P.n, SORT_BLOCK);
   const int64_t mpad = round_up(m, 256);
-  const int splits = std::min(8, ts_choose_splits((P.nloc + 1) / 2, m, h->num_sms / 2));
   const StreamA A{h->Xhi, h->Xlo, h->norms, h->rscale, P.npad, P.row0, P.nloc, P.B};
   for (int pass = 0; pass < 2; ++pass) {  // 0: + new labels, 1: - old labels
     moved_key_kernel<<<(unsigned)ceil_div(P.lablen, 256), 256, 0, h->st>>>(cl_old, cl_new, P.n, P.lablen, k,
@@ -154,7 +153,7 @@ int delta_update(kkm_ctx *h, int64_t m) {
     CKL();
     // B = the m moved points (clusters 0..k-1 of the k+1 buckets); pos: sorted position of
     // each point (>= m for the points that did not move) for the Gaussian diagonal
-    CKR(stream_pass(h, h->ts_delta, A, D, mpad, m, 0, D.pos, P.n, splits, h->fx_scale, h->Sdx, h->Sd));
+    CKR(stream_pass(h, h->ts_delta, A, D, mpad, m, 0, D.pos, P.n, h->fx_scale, h->Sdx, h->Sd));
     sinc_add_kernel<<<(unsigned)ceil_div(P.nloc * k, 256), 256, 0, h->st>>>(h->Sd, 1, P.B, P.nloc, k,
                                                                             pass == 0 ? 1.0 : -1.0, h->Sinc);
     CKL();

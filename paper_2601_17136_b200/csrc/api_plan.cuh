@@ -32,7 +32,6 @@ struct Plan {
   int sort_blocks;              // streaming: blocks of the counting sort
   bool spmm_v2;                 // materialised a2 with label-sorted 32-column groups (k <= 64)
   int nsplit, chunks_per_split, nfin, nspmm_pass;
-  int stream_splits = 1;  // column splits per row tile of the full streaming kernel (tc3_stream_kernel)
   int64_t rows_per_block;
   size_t kelems;       // materialised K elements (per 16-bit plane)
   int64_t s_rows_pad;  // row pitch of the S (or S partials) finalize reads
@@ -208,17 +207,9 @@ int make_plan(const kkm_params *p, int64_t n, int64_t d, int32_t rank, int32_t n
     P.nsplit = (int)ceil_div(nchunks, SP_MAX_CHUNKS_PER_SPLIT * 1024 / ch);
     P.chunks_per_split = (int)ceil_div(nchunks, P.nsplit);
   } else {
-    // work units of the fused kernel = 128-row tiles x column splits; 148 SMs assumed for the
-    // load-balance choice (B200). Work units = 256-row pair tiles x column splits (74 CTA pairs),
-    // ordered tile-major (the clusters working on one row tile's splits share its A operand in
-    // L2). Splits: at most 512 256-column tiles per unit, which bounds how far the concurrent
-    // sweeps over B drift apart (measured at n = 1M: 4.41 -> 3.92 s per iteration); then the best
-    // last-wave fill. The kernel sums S in int64 fixed point (one [rows][k] array, any number of
-    // splits), converted once to fp64: one partial for a3 (nsplit = 1).
-    const int64_t tiles_n = ceil_div(std::max<int64_t>(P.nB, 1), 256);
-    const int64_t s_l2 = ceil_div(tiles_n, 512);
-    const int s_bal = ts_choose_splits((P.nA + 1) / 2, P.nB, 74);
-    P.stream_splits = (int)std::max<int64_t>(s_l2, s_bal);
+    // the fused streaming kernel takes units of W column tiles in G-row supertiles dynamically
+    // (tc3.cuh T2StreamSched); it sums S in int64 fixed point (one [rows][k] array), converted
+    // once to fp64: one partial for a3 (nsplit = 1).
     P.nsplit = 1;
     P.chunks_per_split = 0;
   }

@@ -8,7 +8,7 @@ namespace {
 // only: streaming handles lend their own), the partials and the outputs.
 struct PredictPlan {
   int64_t mpad;
-  int splits, nblk;
+  int nblk;
   bool own_sorted;
   size_t oYf, oYhi, oYlo, oYn, oYr, oYd, oSp, oSx, oFx, oLab, oD, oPerm, oPos, oSeg, oBc, oBo, oShi, oSlo, oSn, oSr,
       total;
@@ -19,8 +19,6 @@ PredictPlan predict_plan(const kkm_ctx *h, int64_t m) {
   PredictPlan q;
   q.mpad = round_up(std::max<int64_t>(m, 1), 256);
   q.nblk = (int)ceil_div(P.n, SORT_BLOCK);
-  const int64_t tiles_n = ceil_div(P.n, 256);
-  q.splits = (int)std::max<int64_t>(ceil_div(tiles_n, 512), ts_choose_splits((m + 1) / 2, P.n, h->num_sms / 2));
   q.own_sorted = P.materialize;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -106,7 +104,7 @@ int predict_run(kkm_ctx *h, const PredictPlan &q, uint8_t *t, const float *Y, in
                                           : std::pow(h->p.gamma * nm + std::fabs(h->p.coef0), (double)h->p.degree);
   }
   const double fx = std::ldexp(1.0, (int)std::floor(61.0 - std::log2(std::max(1e-300, (double)P.n * kmax * 1.0001))));
-  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, 0, q.splits, fx, (long long *)(t + q.oSx), Sp));
+  CKR(stream_pass(h, ts, A, B, P.npad, P.n, 0, nullptr, 0, fx, (long long *)(t + q.oSx), Sp));
   predict_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, h->st>>>(Sp, 1, m, q.mpad, k, h->sizes[h->cur],
                                                                 h->cnorm2, yd, ylab, Dy);
   CKL();

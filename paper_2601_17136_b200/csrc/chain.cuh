@@ -263,6 +263,146 @@ __device__ __forceinline__ void ch_drain(const ChSmem &s, uint32_t tq, int nch, 
 }
 
 
+// ---------------------------------------------------------------- dynamic unit schedule
+// The CTA pairs of a persistent chained kernel take work units from ONE global counter instead of
+// a static round robin (pair p: units p, p + 74, ...), so the units in flight stay consecutive in
+// the host's unit order however the pairs' speeds drift over a long launch.
+constexpr int CH_RING = 8;  // unit-index slots in flight per pair
+constexpr size_t CH_RING_BYTES = 2 * CH_RING * 8 + CH_RING * 4;
+// arrivals that free a ring slot (on the leader CTA): per CTA its 16 epilogue warps + the MMA
+// issuer (leader) / the producer (peer CTA)
+constexpr uint32_t CH_RING_CONSUMERS = 2 * (CH_EPI_WARPS + 1);
+
+
+__device__ __forceinline__ void st_cluster_s32(int32_t *p, uint32_t cta, int32_t v) {
+  asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.s32 [ra], %2;\n\t}" ::"r"(
+                   smem_u32(p)),
+               "r"(cta), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint64_t *bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t parity) {
+  uint32_t ns = 32;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
+// The pair's unit source. Static: pair cl takes units cl, cl + ncl, ... Dynamic: position i of the
+// ring (slot i % CH_RING) carries the i-th unit the pair fetched from the global counter work[0]
+// (-1: none left); the leader producer fetches (one ahead) and publishes, the other roles read.
+// work[1] counts the pairs that saw the end; the last one resets both counters for the next launch.
+struct ChRing {
+  int32_t *slot;
+  uint64_t *full, *empty;  // full: 1 arrival (the leader producer), in both CTAs; empty: leader CTA only
+  bool dyn;
+  int64_t nitems;
+  int32_t *work;
+  __device__ __forceinline__ int64_t static_unit(int64_t i) const {
+    const int64_t u = (int64_t)(blockIdx.x >> 1) + i * (int64_t)(gridDim.x >> 1);
+    return u < nitems ? u : -1;
+  }
+  // leader producer: publish the pair's next unit (nxt: the prefetched counter value)
+  __device__ __forceinline__ int64_t publish(int64_t i, int &nxt) const {
+    if (!dyn) return static_unit(i);
+    const int sl = (int)(i % CH_RING);
+    mbar_wait_acq_cluster(&empty[sl], (uint32_t)((i / CH_RING) & 1) ^ 1u);
+    int u = nxt < nitems ? nxt : -1;
+    if (u >= 0) {
+      nxt = atomicAdd(work, 1);
+    } else if (atomicAdd(work + 1, 1) == (int)(gridDim.x >> 1) - 1) {
+      work[0] = 0;
+      work[1] = 0;
+    }
+    slot[sl] = u;
+    st_cluster_s32(&slot[sl], 1, u);
+    mbar_arrive(&full[sl]);
+    mbar_arrive_cluster_release(&full[sl], 1);
+    return u;
+  }
+  // other roles: the unit at ring position i; `arrive`: this thread frees the slot for its warp
+  __device__ __forceinline__ int64_t take(int64_t i, bool arrive) const {
+    if (!dyn) return static_unit(i);
+    const int sl = (int)(i % CH_RING);
+    mbar_wait_acq_cluster(&full[sl], (uint32_t)((i / CH_RING) & 1));
+    const int u = *reinterpret_cast<volatile int32_t *>(&slot[sl]);
+    __syncwarp(__activemask());
+    if (arrive) mbar_arrive_cluster_release(&empty[sl], 0);
+    return u;
+  }
+};
+
+
+// The ring in `bytes` (CH_RING_BYTES of shared memory, 8-byte aligned).
+__device__ __forceinline__ ChRing ch_ring_carve(uint8_t *bytes, bool dyn, int64_t nitems, int32_t *work) {
+  ChRing r;
+  r.full = reinterpret_cast<uint64_t *>(bytes);
+  r.empty = r.full + CH_RING;
+  r.slot = reinterpret_cast<int32_t *>(r.empty + CH_RING);
+  r.dyn = dyn;
+  r.nitems = nitems;
+  r.work = work;
+  return r;
+}
+// (thread 0, before ch_setup: its fence and cluster barrier publish the init)
+__device__ __forceinline__ void ch_ring_init(const ChRing &r) {
+  if (threadIdx.x == 0)
+    for (int i = 0; i < CH_RING; ++i) {
+      mbar_init(&r.full[i], 1);
+      mbar_init(&r.empty[i], CH_RING_CONSUMERS);
+    }
+}
+
+// Warp 0 lane 0 (both CTAs) of a chained kernel on the dynamic schedule: the leader's producer
+// fetches and publishes the units (ChRing::publish), the peer's takes them; both load their halves.
+template <class Sched>
+__device__ __forceinline__ void ch_ring_producer(const Sched &sc, const ChRing &ring, const ChSmem &s, uint32_t cr,
+                                                 const CUtensorMap *a_hi, const CUtensorMap *a_lo,
+                                                 const CUtensorMap *b_hi, const CUtensorMap *b_lo, int nkb) {
+  T2Smem ts;  // the producer only uses the stage ring
+  ts.stages = s.stages;
+  ts.full = s.full;
+  ts.empty = s.empty;
+  const T2Policy pol(sc.hint);
+  int stage = 0;
+  uint32_t phase = 0;
+  int nxt = (ring.dyn && cr == 0) ? atomicAdd(ring.work, 1) : 0;
+  for (int64_t i = 0;; ++i) {
+    const int64_t u = cr == 0 ? ring.publish(i, nxt) : ring.take(i, true);
+    if (u < 0) break;
+    t2_produce_item(sc, ts, u, a_hi, a_lo, b_hi, b_lo, nkb, cr, pol, stage, phase);
+  }
+}
+
+// Warp 1 lane 0 of the leader CTA on the dynamic schedule: the MMA issuer.
+template <class Sched>
+__device__ __forceinline__ void ch_ring_mma(const Sched &sc, const ChRing &ring, const ChSmem &s, int nkb, int nch,
+                                            uint32_t idesc, uint32_t tmem_base) {
+  int stage = 0;
+  uint32_t phase = 0;
+  int64_t chain = 0;
+  for (int64_t i = 0;; ++i) {
+    const int64_t u = ring.take(i, true);
+    if (u < 0) break;
+    ch_mma_item(sc, s, u, nkb, nch, idesc, tmem_base, stage, phase, chain);
+  }
+}
+
 // Warps 0 (TMA producer, both CTAs) and 1 (MMA issuer, leader CTA) of a chained kernel.
 template <class Sched>
 __device__ __forceinline__ void ch_producer_mma(const Sched &sc, const ChSmem &s, int warp, int lane, uint32_t cr,

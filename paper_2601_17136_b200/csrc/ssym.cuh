@@ -36,85 +36,8 @@ constexpr int SS_THREADS = CH_THREADS;
 constexpr int SS_COLS = CH_COLS;
 constexpr size_t SS_COLC_BYTES = CH_COLC_BYTES;
 constexpr size_t SS_SEG_BYTES = (size_t)(KKM_MAX_K + 1) * 4;
-constexpr int SS_RING = 8;  // unit-index slots in flight per pair (dynamic schedule)
 constexpr size_t SS_RING_OFF = SS_EPI_WARPS * SS_COLC_BYTES + (SS_SEG_BYTES + 15) / 16 * 16;
-constexpr size_t SS_EXTRA = SS_RING_OFF + 2 * SS_RING * 8 + SS_RING * 4;
-// arrivals that free a ring slot (on the leader CTA): per CTA its 16 epilogue warps + the MMA
-// issuer (leader) / the producer (peer CTA)
-constexpr uint32_t SS_RING_CONSUMERS = 2 * (SS_EPI_WARPS + 1);
-
-__device__ __forceinline__ void st_cluster_s32(int32_t *p, uint32_t cta, int32_t v) {
-  asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.s32 [ra], %2;\n\t}" ::"r"(
-                   smem_u32(p)),
-               "r"(cta), "r"(v)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cluster_release(uint64_t *bar, uint32_t cta) {
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
-      "r"(cta)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t parity) {
-  uint32_t ns = 32;
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    __nanosleep(ns);
-    if (ns < 512) ns <<= 1;
-  }
-}
-
-// The pair's unit source. Static: pair cl takes units cl, cl + ncl, ... Dynamic: position i of the
-// ring (slot i % SS_RING) carries the i-th unit the pair fetched from the global counter work[0]
-// (-1: none left); the leader producer fetches (one ahead) and publishes, the other roles read.
-// work[1] counts the pairs that saw the end; the last one resets both counters for the next launch.
-struct SsRing {
-  int32_t *slot;
-  uint64_t *full, *empty;  // full: 1 arrival (the leader producer), in both CTAs; empty: leader CTA only
-  bool dyn;
-  int64_t nitems;
-  int32_t *work;
-  __device__ __forceinline__ int64_t static_unit(int64_t i) const {
-    const int64_t u = (int64_t)(blockIdx.x >> 1) + i * (int64_t)(gridDim.x >> 1);
-    return u < nitems ? u : -1;
-  }
-  // leader producer: publish the pair's next unit (nxt: the prefetched counter value)
-  __device__ __forceinline__ int64_t publish(int64_t i, int &nxt) const {
-    if (!dyn) return static_unit(i);
-    const int sl = (int)(i % SS_RING);
-    mbar_wait_acq_cluster(&empty[sl], (uint32_t)((i / SS_RING) & 1) ^ 1u);
-    int u = nxt < nitems ? nxt : -1;
-    if (u >= 0) {
-      nxt = atomicAdd(work, 1);
-    } else if (atomicAdd(work + 1, 1) == (int)(gridDim.x >> 1) - 1) {
-      work[0] = 0;
-      work[1] = 0;
-    }
-    slot[sl] = u;
-    st_cluster_s32(&slot[sl], 1, u);
-    mbar_arrive(&full[sl]);
-    mbar_arrive_cluster_release(&full[sl], 1);
-    return u;
-  }
-  // other roles: the unit at ring position i; `arrive`: this thread frees the slot for its warp
-  __device__ __forceinline__ int64_t take(int64_t i, bool arrive) const {
-    if (!dyn) return static_unit(i);
-    const int sl = (int)(i % SS_RING);
-    mbar_wait_acq_cluster(&full[sl], (uint32_t)((i / SS_RING) & 1));
-    const int u = *reinterpret_cast<volatile int32_t *>(&slot[sl]);
-    __syncwarp(__activemask());
-    if (arrive) mbar_arrive_cluster_release(&empty[sl], 0);
-    return u;
-  }
-};
+constexpr size_t SS_EXTRA = SS_RING_OFF + CH_RING_BYTES;
 constexpr size_t SS_SMEM = (size_t)T2_STAGES * T2_STAGE_BYTES + SS_EXTRA + 1024 + 128;
 
 // One 32-column chunk of a tile (columns p0 .. p0 + 31, this thread's row p): kappa, the row part
@@ -170,52 +93,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SS_THREADS, 1)
   const ChSmem s = ch_carve(smem_raw, (uint32_t)SS_EXTRA, &extra);
   float *colc = reinterpret_cast<float *>(extra);
   int32_t *seg = reinterpret_cast<int32_t *>(extra + SS_EPI_WARPS * SS_COLC_BYTES);
-  SsRing ring;
-  ring.full = reinterpret_cast<uint64_t *>(extra + SS_RING_OFF);
-  ring.empty = ring.full + SS_RING;
-  ring.slot = reinterpret_cast<int32_t *>(ring.empty + SS_RING);
-  ring.dyn = dyn;
-  ring.nitems = sc.nitems;
-  ring.work = work;
+  const ChRing ring = ch_ring_carve(extra + SS_RING_OFF, dyn, sc.nitems, work);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cr = cluster_ctarank();
   const bool fp16 = srscale != nullptr;
   for (int c = threadIdx.x; c <= k; c += blockDim.x) seg[c] = seg_g[c];
-  if (threadIdx.x == 0)
-    for (int i = 0; i < SS_RING; ++i) {
-      mbar_init(&ring.full[i], 1);
-      mbar_init(&ring.empty[i], SS_RING_CONSUMERS);
-    }
+  ch_ring_init(ring);
   ch_setup(s, warp, 2 * SS_EPI_WARPS);  // (its fence + cluster barrier also publish the ring's init)
   const uint32_t tmem_base = *s.tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      T2Smem ts;  // the producer only uses the stage ring
-      ts.stages = s.stages;
-      ts.full = s.full;
-      ts.empty = s.empty;
-      const T2Policy pol(sc.hint);
-      int stage = 0;
-      uint32_t phase = 0;
-      int nxt = (dyn && cr == 0) ? atomicAdd(work, 1) : 0;
-      for (int64_t i = 0;; ++i) {
-        const int64_t u = cr == 0 ? ring.publish(i, nxt) : ring.take(i, true);
-        if (u < 0) break;
-        t2_produce_item(sc, ts, u, &t_hi, &t_lo, &t_hi, &t_lo, nkb, cr, pol, stage, phase);
-      }
-    }
+    if (lane == 0) ch_ring_producer(sc, ring, s, cr, &t_hi, &t_lo, &t_hi, &t_lo, nkb);
   } else if (warp == 1) {
-    if (lane == 0 && cr == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int64_t chain = 0;
-      for (int64_t i = 0;; ++i) {
-        const int64_t u = ring.take(i, true);
-        if (u < 0) break;
-        ch_mma_item(sc, s, u, nkb, nch, idesc, tmem_base, stage, phase, chain);
-      }
-    }
+    if (lane == 0 && cr == 0) ch_ring_mma(sc, ring, s, nkb, nch, idesc, tmem_base);
   } else {
     const int e = warp - 2;
     const int quarter = warp & 3;

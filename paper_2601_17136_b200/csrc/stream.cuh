@@ -1,6 +1,6 @@
 // stream.cuh -- host side of the fused streaming a1+a2 (K never stored; the kernels are
 // tc3_stream_kernel in tc3.cuh and ssym_kernel in ssym.cuh): operand tensor maps of the A set and
-// of the label-sorted B set (sort.cuh), and the choice of column splits per row tile.
+// of the label-sorted B set (sort.cuh).
 #pragma once
 #include "gemm_tc.cuh"
 
@@ -13,6 +13,13 @@ struct TcStream {
   int64_t arows = 0, brows = 0;
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
   int num_sms = 0;
+  int32_t *work = nullptr;  // tc3_stream_kernel's dynamic unit counters (allocated at first launch)
+  TcStream() = default;
+  TcStream(const TcStream &) = delete;
+  TcStream &operator=(const TcStream &) = delete;
+  ~TcStream() {
+    if (work) cudaFree(work);
+  }
 };
 
 inline int ts_encode(CUtensorMap *m, const void *ptr, bool fp16, int64_t rows, int64_t dp) {
@@ -29,25 +36,6 @@ inline int ts_encode(CUtensorMap *m, const void *ptr, bool fp16, int64_t rows, i
     return 1;
   }
   return 0;
-}
-
-// Splits of the sorted column range: enough work units for a full last wave. Callers pass half
-// the rows and the CTA-pair count, so 128-row tiles here are the kernel's 256-row pair tiles.
-inline int ts_choose_splits(int64_t nloc, int64_t n, int num_sms) {
-  const int64_t tiles_m = (nloc + 127) / 128;
-  const int64_t tiles_n = (n + 255) / 256;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 8 && s <= tiles_n; ++s) {
-    const int64_t units = tiles_m * s;
-    const int64_t waves = (units + num_sms - 1) / num_sms;
-    const double eff = (double)units / (double)(waves * num_sms) - 0.002 * s;  // mild preference for fewer splits
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = s;
-    }
-  }
-  return best;
 }
 
 }  // namespace kkm

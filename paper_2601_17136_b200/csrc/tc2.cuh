@@ -264,28 +264,30 @@ struct T2DiagSched {
 };
 
 // ---------------------------------------------------------------- fused streaming kernel
+// Work units of the full streaming kernel: (pair row tile, W column tiles) in a G-row supertile
+// raster -- row groups of G pair tiles, each swept W column tiles at a time across its G rows --
+// computed from the unit index (no table): unit u of group gi = u / (G ncb) is column block
+// cb = r / gm, row gi G + r % gm (r = u - gi G ncb, gm = the group's rows, ncb = ceil(tiles_n / W)).
 struct T2StreamSched {
-  int64_t nitems;
-  int tiles_m, tiles_n, nsplit, tps;
+  int64_t nitems;  // tiles_m * ncb
+  int tiles_m, tiles_n, G, W, ncb;
   int64_t row0;
-  int split_major;  // 1: consecutive work items share a split (column region) -> L2 reuse
-  int hint;         // 1: L2 evict_last on the operand loads
-  __device__ __forceinline__ void unit(int64_t u, int &tm, int &sp) const {
-    if (split_major) {
-      sp = (int)(u / tiles_m);
-      tm = (int)(u % tiles_m);
-    } else {
-      tm = (int)(u / nsplit);
-      sp = (int)(u % nsplit);
-    }
+  int hint;        // 1: L2 evict_last on the operand loads
+  __device__ __forceinline__ void unit(int64_t u, int &tm, int &tn0, int &ntn) const {
+    const int64_t per_group = (int64_t)G * ncb;
+    const int gi = (int)(u / per_group);
+    const int64_t r = u - (int64_t)gi * per_group;
+    const int gm = min(G, tiles_m - gi * G);
+    const int cb = (int)(r / gm);
+    tm = gi * G + (int)(r % gm);
+    tn0 = cb * W;
+    ntn = min(W, tiles_n - tn0);
   }
   __device__ __forceinline__ void item(int64_t u, int &ra, int &rb0, int &ntn) const {
-    int tm, sp;
-    unit(u, tm, sp);
-    const int tn0 = sp * tps, tn1 = min(tiles_n, tn0 + tps);
+    int tm, tn0;
+    unit(u, tm, tn0, ntn);
     ra = (int)(row0 + (int64_t)tm * T2_BM);
     rb0 = tn0 * 256;
-    ntn = tn1 > tn0 ? tn1 - tn0 : 0;
   }
 };
 

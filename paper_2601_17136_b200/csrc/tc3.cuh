@@ -271,7 +271,8 @@ inline int tc3_self_dots(TcGemm &g, const uint16_t *Xhi, const uint16_t *Xlo, bo
 // sum_{q in segment c} kappa(a_r, b_q) -- Eqs. (b), (k), (e); one running sum per row flushed at
 // segment changes (ch_row_part). pos (may be NULL): sorted position of A row i for b0 <= i <
 // b0 + npos, where kappa(x_i, x_i) = 1 exactly (A1). K(A, B) is never stored.
-constexpr size_t T3_STREAM_EXTRA = CH_EPI_WARPS * CH_COLC_BYTES + ((size_t)(KKM_MAX_K + 1) * 4 + 15) / 16 * 16;
+constexpr size_t T3_STREAM_RING_OFF = CH_EPI_WARPS * CH_COLC_BYTES + ((size_t)(KKM_MAX_K + 1) * 4 + 15) / 16 * 16;
+constexpr size_t T3_STREAM_EXTRA = T3_STREAM_RING_OFF + CH_RING_BYTES;
 constexpr size_t T3_STREAM_SMEM = (size_t)T2_STAGES * T2_STAGE_BYTES + T3_STREAM_EXTRA + 1024 + 128;
 
 template <int KIND>
@@ -282,32 +283,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CH_THREADS, 1)
                       const float *__restrict__ norms, const float *__restrict__ rscale,
                       const float *__restrict__ snorms, const float *__restrict__ srscale,
                       const int32_t *__restrict__ pos, int64_t npos, const int32_t *__restrict__ seg_g, int k,
-                      KappaParams kp, T2StreamSched sc, float fx, long long *__restrict__ Sx) {
+                      KappaParams kp, T2StreamSched sc, bool dyn, int32_t *__restrict__ work, float fx,
+                      long long *__restrict__ Sx) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *extra;
   const ChSmem s = ch_carve(smem_raw, (uint32_t)T3_STREAM_EXTRA, &extra);
   float *colc = reinterpret_cast<float *>(extra);
   int32_t *seg = reinterpret_cast<int32_t *>(extra + CH_EPI_WARPS * CH_COLC_BYTES);
+  const ChRing ring = ch_ring_carve(extra + T3_STREAM_RING_OFF, dyn, sc.nitems, work);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cr = cluster_ctarank();
   const bool fp16 = rscale != nullptr;
   for (int c = threadIdx.x; c <= k; c += blockDim.x) seg[c] = seg_g[c];
-  ch_setup(s, warp, 2 * CH_EPI_WARPS);  // (its cluster barrier also publishes seg)
+  ch_ring_init(ring);
+  ch_setup(s, warp, 2 * CH_EPI_WARPS);  // (its cluster barrier also publishes seg and the ring's init)
   const uint32_t tmem_base = *s.tmem_slot;
-  if (warp < 2) {
-    ch_producer_mma(sc, s, warp, lane, cr, &ta_hi, &ta_lo, &tb_hi, &tb_lo, nkb, nch, idesc, tmem_base, sc.hint);
+  if (warp == 0) {
+    if (lane == 0) ch_ring_producer(sc, ring, s, cr, &ta_hi, &ta_lo, &tb_hi, &tb_lo, nkb);
+  } else if (warp == 1) {
+    if (lane == 0 && cr == 0) ch_ring_mma(sc, ring, s, nkb, nch, idesc, tmem_base);
   } else {
     const int e = warp - 2;
     const int quarter = warp & 3;
     const int colq = e >> 2;
     float *cn = colc + e * (2 * CH_COLS);
     const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colq * CH_COLS);
-    const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     int64_t chain = 0;
-    for (int64_t u = cl; u < sc.nitems; u += ncl) {
-      int tm, sp;
-      sc.unit(u, tm, sp);
-      const int tn0 = sp * sc.tps, tn1 = min(sc.tiles_n, tn0 + sc.tps);
+    for (int64_t iu = 0;; ++iu) {
+      const int64_t u = ring.take(iu, lane == 0);
+      if (u < 0) break;
+      int tm, tn0, ntn;
+      sc.unit(u, tm, tn0, ntn);
+      const int tn1 = tn0 + ntn;
       const int64_t r = (int64_t)tm * T2_BM + (int64_t)cr * 128 + quarter * 32 + lane;  // A-set row
       const bool row_ok = r < nloc;
       const int64_t i = sc.row0 + r;
@@ -357,7 +364,7 @@ inline int tc3_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
                              const uint16_t *Slo, bool fp16, int64_t rows_a, int64_t rows_b, int64_t dp, int64_t nB,
                              int64_t b0, int64_t row0, int64_t nloc, const float *norms, const float *rscale,
                              const float *snorms, const float *srscale, const int32_t *pos, int64_t npos,
-                             const int32_t *seg, int k, const KappaParams &kp, int splits, double fx,
+                             const int32_t *seg, int k, const KappaParams &kp, double fx,
                              long long *Sx, cudaStream_t st, int64_t *launches, int ckb = 0) {
   if (!tc_encode_fn()) {
     TcGemm tmp;
@@ -386,15 +393,28 @@ inline int tc3_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
     tc_err_slot() = "tc3_stream_launch: k > KKM_MAX_K";
     return 1;
   }
+  if (!g.work) {  // the dynamic schedule's two counters (zero between launches: the kernel resets them)
+    if (cudaMalloc((void **)&g.work, 16) != cudaSuccess || cudaMemset(g.work, 0, 16) != cudaSuccess) {
+      g.work = nullptr;
+      tc_err_slot() = "cudaMalloc (stream unit counter) failed";
+      return 1;
+    }
+  }
+  // units of W column tiles in G-row supertiles (T2StreamSched), taken dynamically: the ~74 units
+  // in flight cover ~G A tiles and a few W-groups of B tiles (as ssym.cuh; KKM_TS_G / KKM_TS_W /
+  // KKM_SSYM_STATIC for A/B runs)
   T2StreamSched sc;
   sc.tiles_m = (int)((nloc + T2_BM - 1) / T2_BM);
   sc.tiles_n = (int)((nB + 255) / 256);
-  sc.nsplit = std::max(1, std::min(splits, sc.tiles_n));
-  sc.tps = (sc.tiles_n + sc.nsplit - 1) / sc.nsplit;
-  sc.nitems = (int64_t)sc.tiles_m * sc.nsplit;
+  sc.G = 32;
+  sc.W = 16;
+  if (const char *e = std::getenv("KKM_TS_G")) sc.G = std::max(1, std::atoi(e));
+  if (const char *e = std::getenv("KKM_TS_W")) sc.W = std::max(1, std::atoi(e));
+  sc.ncb = (sc.tiles_n + sc.W - 1) / sc.W;
+  sc.nitems = (int64_t)sc.tiles_m * sc.ncb;
   sc.row0 = row0;
-  sc.hint = 1;         // L2 evict_last on the operand loads
-  sc.split_major = 0;  // tile-major: the pairs on one row tile's splits share its A operand in L2
+  sc.hint = 1;  // L2 evict_last on the operand loads
+  const bool dyn = std::getenv("KKM_SSYM_STATIC") == nullptr;
   const int64_t clusters = sc.nitems < g.num_sms / 2 ? sc.nitems : g.num_sms / 2;
   const unsigned grid = (unsigned)(2 * clusters);
   const int nkb = (int)(dp / TC_BK);
@@ -406,7 +426,7 @@ inline int tc3_stream_launch(TcStream &g, const uint16_t *Xhi, const uint16_t *X
     if (ensure_smem_attr((const void *)tc3_stream_kernel<KIND>, T3_STREAM_SMEM) != cudaSuccess) return 1;
     tc3_stream_kernel<KIND><<<grid, CH_THREADS, T3_STREAM_SMEM, st>>>(
         g.a_hi, g.a_lo, g.b_hi, g.b_lo, t2_idesc(fp16), nkb, nch, nB, b0, nloc, norms, rs, snorms, srs, pos, npos, seg,
-        k, kp, sc, (float)fx, Sx);
+        k, kp, sc, dyn, g.work, (float)fx, Sx);
     return 0;
   });
   if (rc) {
