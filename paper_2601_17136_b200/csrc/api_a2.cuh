@@ -153,10 +153,7 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
     if (nl32) CK(ensure_smem_attr((const void *)spmm_tc_kernel<32>, TsCfg<32>::SMEM));
     else CK(ensure_smem_attr((const void *)spmm_tc_kernel<16>, TsCfg<16>::SMEM));
     long long *Sx = h->tSfix;
-    if (h->p2p) {  // this epoch's half of the own exchange buffer (the other half may still be read)
-      ++h->epoch;
-      Sx = (long long *)(h->xbuf + (h->epoch & 1) * (size_t)P.npad * k * 8);
-    } else if (h->lsa) {  // alternate parities of the symmetric window: a peer may still read the
+    if (h->lsa) {  // alternate parities of the symmetric window: a peer may still read the
       h->ls_par ^= 1;     // other one (its reads end before it reaches the next cross-rank barrier)
       Sx = (long long *)(h->lsbuf + (size_t)h->ls_par * h->ls_sb);
       h->tSfix = Sx;
@@ -182,13 +179,6 @@ int launch_spmm_sym(kkm_ctx *h, const int32_t *labels, const double **s_out) {
       }
     }
     a2_mark(h);
-    if (h->p2p) {  // publish; run_cnorm's finalize sums the ranks' S over NVLink
-      peer_signal_kernel<<<1, 1, 0, h->st>>>(
-          (unsigned long long *)(h->xbuf + 2 * (size_t)P.npad * k * 8), h->epoch);
-      CKL();
-      *s_out = nullptr;
-      return KKM_OK;
-    }
     if (h->lsa && h->ls_fused_next) {  // update_grid_kernel<true> sums the ranks' S itself
       *s_out = nullptr;
       return KKM_OK;

@@ -15,13 +15,9 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
   const int nr = P.repl ? 1 : P.nranks, r = P.repl ? 0 : P.rank;  // replicated a3: one "rank"
   if (P.a3fix && P.a_n > 0) {  // int64 S in, c and J from the last block (same sums as below)
     const int fth = fin_threads(P.k);
-    const A3Peers peers = h->p2p ? A3Peers{h->xtable, P.nranks, (int64_t)((h->epoch & 1) * (size_t)P.npad * P.k * 8),
-                                           (int64_t)h->xflag_off, h->epoch, h->p2p_timeout_ns,
-                                           (int *)(h->xbuf + h->xflag_off + 64)}
-                                 : A3Peers{nullptr, 0, 0, 0, 0ull, 0ull, nullptr};
     finalize_kernel<<<P.nfin, fth, (size_t)k1 * fth * 8, h->st>>>(
         nullptr, 1, P.a_n, P.npad, P.k, sizes, labels + P.a_row0, h->diag, P.rows_per_block, E_out, h->blockpart,
-        h->tSfix, h->tfx_inv, A3Fused{h->a3ctr, sizes, cnorm_out, J_out, sizes_next, changed_out}, peers);
+        h->tSfix, h->tfx_inv, A3Fused{h->a3ctr, sizes, cnorm_out, J_out, sizes_next, changed_out});
     CKL();
     return KKM_OK;
   }
@@ -48,7 +44,7 @@ int run_cnorm(kkm_ctx *h, const double *S, int nsplit, int64_t rows_pad, double 
 // With the NVLink peer-memory window (h->lsa, in the fit loop) the launch is the distributed
 // variant: own rows only, S summed over the ranks while read, labels / sizes / changed stored into
 // every rank's copies, three cross-rank arrivals.
-bool use_update_grid(const kkm_ctx *h) { return h->ug_grid > 0 && !h->p2p; }
+bool use_update_grid(const kkm_ctx *h) { return h->ug_grid > 0; }
 int run_update_grid(kkm_ctx *h, double *J_out, unsigned long long *changed_out) {
   const Plan &P = h->P;
   const int nx = h->cur ^ 1;

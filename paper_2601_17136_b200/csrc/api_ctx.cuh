@@ -59,16 +59,6 @@ struct kkm_ctx {
   double *colsum = nullptr, *Sfin = nullptr;
   int32_t *work = nullptr;  // item schedulers: [0, 2) spmm_tc, [2, 4) ssym (zero between launches)
   unsigned *a3ctr = nullptr;  // finalize's last-block counter (zero between launches)
-  // peer-memory exchange of S (16-bit bands, replicated a3, several ranks): own IPC buffer
-  // [2 epochs][k][npad] int64 + flag + peer table; peers' buffers mapped with cudaIpcOpenMemHandle
-  bool p2p = false;
-  uint8_t *xbuf = nullptr;
-  std::vector<void *> xpeers;  // opened peer mappings (closed in destroy)
-  const uint8_t **xtable = nullptr;  // device [nranks] bases (inside xbuf)
-  size_t xflag_off = 0;              // byte offset of the epoch flag in every exchange buffer
-                                     // (+64: this rank's timed-out word, checked by check_p2p)
-  unsigned long long epoch = 0;
-  unsigned long long p2p_timeout_ns = 0;
   // Distributed a3/a4 over NVLink peer memory (16-bit bands, replicated plan, several ranks;
   // api_exchange.cuh setup_lsa): an NCCL symmetric window per rank [2 parities of k x npad int64 S |
   // 2 label buffers | 2 size histograms | changed counters | rank partials | flag page], mapped by

@@ -433,22 +433,6 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
       return KKM_OK;
     }();
   }
-  // (p2p needs the a3 that reads the int64 S itself: a3fix; the single-CTA fused path reads fp64 S)
-  // Opt-in (KKM_P2P=1): measured only 2 % faster than the NCCL allreduce at 4 GPUs, and
-  // every rank reads all (P - 1) peers' whole S, so it is limited to P <= KKM_P2P_MAX_RANKS (4).
-  // The decision is agreed by all ranks (an allreduce of the local wish) before the collective
-  // setup, so ranks with different environments cannot issue mismatched collectives.
-  if (rc == KKM_OK && P.a3fix && P.repl && P.nranks > 1 && P.k <= 16) {  // (finalize's peer reads: k <= 16)
-    int p2p_max = 4;
-    if (const char *e = std::getenv("KKM_P2P_MAX_RANKS")) p2p_max = std::atoi(e);
-    const char *want_env = std::getenv("KKM_P2P");
-    int want = (want_env && std::atoi(want_env) == 1 && P.nranks <= p2p_max) ? 1 : 0;
-    double tmo = 600.0;  // seconds a finalize waits for a peer's flag before it reports a timeout
-    if (const char *e = std::getenv("KKM_P2P_TIMEOUT_S")) tmo = std::max(1.0, std::atof(e));
-    h->p2p_timeout_ns = (unsigned long long)(tmo * 1e9);
-    rc = agree_min(h, &want);
-    if (rc == KKM_OK && want) rc = setup_p2p(h);
-  }
   if (rc == KKM_OK && P.a3fix && P.k <= UG_MAX_K && P.a_n > 0) {  // a3 + a4 as one cooperative launch
     int coop = 0, per_sm = 0, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -463,7 +447,7 @@ int kkm_init(kkm_handle *out, const kkm_params *p, const float *X_local, int64_t
   // update (0.398 vs 0.404 ms at config 2; three cross-rank arrivals cost what the allreduce did)
   // and +50 ms of window registration per handle, so the default stays on NCCL. Every rank
   // evaluates the same condition (same plan, env) and agrees before the collective setup.
-  if (rc == KKM_OK && P.repl && P.nranks > 1 && P.nranks <= LSA_MAX_RANKS && !h->p2p && P.a3fix &&
+  if (rc == KKM_OK && P.repl && P.nranks > 1 && P.nranks <= LSA_MAX_RANKS && P.a3fix &&
       P.k <= UG_MAX_K) {
     int want = 0;
     if (const char *e = std::getenv("KKM_LSA")) want = h->ug_grid > 0 && std::atoi(e) == 1;
@@ -579,7 +563,6 @@ int kkm_fit(kkm_handle h, int32_t *iters_run, double *J_trace, int64_t *changed)
   CK(cudaMemcpyAsync(J.data(), h->J, (size_t)(t + 1) * 8, cudaMemcpyDeviceToHost, h->st));
   if (t > 0) CK(cudaMemcpyAsync(ch.data(), h->changed, (size_t)t * 8, cudaMemcpyDeviceToHost, h->st));
   CKR(sync_stream(h));
-  CKR(check_p2p(h));
   CKR(check_lsa(h));
 #ifdef KKM_EXP_LSA_STAMPS
   if (h->lsa) {
@@ -638,7 +621,6 @@ int kkm_objective(kkm_handle h, double *J) {
   h->cnorm2_valid = true;
   CK(cudaMemcpyAsync(J, slot, 8, cudaMemcpyDeviceToHost, h->st));
   CKR(sync_stream(h));
-  CKR(check_p2p(h));
   return KKM_OK;
 }
 
@@ -869,26 +851,6 @@ int kkm_destroy(kkm_handle h) {
     ncclDevCommDestroy(h->comm, &h->lsdev);
     ncclCommWindowDeregister(h->comm, h->lswin);
     ncclMemFree(h->lsbuf);
-    cudaGetLastError();
-  }
-  if (h->xbuf) {
-    // no rank frees its exchange buffer while a peer may still read it: raise the own flag to
-    // DONE (after the stream is idle) and wait, bounded, for every peer's DONE -- no NCCL here, so
-    // destroy stays safe after the communicator is gone or when handles die in any order
-    const unsigned long long done = ~0ull;
-    cudaMemcpy(h->xbuf + h->xflag_off, &done, 8, cudaMemcpyHostToDevice);
-    const auto t0 = std::chrono::steady_clock::now();
-    bool all_done = true;
-    for (void *q : h->xpeers) {
-      unsigned long long v = 0;
-      while (cudaMemcpy(&v, (uint8_t *)q + h->xflag_off, 8, cudaMemcpyDeviceToHost) == cudaSuccess && v != done &&
-             std::chrono::steady_clock::now() - t0 < std::chrono::seconds(20))
-        std::this_thread::sleep_for(std::chrono::microseconds(200));
-      all_done = all_done && v == done;
-    }
-    for (void *q : h->xpeers) cudaIpcCloseMemHandle(q);
-    // a peer that never reported DONE may still read this buffer: keep it (leak) rather than free
-    if (all_done) cudaFree(h->xbuf);
     cudaGetLastError();
   }
   delete h;

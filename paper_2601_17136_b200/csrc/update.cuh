@@ -38,37 +38,6 @@ struct A3Fused {
   unsigned long long *changed_out;
 };
 
-// Peer-memory exchange of the int64 S (replicated a3, §6): every rank's spmm_tc writes its own
-// S into its own IPC buffer and raises its epoch flag; finalize waits for all flags and sums the
-// ranks' S in rank order while reading them over NVLink -- the allreduce fused into the a3 read.
-struct A3Peers {
-  const uint8_t *const *bases;  // [nranks] every rank's exchange buffer, mapped here (device table)
-  int nranks;
-  int64_t s_off;                // byte offset of this epoch's S in a buffer
-  int64_t flag_off;             // byte offset of the epoch flag in a buffer
-  unsigned long long epoch;
-  unsigned long long timeout_ns;  // bound on the wait for a peer's flag (globaltimer)
-  int *timed_out;                 // set to 1 when a wait ran out (the host checks it and poisons)
-};
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Raises this rank's flag to `epoch` after its S is complete (stream order: after spmm_tc).
-__global__ void peer_signal_kernel(unsigned long long *flag, unsigned long long epoch) {
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(epoch) : "memory");
-}
-
 __device__ __forceinline__ void cnorm_reduce_last(const double *__restrict__ blockpart, int nblocks, int k,
                                                   const A3Fused &f) {
   // = cnorm_local_kernel (one warp per c, lanes over blocks, fixed shuffle tree) + cnorm_final_kernel
@@ -105,53 +74,18 @@ __global__ void __launch_bounds__(128) finalize_kernel(
     const int32_t *__restrict__ sizes, const int32_t *__restrict__ cl_local,
     const double *__restrict__ diag, int64_t rows_per_block, double *__restrict__ E,
     double *__restrict__ blockpart, const long long *__restrict__ Sfix = nullptr, double inv = 1.0,
-    A3Fused fin = A3Fused{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr},
-    A3Peers peers = A3Peers{nullptr, 0, 0, 0, 0ull, 0ull, nullptr}) {
+    A3Fused fin = A3Fused{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}) {
   extern __shared__ double sacc[];  // [(k + 1)][blockDim.x]
   __shared__ unsigned s_last;
   const int T = blockDim.x;
   const int t = threadIdx.x;
-  if (peers.bases) {  // wait for every rank's S of this epoch; bounded: a lost peer raises timed_out
-    if (t < peers.nranks) {  // (the kernel then finishes on whatever S it reads; the host poisons the handle)
-      const unsigned long long *flag =
-          reinterpret_cast<const unsigned long long *>(peers.bases[t] + peers.flag_off);
-      const unsigned long long t0 = globaltimer_ns();
-      while (ld_acquire_sys(flag) < peers.epoch)
-        if (globaltimer_ns() - t0 > peers.timeout_ns) {
-          atomicExch(peers.timed_out, 1);
-          break;
-        }
-    }
-    __syncthreads();
-  }
   for (int c = 0; c <= k; ++c) sacc[c * T + t] = 0.0;
   const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
   const int64_t re = rb + rows_per_block < nrows ? rb + rows_per_block : nrows;
   for (int64_t i = rb + t; i < re; i += T) {
     const int li = cl_local[i];
     double zi = 0.0;
-    if (peers.bases && k <= 16) {  // S = the ranks' int64 S summed in rank order (exact), over NVLink
-      long long sv[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) sv[c] = 0ll;
-      for (int r = 0; r < peers.nranks; ++r) {
-        const long long *Sr = reinterpret_cast<const long long *>(peers.bases[r] + peers.s_off);
-        long long v[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = c < k ? __ldcv(Sr + (int64_t)c * rows_pad + i) : 0ll;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) sv[c] += v[c];
-      }
-#pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c < k) {
-          const double s = 0.0 + (double)sv[c] * inv;
-          const int32_t sz = sizes[c];
-          const double e = sz > 0 ? s / (double)sz : 0.0;
-          E[i * k + c] = e;
-          if (c == li) zi = e;
-        }
-    } else if (Sfix && k <= 16) {  // all k loads in flight first (the caller guarantees k <= 16 here)
+    if (Sfix && k <= 16) {  // all k loads in flight first (the caller guarantees k <= 16 here)
       long long sv[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) sv[c] = c < k ? Sfix[(int64_t)c * rows_pad + i] : 0ll;

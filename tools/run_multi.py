@@ -35,20 +35,16 @@ cases += [("har200k", 3001, 6, kkm.PATH_MATERIALIZE, 1, dict(symmetric=kkm.SYM_O
           ("mnist60k", 2500, 12, kkm.PATH_MATERIALIZE, 1, dict(incremental=True)),
           ("mnist60k", 2500, 12, kkm.PATH_STREAM, 1, dict(incremental=True)),
           ("rings", 1000, 60, kkm.PATH_MATERIALIZE, 1, dict(stop_on_no_change=True)),
-          # n > 32768: the a3 that reads the int64 S itself and, on several ranks, the peer-memory
-          # exchange of S over NVLink (setup_p2p); checked against the 1-GPU run (bitwise), no oracle
+          # n > 32768: the one-launch a3/a4 over the int64 S (with KKM_LSA=1 in the environment:
+          # the distributed update over NCCL symmetric windows); checked against the 1-GPU run
+          # (bitwise), no oracle
           ("mnist60k", 36001, 6, kkm.PATH_MATERIALIZE, 1, {}),
-          ("mnist60k", 36001, 6, kkm.PATH_MATERIALIZE, 1, dict(p2p=True)),
           ("rings", 1000, 60, kkm.PATH_STREAM, 1, dict(stop_on_no_change=True, incremental=True))]
 for name, n, iters, path, g, opt in cases:
     X, cfg = synth.make_config(name, n=n)
     args = (cfg["kind"], cfg["gamma"], cfg["coef0"], cfg["degree"])
     r0, r1 = kkm.shard_begin(n, rank, world), kkm.shard_begin(n, rank + 1, world)
     opt = dict(opt)
-    if opt.pop("p2p", False):  # the opt-in peer-memory exchange (read by kkm_init, agreed by all ranks)
-        os.environ["KKM_P2P"] = "1"
-    else:
-        os.environ.pop("KKM_P2P", None)
     h = kkm.KernelKMeans(torch.from_numpy(X[r0:r1]).cuda(), n, cfg["k"], *args, max_iter=iters,
                          rank=rank, nranks=world, comm=comm, path=path, grid_rows=g, **opt)
     it, J, ch = h.fit()
