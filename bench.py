@@ -111,7 +111,12 @@ def run_reference(args):
         return 0
     X, cfg = synth.make_config(WORKLOAD)
     iters = args.iters or cfg["iters"]
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores()))
+    # rank 0 runs alone (the other ranks exit above), so it takes every host core: torchrun's
+    # OMP_NUM_THREADS=1 default (set against oversubscription) is replaced before the oracle's
+    # OpenMP runtime loads; an explicit setting on a 1-process run is kept
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or "OMP_NUM_THREADS" not in os.environ:
+        os.environ["OMP_NUM_THREADS"] = str(cores())
+    threads = int(os.environ["OMP_NUM_THREADS"])
     for _ in range(args.warmup):
         oracle_sample(X, cfg, args.ref_rows)
     samples = [oracle_sample(X, cfg, args.ref_rows, seed=s) for s in range(args.steps)]
@@ -119,7 +124,7 @@ def run_reference(args):
     kb = statistics.mean(s["k_build_s"] for s in samples)
     total = kb + iters * spi
     sample = (f"{args.ref_rows} of {cfg['n']} rows per step: exact fp64 K rows + one E/c/D/argmin "
-              f"pass, extrapolated x n/{args.ref_rows} (OMP threads={os.environ['OMP_NUM_THREADS']})")
+              f"pass, extrapolated x n/{args.ref_rows} (OMP threads={threads})")
     line = {
         "impl": "reference", "metric": METRIC, "value": spi, "unit": "s/iteration",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -128,7 +133,7 @@ def run_reference(args):
         "data": "synthetic", "total_clustering_s": total,
         "config": bench_config(cfg, iters),
         "parallelism": "cpu-oracle",
-        "cpu_baseline": {"value": spi, "unit": "s/iteration", "cores": cores(), "kind": "oracle",
+        "cpu_baseline": {"value": spi, "unit": "s/iteration", "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": spi, "unit": "s/iteration", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -530,10 +535,12 @@ def run_ours(args):
             "final_J": float(J_last[-1]),
         }
         if world == 1 and not args.no_cpu_baseline:
+            os.environ.setdefault("OMP_NUM_THREADS", str(cores()))  # (before the oracle's OpenMP loads)
+            threads = int(os.environ["OMP_NUM_THREADS"])
             X, full_cfg = synth.make_config(WORKLOAD)
             s = oracle_sample(X, full_cfg, args.ref_rows)
             line["cpu_baseline"] = {
-                "value": s["sec_per_iter"], "unit": "s/iteration", "cores": cores(), "kind": "oracle",
+                "value": s["sec_per_iter"], "unit": "s/iteration", "cores": threads, "kind": "oracle",
                 "sample": (f"{args.ref_rows} of {n} rows: exact fp64 K rows + one E/c/D/argmin pass, "
                            f"extrapolated x n/{args.ref_rows}; K build extrapolated {s['k_build_s']:.1f} s"),
                 "total_clustering_s": s["k_build_s"] + iters * s["sec_per_iter"]}
